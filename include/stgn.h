@@ -1,0 +1,233 @@
+/*
+ * stgn.h — C ABI of the B200-native StreamTGN incremental inference path.
+ *
+ * Two plug-in points, matching the two places the reference dispatches
+ * this path (reference = /root/reference/pkg/src/streamtgn, "S/"):
+ *
+ *  1. Engine level — replaces IncrementalEngine (S/engine.py:155-453):
+ *       stgn_engine_create / _destroy       <- IncrementalEngine.__init__ (S/engine.py:156-166,
+ *                                               S/engine_base.py:62-74)
+ *       stgn_engine_bind                    <- the state tables of S/state.py:23-127 and
+ *                                               S/graph_store.py:102-152, held on the device
+ *       stgn_engine_process_batch           <- IncrementalEngine.process_batch (S/engine.py:400-438)
+ *       stgn_engine_process_batch_dev       <- same, inputs already resident on the device
+ *       stgn_engine_rebuild                 <- IncrementalEngine.rebuild_nodes (S/engine.py:385-396)
+ *       stgn_engine_full_reference          <- IncrementalEngine.full_reference (S/engine.py:374-381)
+ *       stgn_engine_affected                <- IncrementalEngine.last_affected (S/engine.py:417-418)
+ *  2. Operator level — replaces kernels.pipeline_many (S/kernels/__init__.py:42-44):
+ *       stgn_pipeline_many
+ *
+ * Conventions: plain pointers and sizes; every device buffer is allocated
+ * by the caller (the Python shim uses PyTorch) and only borrowed here; the
+ * engine handle owns nothing but a few pinned host staging buffers and its
+ * CUDA graphs. `stream` is a cudaStream_t passed as void*. Functions
+ * return STGN_OK or an error code; the Python shim maps codes onto the
+ * reference's exception classes.
+ */
+#ifndef STGN_H
+#define STGN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STGN_OK            0
+#define STGN_ERR_INVALID   1  /* bad dims/config/argument   -> ConfigError / KernelInputError */
+#define STGN_ERR_BOUNDS    2  /* node id / edge id range    -> InputError                     */
+#define STGN_ERR_CUDA      3  /* CUDA runtime failure       -> RuntimeError                   */
+#define STGN_ERR_CAPACITY  4  /* bound tables too small     -> host grows + rebinds           */
+#define STGN_ERR_ORDER     5  /* timestamps decrease        -> MonotonicityError              */
+
+#define STGN_AGG_MEAN 0
+#define STGN_AGG_LAST 1
+#define STGN_AGG_SUM  2
+
+#define STGN_REBUILD_NEVER    0
+#define STGN_REBUILD_FIXED    1
+#define STGN_REBUILD_ADAPTIVE 2
+
+#define STGN_SCOPE_AFFECTED 0  /* recompute every node of A (the reference's literal exact mode) */
+#define STGN_SCOPE_DIRECT   1  /* recompute V_direct only; value-identical when window = inf     */
+
+/* Model widths; same meaning as the reference Dims (S/config.py:11-55). */
+typedef struct {
+  int32_t d_s, d_e, d_t, d_x, d_m, d_k, heads, layers;
+} stgn_dims;
+
+/* Run options; same meaning as RunConfig (S/config.py:61-103). */
+typedef struct {
+  int32_t fanout;            /* L */
+  int32_t aggregator;        /* STGN_AGG_* */
+  int32_t rebuild;           /* STGN_REBUILD_* */
+  int32_t rebuild_interval;
+  double  gamma, delta_max, alpha;
+  double  window;            /* +inf = no temporal window */
+  int32_t scope;             /* STGN_SCOPE_* */
+  int32_t max_batch;         /* capacity of the per-batch scratch (edges) */
+} stgn_config;
+
+/*
+ * Device-resident weights, float32, packed by the host shim (row-major):
+ *   wq    [K][q_in][H*d_k]      from w_q (K,H,q_in,d_k)
+ *   wkt   [K][H][d_k][k_in]     from w_k (K,H,k_in,d_k), transposed per head
+ *   wv    [K][H][k_in][d_k]     from w_v
+ *   wo    [K][H*d_k][d]         from w_o
+ *   wmsg  [2][msg_in][d_m]      from w_msg_src / w_msg_dst (transposed)
+ *   bmsg  [2][d_m]
+ *   wgru  [3][d_m][d_s]         from w_z, w_r, w_h (transposed)
+ *   ugru  [3][d_s][d_s]         from u_z, u_r, u_h (transposed)
+ *   bgru  [3][d_s]
+ *   wpred [2*d]   bpred (double, host)
+ *   omega [d_t/2] double;  phi0 [d_t] float
+ */
+typedef struct {
+  const float *wq, *wkt, *wv, *wo;
+  const float *wmsg, *bmsg, *wgru, *ugru, *bgru;
+  const double *wpred;
+  const double *omega;
+  const float *phi0;
+  double bpred;
+} stgn_weights;
+
+/* Persistent control block (device). */
+typedef struct {
+  int64_t tau;               /* drift scheduler clock (S/drift.py:30) */
+  int64_t cum_count;         /* |cumulative affected set| */
+  uint32_t cum_gen;          /* generation stamp of cum_mark */
+  uint32_t pad0;
+  int64_t reserved[6];
+} stgn_ctl;
+
+/*
+ * Device state tables (all caller-allocated). Row strides:
+ *   ld_s = round_up(d_s,4), ld_d = round_up(d,4), ld_e = round_up(max(d_e,1),4).
+ * The ring holds, per node, the L newest adjacency entries (newest at
+ * ring_head, walking forward mod L); ring_ccnt is the neighbour-cache
+ * prefix length (-1 = node not cached, S/state.py:154-171). Frozen
+ * payload stacks live in the ring slot: ring_pay[node][layer][slot][ld_d].
+ */
+typedef struct {
+  int64_t cap_nodes, cap_edges, gpow_len;
+  float    *mem;        /* [cap_nodes][ld_s]       S/state.py:23-48 */
+  double   *last;       /* [cap_nodes]                                */
+  int64_t  *version;    /* [cap_nodes]                                */
+  float    *h;          /* [cap_nodes][K][ld_d]    S/state.py:91-127  */
+  uint8_t  *valid;      /* [cap_nodes]                                */
+  double   *valid_at;   /* [cap_nodes]                                */
+  int32_t  *ring_cnt, *ring_head, *ring_ccnt;   /* [cap_nodes] */
+  int32_t  *ring_nbr;   /* [cap_nodes][L] */
+  int64_t  *ring_eid;   /* [cap_nodes][L] */
+  double   *ring_t;     /* [cap_nodes][L] */
+  float    *ring_pay;   /* [cap_nodes][K][L][ld_d] */
+  float    *ring_feat;  /* [cap_nodes][L][ld_e] */
+  uint32_t *amark, *dmark;                      /* [cap_nodes] batch stamps */
+  int32_t  *nodecnt, *nodeadj, *nodefill, *nodeoff;  /* [cap_nodes] scratch */
+  double   *drift_acc;  /* [cap_nodes] */
+  int64_t  *drift_touched; /* [cap_nodes] */
+  uint32_t *cum_mark;   /* [cap_nodes] */
+  int32_t  *cum_list;   /* [cap_nodes] */
+  int32_t  *e_src, *e_dst;  /* [cap_edges]   append-only temporal store */
+  double   *e_t;            /* [cap_edges] */
+  float    *e_feat;         /* [cap_edges][ld_e] */
+  int64_t  *e_prev;         /* [2*cap_edges] previous entry of the same node, -1 none */
+  int64_t  *adj_head;       /* [cap_nodes] newest entry (2*eid+side), -1 none */
+  int64_t  *adj_deg;        /* [cap_nodes] */
+  double   *gpow;           /* [gpow_len] gamma^k, k = 0..gpow_len-1 (host-computed) */
+  stgn_ctl *ctl;
+  uint8_t  *scratch;        /* stgn_scratch_bytes(...) bytes */
+} stgn_state;
+
+/* Per-batch report written by process_batch (host memory). Counter
+ * names follow S/runner.py:73-77 and S/engine.py:432-433. */
+typedef struct {
+  int64_t direct, affected;
+  int64_t nbr_hit, nbr_miss;
+  int64_t entries_affected, entries_direct;   /* sum of list lengths (MAC tallies) */
+  int64_t rebuild_kind;                       /* 0 none, 1 partial, 2 full */
+  int64_t rebuild_nodes;
+  int64_t entries_rebuild;
+  int64_t tau, cum_count;
+  int64_t changed;                            /* nodes with a non-empty change record */
+  double  global_drift;
+  int64_t reserved[3];
+} stgn_report;
+
+typedef struct stgn_engine stgn_engine;
+
+/* Bytes of scratch the engine needs for these capacities. */
+int64_t stgn_scratch_bytes(const stgn_dims* dims, const stgn_config* cfg, int64_t cap_nodes);
+
+int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engine** out);
+int stgn_engine_destroy(stgn_engine* eng);
+int stgn_engine_set_weights(stgn_engine* eng, const stgn_weights* w);
+/* (Re)bind state tables after allocation or growth; drops cached graphs. */
+int stgn_engine_bind(stgn_engine* eng, const stgn_state* st);
+
+/*
+ * One batch, host buffers in, host buffers out (the end-to-end path).
+ * src/dst: int32 node ids; t: float64 non-decreasing and >= t_now;
+ * feat: float32 [B][d_e] (row stride d_e). m0 = committed edge count,
+ * batch_index = 1-based index of this batch, node_count = max(n seen, hint)
+ * after this batch. preds_out: float64 [B]. Blocks until done.
+ */
+int stgn_engine_process_batch(stgn_engine* eng, int32_t B, const int32_t* src,
+                              const int32_t* dst, const double* t, const float* feat,
+                              int64_t m0, int64_t batch_index, int64_t node_count,
+                              double* preds_out, stgn_report* rep, void* stream);
+
+/* Same, inputs already on the device (src/dst int32, t f64, feat f32 [B][ld_e]);
+ * preds_dev f64 [B] stays on the device; the report is copied to rep (host)
+ * only if rep != NULL (that forces a stream sync). */
+int stgn_engine_process_batch_dev(stgn_engine* eng, int32_t B, const int32_t* src_dev,
+                                  const int32_t* dst_dev, const double* t_dev,
+                                  const float* feat_dev, int64_t m0, int64_t batch_index,
+                                  int64_t node_count, double* preds_dev, stgn_report* rep,
+                                  void* stream);
+
+/* Exact recompute of `ids` (host int32 list, or NULL = all of 0..node_count-1)
+ * with current memory; fills missing neighbour caches from the store first.
+ * valid_at_value is written to valid_at. Returns the count in *count. */
+int stgn_engine_rebuild(stgn_engine* eng, const int32_t* ids, int64_t n_ids,
+                        int64_t node_count, double valid_at_value, int64_t* count,
+                        void* stream);
+
+/* Read-only full recompute; final-layer rows into out_dev f32 [node_count][ld_d]. */
+int stgn_engine_full_reference(stgn_engine* eng, int64_t node_count, float* out_dev,
+                               void* stream);
+
+/* Copy the last batch's direct / affected node lists (unordered) to host
+ * buffers of capacity cap; *n_direct / *n_affected receive the sizes. */
+int stgn_engine_affected(stgn_engine* eng, int32_t* direct, int32_t* affected, int64_t cap,
+                         int64_t* n_direct, int64_t* n_affected, int32_t* change_sizes,
+                         void* stream);
+
+/* Copy the last batch's prediction-time final-layer embeddings of the
+ * direct nodes (same order as stgn_engine_affected's direct list):
+ * host float32 [n_direct][d]. */
+int stgn_engine_pred_embeddings(stgn_engine* eng, float* out, int64_t n_direct, void* stream);
+
+/*
+ * Operator level: the reference's pipeline_many on flat inputs, float32
+ * device buffers in the reference layouts (row-major):
+ *   qbase (N,d) offsets (N+1,int64) payload (E,K,d) feat (E,d_e) dt (E,f64)
+ *   omega (d_t/2,f64) phi0 (d_t) wq (K,H,q_in,d_k) wk/wv (K,H,k_in,d_k) wo (K,H*d_k,d)
+ * Outputs (caller-allocated): out (N,K,d) scores (E,K,H) values (E,K,H,d_k)
+ *   maxlog/zsum (N,K,H) qvecs (N,K,H,d_k). scores are in the max-scaled
+ * frame; rows with no entries give out = 0, maxlog = -inf, zsum = 0.
+ */
+int stgn_pipeline_many(const stgn_dims* dims, int64_t N, int64_t E, const float* qbase,
+                       const int64_t* offsets, const float* payload, const float* feat,
+                       const double* dt, const double* omega, const float* phi0,
+                       const float* wq, const float* wk, const float* wv, const float* wo,
+                       float* out, float* scores, float* values, float* maxlog, float* zsum,
+                       float* qvecs, void* stream);
+
+/* Library version string and the sm architecture it was built for. */
+const char* stgn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STGN_H */

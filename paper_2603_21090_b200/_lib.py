@@ -1,0 +1,129 @@
+"""ctypes binding of the C ABI in include/stgn.h (the in-tree _stgn.so).
+
+There is no fallback: if the library or a GPU is missing, `lib()` raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .config import ConfigError
+from .edges import InputError, KernelInputError, MonotonicityError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_stgn.so")
+
+STGN_OK, STGN_ERR_INVALID, STGN_ERR_BOUNDS, STGN_ERR_CUDA, STGN_ERR_CAPACITY, STGN_ERR_ORDER = range(6)
+AGG = {"mean": 0, "last": 1, "sum": 2}
+REBUILD = {"never": 0, "fixed": 1, "adaptive": 2}
+SCOPE = {"affected": 0, "direct": 1}
+
+# Symbols include/stgn.h declares (checked by tests/test_capi_symbols.py).
+EXPORTS = (
+    "stgn_version", "stgn_scratch_bytes", "stgn_engine_create", "stgn_engine_destroy",
+    "stgn_engine_set_weights", "stgn_engine_bind", "stgn_engine_process_batch",
+    "stgn_engine_process_batch_dev", "stgn_engine_rebuild", "stgn_engine_full_reference",
+    "stgn_engine_affected", "stgn_engine_pred_embeddings", "stgn_pipeline_many",
+)
+
+
+class Dims(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in
+                ("d_s", "d_e", "d_t", "d_x", "d_m", "d_k", "heads", "layers")]
+
+
+class Config(C.Structure):
+    _fields_ = [("fanout", C.c_int32), ("aggregator", C.c_int32), ("rebuild", C.c_int32),
+                ("rebuild_interval", C.c_int32), ("gamma", C.c_double),
+                ("delta_max", C.c_double), ("alpha", C.c_double), ("window", C.c_double),
+                ("scope", C.c_int32), ("max_batch", C.c_int32)]
+
+
+class Weights(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in
+                ("wq", "wkt", "wv", "wo", "wmsg", "bmsg", "wgru", "ugru", "bgru", "wpred",
+                 "omega", "phi0")] + [("bpred", C.c_double)]
+
+
+class Ctl(C.Structure):
+    _fields_ = [("tau", C.c_int64), ("cum_count", C.c_int64), ("cum_gen", C.c_uint32),
+                ("pad0", C.c_uint32), ("reserved", C.c_int64 * 6)]
+
+
+STATE_PTRS = (
+    "mem", "last", "version", "h", "valid", "valid_at", "ring_cnt", "ring_head", "ring_ccnt",
+    "ring_nbr", "ring_eid", "ring_t", "ring_pay", "ring_feat", "amark", "dmark", "nodecnt",
+    "nodeadj", "nodefill", "nodeoff", "drift_acc", "drift_touched", "cum_mark", "cum_list",
+    "e_src", "e_dst", "e_t", "e_feat", "e_prev", "adj_head", "adj_deg", "gpow", "ctl", "scratch",
+)
+
+
+class State(C.Structure):
+    _fields_ = [("cap_nodes", C.c_int64), ("cap_edges", C.c_int64), ("gpow_len", C.c_int64)] + \
+               [(n, C.c_void_p) for n in STATE_PTRS]
+
+
+class Report(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in
+                ("direct", "affected", "nbr_hit", "nbr_miss", "entries_affected",
+                 "entries_direct", "rebuild_kind", "rebuild_nodes", "entries_rebuild", "tau",
+                 "cum_count", "changed")] + [("global_drift", C.c_double),
+                                              ("reserved", C.c_int64 * 3)]
+
+
+_LIB = None
+
+
+def lib():
+    """Load _stgn.so (building it first if the sources are newer)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        from .build import build
+        build()
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    P = C.POINTER
+    L.stgn_version.restype = C.c_char_p
+    L.stgn_scratch_bytes.restype = i64
+    L.stgn_scratch_bytes.argtypes = [P(Dims), P(Config), i64]
+    L.stgn_engine_create.argtypes = [P(Dims), P(Config), P(vp)]
+    L.stgn_engine_destroy.argtypes = [vp]
+    L.stgn_engine_set_weights.argtypes = [vp, P(Weights)]
+    L.stgn_engine_bind.argtypes = [vp, P(State)]
+    L.stgn_engine_process_batch.argtypes = [vp, i32, vp, vp, vp, vp, i64, i64, i64, vp,
+                                            P(Report), vp]
+    L.stgn_engine_process_batch_dev.argtypes = [vp, i32, vp, vp, vp, vp, i64, i64, i64, vp,
+                                                P(Report), vp]
+    L.stgn_engine_rebuild.argtypes = [vp, vp, i64, i64, dbl, P(i64), vp]
+    L.stgn_engine_full_reference.argtypes = [vp, i64, vp, vp]
+    L.stgn_engine_affected.argtypes = [vp, vp, vp, i64, P(i64), P(i64), vp, vp]
+    L.stgn_engine_pred_embeddings.argtypes = [vp, vp, i64, vp]
+    L.stgn_pipeline_many.argtypes = [P(Dims), i64, i64] + [vp] * 18
+    for name in EXPORTS:
+        if name not in ("stgn_version", "stgn_scratch_bytes"):
+            getattr(L, name).restype = C.c_int
+    _LIB = L
+    return L
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == STGN_OK:
+        return
+    msg = f"{what}: stgn error {rc}"
+    if rc == STGN_ERR_INVALID:
+        raise ConfigError(msg)
+    if rc == STGN_ERR_BOUNDS:
+        raise InputError(msg)
+    if rc == STGN_ERR_ORDER:
+        raise MonotonicityError(msg)
+    if rc == STGN_ERR_CAPACITY:
+        raise KernelInputError(msg + " (capacity)")
+    raise RuntimeError(msg + " (CUDA failure)")
+
+
+def dims_struct(dims) -> Dims:
+    return Dims(dims.d_s, dims.d_e, dims.d_t, dims.d_x, dims.d_m, dims.d_k, dims.heads,
+                dims.layers)

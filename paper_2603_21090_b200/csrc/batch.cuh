@@ -1,0 +1,664 @@
+// Per-batch kernels of the incremental path (everything except the
+// attention recompute). All sizes are read from the device header/results
+// so the whole sequence can be captured once in a CUDA graph.
+//
+// Reference anchors (S/ = /root/reference/pkg/src/streamtgn):
+//   k_claim / k_scan / k_place / k_rank   grouping  S/engine.py:170-180
+//   k_ring / k_dupdate                    neighbour cache insert + store append
+//                                         S/engine.py:216-243, S/graph_store.py:126-152,
+//                                         payload freeze S/engine_base.py:88-106
+//   k_hop                                 affected set S/engine.py:182-212
+//   k_records                             change records S/engine.py:216-243
+//   k_predict                             S/kernels/reference.py:183-186
+//   k_messages / k_gru                    S/engine_base.py:193-247
+//   k_drift_record / k_drift_decide       S/drift.py:52-78, S/engine.py:366-372, 440-453
+#pragma once
+
+#include "attn.cuh"
+
+struct StateView {
+  float* mem;
+  double* last;
+  int64_t* version;
+  float* h;
+  uint8_t* valid;
+  double* valid_at;
+  int32_t *ring_cnt, *ring_head, *ring_ccnt, *ring_nbr;
+  int64_t* ring_eid;
+  double* ring_t;
+  float *ring_pay, *ring_feat;
+  uint32_t *amark, *dmark;
+  int32_t *nodecnt, *nodeadj, *nodefill, *nodeoff;
+  double* drift_acc;
+  int64_t* drift_touched;
+  uint32_t* cum_mark;
+  int32_t* cum_list;
+  int32_t *e_src, *e_dst;
+  double* e_t;
+  float* e_feat;
+  int64_t *e_prev, *adj_head, *adj_deg;
+  const double* gpow;
+  int64_t gpow_len;
+  stgn_ctl* ctl;
+};
+
+__device__ __forceinline__ int rec_node(const Scratch& s, int r) {
+  return (r & 1) ? s.in_dst[r >> 1] : s.in_src[r >> 1];
+}
+__device__ __forceinline__ int rec_other(const Scratch& s, int r) {
+  return (r & 1) ? s.in_src[r >> 1] : s.in_dst[r >> 1];
+}
+// A self-loop produces two messages but one adjacency entry (the src side),
+// S/graph_store.py:147-148, S/engine.py:177-179, S/engine_base.py:209-215.
+__device__ __forceinline__ bool rec_is_adj(const Scratch& s, int r) {
+  return !(r & 1) || (s.in_src[r >> 1] != s.in_dst[r >> 1]);
+}
+
+#define GRID_STRIDE(i, n) \
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+// Reset per-batch results.
+__global__ void k_begin(Scratch s) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    BatchRes* r = s.res;
+    r->nD = 0;
+    r->nA = 0;
+    for (int k = 0; k < STGN_MAX_LAYERS + 2; ++k) r->hop_off[k] = 0;
+    r->n_drifted = 0;
+    r->nbr_hit = r->nbr_miss = r->E_A = r->E_D = r->E_R = r->changed = 0;
+    r->rebuild_kind = 0;
+    r->rebuild_nodes = 0;
+    r->global_drift = 0.0;
+    r->rb_partial_n = 0;
+    r->rb_full_n = 0;
+    r->ticket = 0;
+  }
+}
+
+// Records r = 2i + side (side 0: owner src, side 1: owner dst). First
+// toucher of a node claims its direct-set slot; counts per node; the
+// side-0 record also appends the edge to the temporal store.
+__global__ void k_claim(Geo g, StateView st, Scratch s) {
+  const BatchHdr* hd = s.hdr;
+  const int64_t B = hd->B;
+  const uint32_t stamp = hd->stamp;
+  GRID_STRIDE(r, 2 * B) {
+    const int rr = (int)r;
+    const int node = rec_node(s, rr);
+    if (atomicExch(&st.dmark[node], stamp) != stamp) {
+      const int di = atomicAdd(&s.res->nD, 1);
+      s.alist[di] = node;
+      st.amark[node] = stamp;
+    }
+    atomicAdd(&st.nodecnt[node], 1);
+    if (rec_is_adj(s, rr)) atomicAdd(&st.nodeadj[node], 1);
+    if (!(rr & 1)) {
+      const int64_t i = r >> 1;
+      const int64_t eid = hd->m0 + i;
+      st.e_src[eid] = s.in_src[i];
+      st.e_dst[eid] = s.in_dst[i];
+      st.e_t[eid] = s.in_t[i];
+      for (int j = 0; j < g.d_e; ++j) st.e_feat[eid * g.ld_e + j] = s.in_feat[i * g.ld_e + j];
+    }
+  }
+}
+
+// One block: exclusive scan of per-direct-node record counts; per-node
+// offsets; remembers each direct node's pre-batch cache state.
+__global__ void k_scan(Geo g, StateView st, Scratch s) {
+  __shared__ int32_t warp_tot[32];
+  __shared__ int32_t carry;
+  const int nD = s.res->nD;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nD; base += blockDim.x) {
+    const int d = base + threadIdx.x;
+    int c = 0;
+    if (d < nD) {
+      const int v = s.alist[d];
+      c = st.nodecnt[v];
+      const int cc = st.ring_ccnt[v];
+      s.d_wascached[d] = cc >= 0;
+      s.d_baselen[d] = cc >= 0 ? cc : st.ring_cnt[v];
+    }
+    // block inclusive scan
+    int x = c;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int t = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      warp_tot[lane] = t;
+    }
+    __syncthreads();
+    const int excl = carry + x - c + (wid > 0 ? warp_tot[wid - 1] : 0);
+    if (d < nD) {
+      s.doff[d] = excl;
+      st.nodeoff[s.alist[d]] = excl;
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + c;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    s.doff[nD] = carry;
+    s.res->nA = nD;
+    s.res->hop_off[0] = 0;
+    s.res->hop_off[1] = nD;
+  }
+}
+
+__global__ void k_place(StateView st, Scratch s) {
+  const int64_t B = s.hdr->B;
+  GRID_STRIDE(r, 2 * B) {
+    const int node = rec_node(s, (int)r);
+    const int slot = atomicAdd(&st.nodefill[node], 1);
+    s.rec_u[st.nodeoff[node] + slot] = (int)r;
+  }
+}
+
+// Rank each record inside its node's segment (segments are small: one
+// entry per incident batch edge), giving message order (ascending r) and
+// the newest-first adjacency rank.
+__global__ void k_rank(StateView st, Scratch s) {
+  const int64_t B = s.hdr->B;
+  GRID_STRIDE(r64, 2 * B) {
+    const int r = (int)r64;
+    const int node = rec_node(s, r);
+    const int off = st.nodeoff[node];
+    const int k = st.nodecnt[node];
+    const bool adj = rec_is_adj(s, r);
+    int rank = 0, arank = 0, prev = -1;
+    for (int q = off; q < off + k; ++q) {
+      const int o = s.rec_u[q];
+      if (o < r) {
+        ++rank;
+        if (rec_is_adj(s, o) && o > prev) prev = o;
+      } else if (o > r && rec_is_adj(s, o)) {
+        ++arank;
+      }
+    }
+    s.rec_s[off + rank] = r;
+    s.rec_adjrank[r] = adj ? arank : -1;
+    s.rec_prev[r] = prev;
+  }
+}
+
+__device__ __forceinline__ int64_t entry_index(int64_t m0, int r) {
+  return 2 * (m0 + (r >> 1)) + (r & 1);
+}
+
+// Write the new adjacency entries into the node rings (newest at rank 0),
+// freezing the opposite endpoint's pre-batch stack [s || 0, h_0..h_{K-2}]
+// as the payload; link the append-only store's per-node chains. One warp
+// per record.
+__global__ void k_ring(Geo g, StateView st, Scratch s) {
+  const BatchHdr* hd = s.hdr;
+  const int64_t R = 2 * hd->B;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r64 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r64 < R; r64 += warps) {
+    const int r = (int)r64;
+    if (!rec_is_adj(s, r)) continue;
+    const int v = rec_node(s, r);
+    const int u = rec_other(s, r);
+    const int64_t i = r >> 1;
+    const int a = s.rec_adjrank[r];
+    if (lane == 0) {
+      const int p = s.rec_prev[r];
+      st.e_prev[entry_index(hd->m0, r)] = p >= 0 ? entry_index(hd->m0, p) : st.adj_head[v];
+    }
+    const int kadj = st.nodeadj[v];
+    const int kk = kadj < g.L ? kadj : g.L;
+    if (a >= kk) continue;  // evicted within the batch
+    int slot = (st.ring_head[v] - kk + a) % g.L;
+    if (slot < 0) slot += g.L;
+    const int64_t rs = (int64_t)v * g.L + slot;
+    if (lane == 0) {
+      st.ring_nbr[rs] = u;
+      st.ring_eid[rs] = hd->m0 + i;
+      st.ring_t[rs] = s.in_t[i];
+    }
+    for (int j = lane; j < g.d_e; j += 32) st.ring_feat[rs * g.ld_e + j] = s.in_feat[i * g.ld_e + j];
+    for (int l = 0; l < g.K; ++l) {
+      float* dstp = st.ring_pay + (((int64_t)v * g.K + l) * g.L + slot) * g.ld_d;
+      if (l == 0) {
+        const float* m = st.mem + (int64_t)u * g.ld_s;
+        for (int j = lane; j < g.d; j += 32) dstp[j] = j < g.d_s ? m[j] : 0.f;
+      } else {
+        const float* hp = st.h + ((int64_t)u * g.K + (l - 1)) * g.ld_d;
+        for (int j = lane; j < g.d; j += 32) dstp[j] = hp[j];
+      }
+    }
+  }
+}
+
+// Per direct node: advance ring head/count, set the post-insertion cache
+// length, and move the store chain head.
+__global__ void k_dupdate(Geo g, StateView st, Scratch s) {
+  const int nD = s.res->nD;
+  const int64_t m0 = s.hdr->m0;
+  GRID_STRIDE(d64, nD) {
+    const int d = (int)d64;
+    const int v = s.alist[d];
+    const int kadj = st.nodeadj[v];
+    const int kk = kadj < g.L ? kadj : g.L;
+    int head = (st.ring_head[v] - kk) % g.L;
+    if (head < 0) head += g.L;
+    st.ring_head[v] = head;
+    const int c = st.ring_cnt[v] + kadj;
+    st.ring_cnt[v] = c < g.L ? c : g.L;
+    const int cc = kadj + s.d_baselen[d];
+    st.ring_ccnt[v] = cc < g.L ? cc : g.L;
+    // newest adjacency record = last adj record in ascending segment order
+    int newest = -1;
+    for (int q = s.doff[d + 1] - 1; q >= s.doff[d]; --q) {
+      const int r = s.rec_s[q];
+      if (rec_is_adj(s, r)) { newest = r; break; }
+    }
+    st.adj_head[v] = entry_index(m0, newest);
+    st.adj_deg[v] += kadj;
+  }
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// One BFS hop: every (frontier node, list position) pair marks its
+// neighbour; first markers append with warp-ballot compaction.
+__global__ void k_hop(Geo g, StateView st, Scratch s, int hop) {
+  const uint32_t stamp = s.hdr->stamp;
+  const int f0 = s.res->hop_off[hop - 1], f1 = s.res->hop_off[hop];
+  const int64_t total = (int64_t)(f1 - f0) * g.L;
+  const int64_t total_r = cdiv(total, 32) * 32;
+  const int lane = threadIdx.x & 31;
+  GRID_STRIDE(x, total_r) {
+    bool fresh = false;
+    int u = -1;
+    if (x < total) {
+      const int w = s.alist[f0 + (int)(x / g.L)];
+      const int j = (int)(x % g.L);
+      const int cc = st.ring_ccnt[w];
+      const int len = cc >= 0 ? cc : st.ring_cnt[w];
+      if (j < len) {
+        int slot = st.ring_head[w] + j;
+        if (slot >= g.L) slot -= g.L;
+        u = st.ring_nbr[(int64_t)w * g.L + slot];
+        fresh = atomicExch(&st.amark[u], stamp) != stamp;
+      }
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, fresh);
+    if (mask) {
+      int basepos = 0;
+      const int leader = __ffs(mask) - 1;
+      if (lane == leader) basepos = atomicAdd(&s.res->nA, __popc(mask));
+      basepos = __shfl_sync(0xffffffffu, basepos, leader);
+      if (fresh) s.alist[basepos + __popc(mask & lanemask_lt())] = u;
+    }
+  }
+}
+
+__global__ void k_hop_fin(Scratch s, int hop) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) s.res->hop_off[hop + 1] = s.res->nA;
+}
+
+// Change records for every affected node (sizes only) + the window filter
+// + cache bookkeeping; S/engine.py:216-243.
+__global__ void k_records(Geo g, StateView st, Scratch s, int finite_window) {
+  const int nA = s.res->nA, nD = s.res->nD;
+  const uint32_t stamp = s.hdr->stamp;
+  const double cutoff = s.hdr->cutoff;
+  unsigned long long hit = 0, miss = 0, changed = 0;
+  GRID_STRIDE(a64, nA) {
+    const int a = (int)a64;
+    const int v = s.alist[a];
+    int added = 0, expired = 0, len, was_cached;
+    if (a < nD) {
+      const int kadj = st.nodeadj[v];
+      was_cached = s.d_wascached[a];
+      const int merged = kadj + s.d_baselen[a];
+      len = merged < g.L ? merged : g.L;
+      expired = was_cached ? (merged > g.L ? merged - g.L : 0) : 0;
+      added = kadj;
+    } else {
+      const int cc = st.ring_ccnt[v];
+      was_cached = cc >= 0;
+      len = was_cached ? cc : st.ring_cnt[v];
+    }
+    int n_new = added < len ? added : len;
+    const int head = st.ring_head[v];
+    const int64_t rb = (int64_t)v * g.L;
+    if (finite_window) {
+      int keep = 0;
+      while (keep < len) {
+        int slot = head + keep;
+        if (slot >= g.L) slot -= g.L;
+        if (st.ring_t[rb + slot] < cutoff) break;
+        ++keep;
+      }
+      expired += len - keep;
+      len = keep;
+      if (n_new > len) n_new = len;
+    }
+    // distinct direct neighbours among the kept old entries
+    int upd = 0;
+    for (int j = n_new; j < len; ++j) {
+      int slot = head + j;
+      if (slot >= g.L) slot -= g.L;
+      const int u = st.ring_nbr[rb + slot];
+      if (st.dmark[u] != stamp) continue;
+      bool dup = false;
+      for (int q = n_new; q < j; ++q) {
+        int s2 = head + q;
+        if (s2 >= g.L) s2 -= g.L;
+        if (st.ring_nbr[rb + s2] == u) { dup = true; break; }
+      }
+      if (!dup) ++upd;
+    }
+    const int size = added + expired + upd;
+    s.a_size[a] = size;
+    s.a_len[a] = len;
+    st.ring_ccnt[v] = len;
+    if (was_cached) ++hit; else ++miss;
+    if (size > 0 && len > 0) ++changed;
+  }
+  // block-aggregate the counters
+  for (int o = 16; o > 0; o >>= 1) {
+    hit += __shfl_xor_sync(0xffffffffu, hit, o);
+    miss += __shfl_xor_sync(0xffffffffu, miss, o);
+    changed += __shfl_xor_sync(0xffffffffu, changed, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (hit) atomicAdd(&s.res->nbr_hit, hit);
+    if (miss) atomicAdd(&s.res->nbr_miss, miss);
+    if (changed) atomicAdd(&s.res->changed, changed);
+  }
+}
+
+// valid / valid_at for A \ D when only V_direct is recomputed.
+__global__ void k_mark_valid(StateView st, Scratch s) {
+  const int nA = s.res->nA, nD = s.res->nD;
+  const double t = s.hdr->t_batch;
+  GRID_STRIDE(a, nA) {
+    if (a < nD) continue;
+    const int v = s.alist[a];
+    st.valid[v] = 1;
+    st.valid_at[v] = t;
+  }
+}
+
+// sigma(w_p . [h_src || h_dst] + b_p) in float64, one warp per edge.
+__global__ void k_predict(Geo g, StateView st, Scratch s, const double* wpred, double bpred) {
+  const int64_t B = s.hdr->B;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < B; i += warps) {
+    const float* hu = st.h + ((int64_t)s.in_src[i] * g.K + (g.K - 1)) * g.ld_d;
+    const float* hv = st.h + ((int64_t)s.in_dst[i] * g.K + (g.K - 1)) * g.ld_d;
+    double acc = 0.0;
+    for (int j = lane; j < g.d; j += 32) acc += wpred[j] * (double)hu[j] + wpred[g.d + j] * (double)hv[j];
+    acc = warp_sum_d(acc);
+    if (lane == 0) s.preds[i] = 1.0 / (1.0 + exp(-(acc + bpred)));
+  }
+}
+
+// Messages: row r = [s_owner || s_other || feat || phi(t - last_owner)],
+// msg = row W_side + b_side. Tile = 16 edges: rows 0..15 src side, 16..31
+// dst side.
+__global__ void __launch_bounds__(STGN_THREADS)
+k_messages(Geo g, StateView st, Scratch s, const float* wmsg, const float* bmsg,
+           const double* omega) {
+  extern __shared__ float4 smem4[];
+  float* Xr = reinterpret_cast<float*>(smem4);   // [32][msg_in]
+  float* Mo = Xr + 32 * g.msg_in;                // [32][d_m]
+  const int64_t B = s.hdr->B;
+  const int64_t ntiles = cdiv(B, 16);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t e0 = tile * 16;
+    for (int o = threadIdx.x; o < 32 * g.msg_in; o += blockDim.x) {
+      const int row = o / g.msg_in, c = o % g.msg_in;
+      const int side = row >> 4;
+      const int64_t i = e0 + (row & 15);
+      float v = 0.f;
+      if (i < B) {
+        const int own = side ? s.in_dst[i] : s.in_src[i];
+        const int oth = side ? s.in_src[i] : s.in_dst[i];
+        if (c < g.d_s) v = st.mem[(int64_t)own * g.ld_s + c];
+        else if (c < 2 * g.d_s) v = st.mem[(int64_t)oth * g.ld_s + c - g.d_s];
+        else if (c < 2 * g.d_s + g.d_e) v = s.in_feat[i * g.ld_e + (c - 2 * g.d_s)];
+        else v = phi_component(omega, c - 2 * g.d_s - g.d_e, s.in_t[i] - st.last[own], g.phi_amp);
+      }
+      Xr[o] = v;
+    }
+    __syncthreads();
+    tile_gemm(Xr, g.msg_in, 16, g.msg_in, wmsg, g.d_m, g.d_m, Mo, g.d_m, 1.f);
+    tile_gemm(Xr + 16 * g.msg_in, g.msg_in, 16, g.msg_in, wmsg + (int64_t)g.msg_in * g.d_m,
+              g.d_m, g.d_m, Mo + 16 * g.d_m, g.d_m, 1.f);
+    __syncthreads();
+    for (int o = threadIdx.x; o < 32 * g.d_m; o += blockDim.x) {
+      const int row = o / g.d_m, c = o % g.d_m;
+      const int side = row >> 4;
+      const int64_t i = e0 + (row & 15);
+      if (i < B) s.msgs[(2 * i + side) * g.ld_m + c] = Mo[o] + bmsg[side * g.d_m + c];
+    }
+    __syncthreads();
+  }
+}
+
+// Aggregate each direct node's messages in message order (mean / last /
+// sum, S/kernels/reference.py:56-74) and apply one GRU step
+// (S/kernels/reference.py:81-90); tile of 32 direct nodes.
+__global__ void __launch_bounds__(STGN_THREADS)
+k_gru(Geo g, StateView st, Scratch s, const float* wgru, const float* ugru, const float* bgru,
+      int aggregator) {
+  extern __shared__ float4 smem4[];
+  const int T = 32;
+  float* Ag = reinterpret_cast<float*>(smem4);  // [T][d_m]
+  float* Sp = Ag + T * g.d_m;                    // [T][d_s]
+  float* Zg = Sp + T * g.d_s;                    // [T][d_s]
+  float* Rg = Zg + T * g.d_s;                    // [T][d_s]
+  float* Hc = Rg + T * g.d_s;                    // [T][d_s]
+  __shared__ int s_node[32];
+  __shared__ int s_lastrec[32];
+  const int nD = s.res->nD;
+  const int64_t ntiles = cdiv(nD, T);
+  const int64_t mats = (int64_t)g.d_m * g.d_s, umats = (int64_t)g.d_s * g.d_s;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int d0 = (int)(tile * T);
+    if (threadIdx.x < T) {
+      const int d = d0 + threadIdx.x;
+      s_node[threadIdx.x] = d < nD ? s.alist[d] : -1;
+      s_lastrec[threadIdx.x] = d < nD ? s.rec_s[s.doff[d + 1] - 1] : -1;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < T * g.d_m; o += blockDim.x) {
+      const int i = o / g.d_m, c = o % g.d_m;
+      const int d = d0 + i;
+      float v = 0.f;
+      if (d < nD) {
+        const int lo = s.doff[d], hi = s.doff[d + 1];
+        if (aggregator == STGN_AGG_LAST) {
+          v = s.msgs[(int64_t)s_lastrec[i] * g.ld_m + c];
+        } else {
+          float acc = 0.f;
+          for (int q = lo; q < hi; ++q) acc += s.msgs[(int64_t)s.rec_s[q] * g.ld_m + c];
+          v = aggregator == STGN_AGG_MEAN ? acc / (float)(hi - lo) : acc;
+        }
+      }
+      Ag[o] = v;
+    }
+    for (int o = threadIdx.x; o < T * g.d_s; o += blockDim.x) {
+      const int i = o / g.d_s, c = o % g.d_s;
+      Sp[o] = s_node[i] >= 0 ? st.mem[(int64_t)s_node[i] * g.ld_s + c] : 0.f;
+    }
+    __syncthreads();
+    tile_gemm(Ag, g.d_m, T, g.d_m, wgru, g.d_s, g.d_s, Zg, g.d_s, 1.f);
+    tile_gemm(Ag, g.d_m, T, g.d_m, wgru + mats, g.d_s, g.d_s, Rg, g.d_s, 1.f);
+    tile_gemm(Ag, g.d_m, T, g.d_m, wgru + 2 * mats, g.d_s, g.d_s, Hc, g.d_s, 1.f);
+    __syncthreads();
+    tile_gemm(Sp, g.d_s, T, g.d_s, ugru, g.d_s, g.d_s, Zg, g.d_s, 1.f, true);
+    tile_gemm(Sp, g.d_s, T, g.d_s, ugru + umats, g.d_s, g.d_s, Rg, g.d_s, 1.f, true);
+    __syncthreads();
+    for (int o = threadIdx.x; o < T * g.d_s; o += blockDim.x) {
+      const int c = o % g.d_s;
+      Zg[o] = sigmoidf_(Zg[o] + bgru[c]);
+      Rg[o] = sigmoidf_(Rg[o] + bgru[g.d_s + c]) * Sp[o];  // r * s
+    }
+    __syncthreads();
+    tile_gemm(Rg, g.d_s, T, g.d_s, ugru + 2 * umats, g.d_s, g.d_s, Hc, g.d_s, 1.f, true);
+    __syncthreads();
+    for (int o = threadIdx.x; o < T * g.d_s; o += blockDim.x) {
+      const int i = o / g.d_s, c = o % g.d_s;
+      const int v = s_node[i];
+      if (v < 0) continue;
+      const float cand = tanhf(Hc[o] + bgru[2 * g.d_s + c]);
+      const float z = Zg[o];
+      st.mem[(int64_t)v * g.ld_s + c] = (1.f - z) * cand + z * Sp[o];
+    }
+    if (threadIdx.x < T && s_node[threadIdx.x] >= 0) {
+      const int v = s_node[threadIdx.x];
+      st.version[v] = s.hdr->batch_index;
+      st.last[v] = s.in_t[s_lastrec[threadIdx.x] >> 1];  // max t = last message (t non-decreasing)
+    }
+    __syncthreads();
+  }
+}
+
+// Drift estimators: acc_v <- gamma^(tau - touched_v) acc_v + |dN_v| / |N_v|
+// for nodes with a non-empty change record; cumulative affected set.
+__global__ void k_drift_record(StateView st, Scratch s) {
+  const int nA = s.res->nA;
+  const int64_t tau = st.ctl->tau + 1;
+  const uint32_t gen = st.ctl->cum_gen;
+  GRID_STRIDE(a64, nA) {
+    const int a = (int)a64;
+    const int v = s.alist[a];
+    const int sz = s.a_size[a], len = s.a_len[a];
+    if (sz > 0 && len > 0) {
+      const double acc = st.drift_acc[v];
+      const double dec = acc == 0.0 ? 0.0 : acc * st.gpow[tau - st.drift_touched[v]];
+      st.drift_acc[v] = dec + (double)sz / (double)len;
+      st.drift_touched[v] = tau;
+    }
+    if (st.cum_mark[v] != gen) {
+      st.cum_mark[v] = gen;
+      const long long pos = atomicAdd((unsigned long long*)&st.ctl->cum_count, 1ull);
+      st.cum_list[pos] = v;
+    }
+  }
+}
+
+// Global drift = mean decayed estimator over the cumulative affected set;
+// the policy decision (S/drift.py:16-23, 72-78; S/engine.py:440-453) is
+// made by the last block to finish. rebuild: 0 never, 1 fixed, 2 adaptive.
+__global__ void k_drift_decide(StateView st, Scratch s, int rebuild, int64_t interval,
+                               double delta_max, double alpha) {
+  __shared__ double red[32];
+  __shared__ bool is_last;
+  const int64_t tau = st.ctl->tau + 1;
+  const int64_t n = st.ctl->cum_count;
+  double part = 0.0;
+  if (rebuild == STGN_REBUILD_ADAPTIVE) {
+    // fixed per-block partition -> deterministic sum
+    const int64_t per = cdiv(n, gridDim.x);
+    const int64_t lo = blockIdx.x * per, hi = lo + per < n ? lo + per : n;
+    for (int64_t q = lo + threadIdx.x; q < hi; q += blockDim.x) {
+      const int v = st.cum_list[q];
+      const double acc = st.drift_acc[v];
+      const double dec = acc == 0.0 ? 0.0 : acc * st.gpow[tau - st.drift_touched[v]];
+      part += dec;
+      if (dec > delta_max) {
+        const int pos = atomicAdd(&s.res->n_drifted, 1);
+        s.drifted[pos] = v;
+      }
+    }
+  }
+  part = warp_sum_d(part);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b += red[w];
+    s.partials[blockIdx.x] = b;
+    __threadfence();
+    const unsigned t = atomicAdd(&s.res->ticket, 1u);
+    is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (is_last && threadIdx.x == 0) {
+    __threadfence();
+    int kind = 0;
+    double gdrift = 0.0;
+    if (rebuild == STGN_REBUILD_ADAPTIVE) {
+      double tot = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) tot += s.partials[b];
+      gdrift = n > 0 ? tot / (double)n : 0.0;
+      if (gdrift > delta_max) {
+        const double nn = (double)s.hdr->node_count;
+        kind = ((double)s.res->n_drifted < alpha * nn) ? 1 : 2;
+      }
+    } else if (rebuild == STGN_REBUILD_FIXED) {
+      if (interval >= 1 && s.hdr->batch_index % interval == 0) kind = 2;
+    }
+    s.res->global_drift = gdrift;
+    s.res->rebuild_kind = kind;
+    s.res->rb_partial_n = kind == 1 ? s.res->n_drifted : 0;
+    s.res->rb_full_n = kind == 2 ? (int32_t)s.hdr->node_count : 0;
+    s.res->rebuild_nodes = kind == 1 ? s.res->n_drifted : (kind == 2 ? s.hdr->node_count : 0);
+    st.ctl->tau = tau;
+  }
+}
+
+// Rebuild prologue: uncached nodes get their cache filled from the store
+// (S/engine.py:390-392).
+__global__ void k_rb_fill(StateView st, const int32_t* list, const int32_t* count_ptr,
+                          int64_t count_const) {
+  const int64_t n = count_ptr ? (int64_t)count_ptr[0] : count_const;
+  GRID_STRIDE(q, n) {
+    const int v = list ? list[q] : (int)q;
+    if (st.ring_ccnt[v] < 0) st.ring_ccnt[v] = st.ring_cnt[v];
+  }
+}
+
+// Scheduler reset after an executed rebuild (S/drift.py:92-96).
+__global__ void k_drift_reset(StateView st, Scratch s) {
+  if (s.res->rebuild_kind == 0) return;
+  const int64_t n = st.ctl->cum_count;
+  GRID_STRIDE(q, n) {
+    const int v = st.cum_list[q];
+    st.drift_acc[v] = 0.0;
+    st.drift_touched[v] = 0;
+  }
+}
+
+__global__ void k_drift_reset_fin(StateView st, Scratch s) {
+  if (threadIdx.x || blockIdx.x) return;
+  if (s.res->rebuild_kind == 0) return;
+  st.ctl->cum_count = 0;
+  st.ctl->cum_gen += 1;
+  st.ctl->tau = 0;
+}
+
+// Clear per-node batch scratch of the direct nodes.
+__global__ void k_cleanup(StateView st, Scratch s) {
+  const int nD = s.res->nD;
+  GRID_STRIDE(d, nD) {
+    const int v = s.alist[d];
+    st.nodecnt[v] = 0;
+    st.nodeadj[v] = 0;
+    st.nodefill[v] = 0;
+  }
+}

@@ -1,0 +1,609 @@
+// C ABI driver: engine handle, per-batch launch sequence (captured once
+// as a CUDA graph), rebuild / full_reference entry points and the
+// operator-level pipeline_many. See include/stgn.h for the contract.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "batch.cuh"
+
+#ifndef STGN_VERSION
+#define STGN_VERSION "stgn 0.1.0 sm_100a"
+#endif
+
+// ---------------------------------------------------------------------------
+// attention launch (template dispatch on the per-lane register widths)
+// ---------------------------------------------------------------------------
+typedef void (*attn_fn_t)(Geo, AttnWeights, RingSrc, FlatSrc, int);
+
+template <bool FLAT>
+static attn_fn_t pick_attn(const Geo& g) {
+  const int a = (int)cdiv(g.k_in, 32);
+  const bool h4 = g.H > 2;
+#define PICK(MA)                                                             \
+  if (a <= MA) return h4 ? (attn_fn_t)attn_kernel<MA, 4, FLAT> : (attn_fn_t)attn_kernel<MA, 2, FLAT>;
+  PICK(2)
+  PICK(4)
+  PICK(8)
+  PICK(12)
+  PICK(16)
+#undef PICK
+  return nullptr;
+}
+
+struct AttnLaunch {
+  attn_fn_t fn = nullptr;
+  int T = 0;
+  size_t smem = 0;
+  int grid = 0;
+};
+
+static int plan_attn(const Geo& g, bool flat, int num_sms, AttnLaunch* out) {
+  attn_fn_t fn = flat ? pick_attn<true>(g) : pick_attn<false>(g);
+  if (!fn) return STGN_ERR_INVALID;
+  int T = 0;
+  size_t smem = 0;
+  for (int cand : {32, 16, 8, 4}) {
+    size_t b = (size_t)attn_smem_floats(g, cand, flat) * sizeof(float);
+    if (b <= 200 * 1024) {
+      T = cand;
+      smem = b;
+      break;
+    }
+  }
+  if (!T) return STGN_ERR_INVALID;
+  CUDA_TRY(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, STGN_THREADS, smem));
+  if (per_sm < 1) per_sm = 1;
+  out->fn = fn;
+  out->T = T;
+  out->smem = smem;
+  out->grid = per_sm * num_sms;
+  return STGN_OK;
+}
+
+// ---------------------------------------------------------------------------
+// engine handle
+// ---------------------------------------------------------------------------
+struct stgn_engine {
+  stgn_dims dims;
+  stgn_config cfg;
+  Geo g;
+  AttnWeights aw;
+  stgn_weights w;
+  bool have_w = false;
+  stgn_state st;
+  bool bound = false;
+  StateView sv;
+  Scratch sc;
+  int num_sms = 148;
+  AttnLaunch attn;
+  size_t msg_smem = 0, gru_smem = 0;
+  // pinned staging mirror of [hdr .. in_feat] and the result area
+  uint8_t* h_in = nullptr;
+  int64_t in_bytes = 0;
+  BatchRes* h_res = nullptr;
+  double* h_preds = nullptr;
+  uint32_t stamp = 0;
+  cudaGraphExec_t graph = nullptr;
+  bool graph_ok = true;   // capture allowed
+};
+
+static void drop_graph(stgn_engine* e) {
+  if (e->graph) {
+    cudaGraphExecDestroy(e->graph);
+    e->graph = nullptr;
+  }
+}
+
+static int validate_dims(const stgn_dims* d, const stgn_config* c) {
+  if (!d || !c) return STGN_ERR_INVALID;
+  if (d->d_s <= 0 || d->d_t <= 0 || d->d_m <= 0 || d->d_k <= 0 || d->heads <= 0 ||
+      d->layers <= 0 || d->d_e < 0 || d->d_x < 0 || (d->d_t & 1))
+    return STGN_ERR_INVALID;
+  if (d->layers > STGN_MAX_LAYERS || d->heads > 4) return STGN_ERR_INVALID;
+  if (c->fanout < 1 || c->max_batch < 1) return STGN_ERR_INVALID;
+  const int k_in = d->d_s + d->d_x + d->d_e + d->d_t;
+  if (k_in > 16 * 32) return STGN_ERR_INVALID;
+  return STGN_OK;
+}
+
+extern "C" {
+
+const char* stgn_version(void) { return STGN_VERSION; }
+
+int64_t stgn_scratch_bytes(const stgn_dims* dims, const stgn_config* cfg, int64_t cap_nodes) {
+  if (validate_dims(dims, cfg) != STGN_OK) return -1;
+  Geo g = make_geo(*dims, cfg->fanout);
+  return scratch_layout(g, cfg->max_batch, cap_nodes, nullptr, nullptr);
+}
+
+int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engine** out) {
+  if (!out) return STGN_ERR_INVALID;
+  int rc = validate_dims(dims, cfg);
+  if (rc) return rc;
+  stgn_engine* e = new (std::nothrow) stgn_engine();
+  if (!e) return STGN_ERR_INVALID;
+  e->dims = *dims;
+  e->cfg = *cfg;
+  if (std::isfinite(cfg->window)) e->cfg.scope = STGN_SCOPE_AFFECTED;  // A\D can change
+  e->g = make_geo(*dims, cfg->fanout);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    delete e;
+    return STGN_ERR_CUDA;
+  }
+  rc = plan_attn(e->g, false, e->num_sms, &e->attn);
+  if (rc) {
+    delete e;
+    return rc;
+  }
+  e->msg_smem = (size_t)(32 * e->g.msg_in + 32 * e->g.d_m) * sizeof(float);
+  e->gru_smem = (size_t)(32 * (e->g.d_m + 4 * e->g.d_s)) * sizeof(float);
+  if (e->msg_smem > 227 * 1024 || e->gru_smem > 227 * 1024) {
+    delete e;
+    return STGN_ERR_INVALID;
+  }
+  if (cudaFuncSetAttribute((const void*)k_messages, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)e->msg_smem) != cudaSuccess ||
+      cudaFuncSetAttribute((const void*)k_gru, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)e->gru_smem) != cudaSuccess) {
+    delete e;
+    return STGN_ERR_CUDA;
+  }
+  Scratch tmp;
+  uint8_t* fake = reinterpret_cast<uint8_t*>(0);
+  scratch_layout(e->g, cfg->max_batch, 1, &tmp, fake + 0);
+  e->in_bytes = (int64_t)((uint8_t*)(tmp.in_feat + (int64_t)cfg->max_batch * e->g.ld_e) - fake);
+  if (cudaMallocHost((void**)&e->h_in, e->in_bytes) != cudaSuccess ||
+      cudaMallocHost((void**)&e->h_res, sizeof(BatchRes)) != cudaSuccess ||
+      cudaMallocHost((void**)&e->h_preds, sizeof(double) * cfg->max_batch) != cudaSuccess) {
+    delete e;
+    return STGN_ERR_CUDA;
+  }
+  memset(e->h_in, 0, e->in_bytes);
+  *out = e;
+  return STGN_OK;
+}
+
+int stgn_engine_destroy(stgn_engine* e) {
+  if (!e) return STGN_OK;
+  drop_graph(e);
+  if (e->h_in) cudaFreeHost(e->h_in);
+  if (e->h_res) cudaFreeHost(e->h_res);
+  if (e->h_preds) cudaFreeHost(e->h_preds);
+  delete e;
+  return STGN_OK;
+}
+
+int stgn_engine_set_weights(stgn_engine* e, const stgn_weights* w) {
+  if (!e || !w) return STGN_ERR_INVALID;
+  e->w = *w;
+  e->aw.wq = w->wq;
+  e->aw.wkt = w->wkt;
+  e->aw.wv = w->wv;
+  e->aw.wo = w->wo;
+  e->aw.omega = w->omega;
+  e->aw.phi0 = w->phi0;
+  e->have_w = true;
+  drop_graph(e);
+  return STGN_OK;
+}
+
+int stgn_engine_bind(stgn_engine* e, const stgn_state* s) {
+  if (!e || !s || !s->scratch || !s->ctl) return STGN_ERR_INVALID;
+  e->st = *s;
+  StateView& v = e->sv;
+  v.mem = s->mem; v.last = s->last; v.version = s->version; v.h = s->h; v.valid = s->valid;
+  v.valid_at = s->valid_at; v.ring_cnt = s->ring_cnt; v.ring_head = s->ring_head;
+  v.ring_ccnt = s->ring_ccnt; v.ring_nbr = s->ring_nbr; v.ring_eid = s->ring_eid;
+  v.ring_t = s->ring_t; v.ring_pay = s->ring_pay; v.ring_feat = s->ring_feat;
+  v.amark = s->amark; v.dmark = s->dmark; v.nodecnt = s->nodecnt; v.nodeadj = s->nodeadj;
+  v.nodefill = s->nodefill; v.nodeoff = s->nodeoff; v.drift_acc = s->drift_acc;
+  v.drift_touched = s->drift_touched; v.cum_mark = s->cum_mark; v.cum_list = s->cum_list;
+  v.e_src = s->e_src; v.e_dst = s->e_dst; v.e_t = s->e_t; v.e_feat = s->e_feat;
+  v.e_prev = s->e_prev; v.adj_head = s->adj_head; v.adj_deg = s->adj_deg;
+  v.gpow = s->gpow; v.gpow_len = s->gpow_len; v.ctl = s->ctl;
+  scratch_layout(e->g, e->cfg.max_batch, s->cap_nodes, &e->sc, s->scratch);
+  e->bound = true;
+  drop_graph(e);
+  return STGN_OK;
+}
+
+}  // extern "C"
+
+static RingSrc ring_src(const stgn_engine* e) {
+  RingSrc r;
+  memset(&r, 0, sizeof(r));
+  const StateView& v = e->sv;
+  r.mem = v.mem; r.h = v.h; r.valid = v.valid; r.valid_at = v.valid_at;
+  r.ring_cnt = v.ring_cnt; r.ring_head = v.ring_head; r.ring_ccnt = v.ring_ccnt;
+  r.ring_t = v.ring_t; r.ring_pay = v.ring_pay; r.ring_feat = v.ring_feat;
+  return r;
+}
+
+static void launch_attn(const stgn_engine* e, const RingSrc& rs, cudaStream_t st) {
+  FlatSrc fs;
+  memset(&fs, 0, sizeof(fs));
+  e->attn.fn<<<e->attn.grid, STGN_THREADS, e->attn.smem, st>>>(e->g, e->aw, rs, fs, e->attn.T);
+}
+
+// The whole per-batch sequence; every size is read on the device.
+static void enqueue_batch(stgn_engine* e, cudaStream_t st) {
+  const Geo& g = e->g;
+  const StateView& v = e->sv;
+  const Scratch& s = e->sc;
+  const int64_t R = 2 * (int64_t)e->cfg.max_batch;
+  const int T = 256;
+  const int g_rec = (int)std::min<int64_t>(cdiv(R, T), 4 * e->num_sms);
+  const int g_wide = 4 * e->num_sms;
+  const int g_warp = (int)std::min<int64_t>(cdiv(R * 32, T), 8 * e->num_sms);
+
+  k_begin<<<1, 32, 0, st>>>(s);
+  k_claim<<<g_rec, T, 0, st>>>(g, v, s);
+  k_scan<<<1, 1024, 0, st>>>(g, v, s);
+  k_place<<<g_rec, T, 0, st>>>(v, s);
+  k_rank<<<g_rec, T, 0, st>>>(v, s);
+  k_ring<<<g_warp, T, 0, st>>>(g, v, s);
+  k_dupdate<<<g_rec, T, 0, st>>>(g, v, s);
+  for (int hop = 1; hop <= g.K; ++hop) {
+    k_hop<<<g_wide, T, 0, st>>>(g, v, s, hop);
+    k_hop_fin<<<1, 32, 0, st>>>(s, hop);
+  }
+  k_records<<<g_wide, T, 0, st>>>(g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
+  // stages 2-4: recompute with pre-batch memory (A, or V_direct)
+  RingSrc rs = ring_src(e);
+  rs.list = s.alist;
+  rs.count_ptr = e->cfg.scope == STGN_SCOPE_DIRECT ? &s.res->nD : &s.res->nA;
+  rs.valid_at_ptr = &s.hdr->t_batch;
+  rs.write_valid = 1;
+  rs.dpred = s.dpred;
+  rs.dpred_count = &s.res->nD;
+  rs.e_count = &s.res->E_A;
+  launch_attn(e, rs, st);
+  if (e->cfg.scope == STGN_SCOPE_DIRECT) k_mark_valid<<<g_wide, T, 0, st>>>(v, s);
+  k_predict<<<g_warp, T, 0, st>>>(g, v, s, e->w.wpred, e->w.bpred);
+  // stage 5: memory update of V_direct, then refresh with post-batch memory
+  k_messages<<<(int)std::min<int64_t>(cdiv(e->cfg.max_batch, 16), 2 * e->num_sms), T,
+               e->msg_smem, st>>>(g, v, s, e->w.wmsg, e->w.bmsg, e->w.omega);
+  k_gru<<<(int)std::min<int64_t>(cdiv(R, 32), 2 * e->num_sms), T, e->gru_smem, st>>>(
+      g, v, s, e->w.wgru, e->w.ugru, e->w.bgru, e->cfg.aggregator);
+  RingSrc rd = ring_src(e);
+  rd.list = s.alist;
+  rd.count_ptr = &s.res->nD;
+  rd.valid_at_ptr = &s.hdr->t_batch;
+  rd.write_valid = 1;
+  rd.e_count = &s.res->E_D;
+  launch_attn(e, rd, st);
+  // drift + rebuild policy
+  k_drift_record<<<g_wide, T, 0, st>>>(v, s);
+  k_drift_decide<<<e->num_sms, T, 0, st>>>(v, s, e->cfg.rebuild, e->cfg.rebuild_interval,
+                                           e->cfg.delta_max, e->cfg.alpha);
+  if (e->cfg.rebuild != STGN_REBUILD_NEVER) {
+    // partial: the drifted list; full: all node ids (each is a no-op unless chosen)
+    k_rb_fill<<<g_wide, T, 0, st>>>(v, s.drifted, &s.res->rb_partial_n, 0);
+    k_rb_fill<<<g_wide, T, 0, st>>>(v, nullptr, &s.res->rb_full_n, 0);
+    RingSrc rp = ring_src(e);
+    rp.list = s.drifted;
+    rp.count_ptr = &s.res->rb_partial_n;
+    rp.valid_at_ptr = &s.hdr->t_batch;
+    rp.write_valid = 1;
+    rp.e_count = &s.res->E_R;
+    launch_attn(e, rp, st);
+    RingSrc rf = rp;
+    rf.list = nullptr;
+    rf.count_ptr = &s.res->rb_full_n;
+    launch_attn(e, rf, st);
+    k_drift_reset<<<g_wide, T, 0, st>>>(v, s);
+    k_drift_reset_fin<<<1, 32, 0, st>>>(v, s);
+  }
+  k_cleanup<<<g_rec, T, 0, st>>>(v, s);
+}
+
+static int run_sequence(stgn_engine* e, cudaStream_t st) {
+  if (e->graph_ok && !e->graph) {
+    cudaGraph_t gr = nullptr;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      enqueue_batch(e, st);
+      if (cudaStreamEndCapture(st, &gr) == cudaSuccess && gr) {
+        if (cudaGraphInstantiate(&e->graph, gr, 0) != cudaSuccess) e->graph = nullptr;
+        cudaGraphDestroy(gr);
+      }
+    }
+    cudaGetLastError();
+    if (!e->graph) e->graph_ok = false;  // fall back to direct launches
+  }
+  if (e->graph) {
+    CUDA_TRY(cudaGraphLaunch(e->graph, st));
+  } else {
+    enqueue_batch(e, st);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return STGN_OK;
+}
+
+static void fill_report(const BatchRes& r, const stgn_ctl* /*unused*/, stgn_report* rep) {
+  memset(rep, 0, sizeof(*rep));
+  rep->direct = r.nD;
+  rep->affected = r.nA;
+  rep->nbr_hit = (int64_t)r.nbr_hit;
+  rep->nbr_miss = (int64_t)r.nbr_miss;
+  rep->entries_affected = (int64_t)r.E_A;
+  rep->entries_direct = (int64_t)r.E_D;
+  rep->rebuild_kind = r.rebuild_kind;
+  rep->rebuild_nodes = r.rebuild_nodes;
+  rep->entries_rebuild = (int64_t)r.E_R;
+  rep->changed = (int64_t)r.changed;
+  rep->global_drift = r.global_drift;
+}
+
+static int check_batch(stgn_engine* e, int32_t B, int64_t m0, int64_t batch_index,
+                       int64_t node_count) {
+  if (!e->bound || !e->have_w) return STGN_ERR_INVALID;
+  if (B < 1 || B > e->cfg.max_batch) return STGN_ERR_CAPACITY;
+  if (m0 + B > e->st.cap_edges || node_count > e->st.cap_nodes) return STGN_ERR_CAPACITY;
+  if (batch_index + 1 >= e->st.gpow_len) return STGN_ERR_CAPACITY;
+  return STGN_OK;
+}
+
+static void fill_hdr(stgn_engine* e, BatchHdr* h, int32_t B, double t_batch, int64_t m0,
+                     int64_t batch_index, int64_t node_count) {
+  memset(h, 0, sizeof(*h));
+  h->B = B;
+  h->m0 = m0;
+  h->batch_index = batch_index;
+  h->node_count = node_count;
+  h->t_batch = t_batch;
+  h->cutoff = std::isfinite(e->cfg.window) ? t_batch - e->cfg.window : -INFINITY;
+  if (++e->stamp == 0) e->stamp = 1;
+  h->stamp = e->stamp;
+}
+
+extern "C" int stgn_engine_process_batch(stgn_engine* e, int32_t B, const int32_t* src,
+                                         const int32_t* dst, const double* t, const float* feat,
+                                         int64_t m0, int64_t batch_index, int64_t node_count,
+                                         double* preds_out, stgn_report* rep, void* stream) {
+  if (!e) return STGN_ERR_INVALID;
+  int rc = check_batch(e, B, m0, batch_index, node_count);
+  if (rc) return rc;
+  for (int32_t i = 0; i < B; ++i) {
+    if (src[i] < 0 || dst[i] < 0 || src[i] >= node_count || dst[i] >= node_count)
+      return STGN_ERR_BOUNDS;
+    if (i && t[i] < t[i - 1]) return STGN_ERR_ORDER;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const Scratch& s = e->sc;
+  uint8_t* base = e->h_in;
+  const uint8_t* dbase = (const uint8_t*)s.hdr;
+  fill_hdr(e, (BatchHdr*)base, B, t[B - 1], m0, batch_index, node_count);
+  memcpy(base + ((uint8_t*)s.in_src - dbase), src, sizeof(int32_t) * B);
+  memcpy(base + ((uint8_t*)s.in_dst - dbase), dst, sizeof(int32_t) * B);
+  memcpy(base + ((uint8_t*)s.in_t - dbase), t, sizeof(double) * B);
+  if (e->g.d_e > 0) {
+    float* fdst = (float*)(base + ((uint8_t*)s.in_feat - dbase));
+    for (int32_t i = 0; i < B; ++i)
+      memcpy(fdst + (int64_t)i * e->g.ld_e, feat + (int64_t)i * e->g.d_e, sizeof(float) * e->g.d_e);
+  }
+  const int64_t bytes = ((uint8_t*)(s.in_feat + (int64_t)B * e->g.ld_e)) - dbase;
+  CUDA_TRY(cudaMemcpyAsync((void*)s.hdr, base, bytes, cudaMemcpyHostToDevice, st));
+  rc = run_sequence(e, st);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(e->h_preds, s.preds, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(e->h_res, s.res, sizeof(BatchRes), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  memcpy(preds_out, e->h_preds, sizeof(double) * B);
+  if (rep) fill_report(*e->h_res, nullptr, rep);
+  return STGN_OK;
+}
+
+__global__ void k_pack_feat(const float* src, float* dst, int64_t B, int d_e, int ld_e) {
+  GRID_STRIDE(x, B * d_e) {
+    const int64_t i = x / d_e, j = x % d_e;
+    dst[i * ld_e + j] = src[x];
+  }
+}
+
+extern "C" int stgn_engine_process_batch_dev(stgn_engine* e, int32_t B, const int32_t* src_dev,
+                                             const int32_t* dst_dev, const double* t_dev,
+                                             const float* feat_dev, int64_t m0,
+                                             int64_t batch_index, int64_t node_count,
+                                             double* preds_dev, stgn_report* rep, void* stream) {
+  if (!e) return STGN_ERR_INVALID;
+  int rc = check_batch(e, B, m0, batch_index, node_count);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Scratch& s = e->sc;
+  double t_last = 0.0;
+  // the header needs t_batch on the host: one 8-byte read of the last timestamp
+  CUDA_TRY(cudaMemcpyAsync(&e->h_preds[0], t_dev + (B - 1), sizeof(double),
+                           cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  t_last = e->h_preds[0];
+  fill_hdr(e, (BatchHdr*)e->h_in, B, t_last, m0, batch_index, node_count);
+  CUDA_TRY(cudaMemcpyAsync((void*)s.hdr, e->h_in, sizeof(BatchHdr), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(s.in_src, src_dev, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(s.in_dst, dst_dev, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(s.in_t, t_dev, sizeof(double) * B, cudaMemcpyDeviceToDevice, st));
+  if (e->g.d_e > 0)
+    k_pack_feat<<<(int)std::min<int64_t>(cdiv((int64_t)B * e->g.d_e, 256), 1024), 256, 0, st>>>(
+        feat_dev, s.in_feat, B, e->g.d_e, e->g.ld_e);
+  rc = run_sequence(e, st);
+  if (rc) return rc;
+  if (preds_dev)
+    CUDA_TRY(cudaMemcpyAsync(preds_dev, s.preds, sizeof(double) * B, cudaMemcpyDeviceToDevice, st));
+  if (rep) {
+    CUDA_TRY(cudaMemcpyAsync(e->h_res, s.res, sizeof(BatchRes), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    fill_report(*e->h_res, nullptr, rep);
+  }
+  return STGN_OK;
+}
+
+extern "C" int stgn_engine_rebuild(stgn_engine* e, const int32_t* ids, int64_t n_ids,
+                                   int64_t node_count, double valid_at_value, int64_t* count,
+                                   void* stream) {
+  if (!e || !e->bound || !e->have_w) return STGN_ERR_INVALID;
+  if (node_count > e->st.cap_nodes) return STGN_ERR_CAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Scratch& s = e->sc;
+  const int32_t* list = nullptr;
+  int64_t n = node_count;
+  if (ids) {
+    if (n_ids > e->st.cap_nodes) return STGN_ERR_CAPACITY;
+    for (int64_t i = 0; i < n_ids; ++i)
+      if (ids[i] < 0 || ids[i] >= node_count) return STGN_ERR_BOUNDS;
+    if (n_ids) CUDA_TRY(cudaMemcpyAsync(s.rb_ids, ids, sizeof(int32_t) * n_ids, cudaMemcpyHostToDevice, st));
+    list = s.rb_ids;
+    n = n_ids;
+  }
+  if (count) *count = n;
+  if (n == 0) return STGN_OK;
+  k_rb_fill<<<4 * e->num_sms, 256, 0, st>>>(e->sv, list, nullptr, n);
+  RingSrc r = ring_src(e);
+  r.list = list;
+  r.count_const = n;
+  r.valid_at_const = valid_at_value;
+  r.write_valid = 1;
+  launch_attn(e, r, st);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return STGN_OK;
+}
+
+extern "C" int stgn_engine_full_reference(stgn_engine* e, int64_t node_count, float* out_dev,
+                                          void* stream) {
+  if (!e || !e->bound || !e->have_w || !out_dev) return STGN_ERR_INVALID;
+  if (node_count > e->st.cap_nodes) return STGN_ERR_CAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  RingSrc r = ring_src(e);
+  r.list = nullptr;
+  r.count_const = node_count;
+  r.use_store = 1;
+  r.final_out = out_dev;
+  launch_attn(e, r, st);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return STGN_OK;
+}
+
+extern "C" int stgn_engine_affected(stgn_engine* e, int32_t* direct, int32_t* affected,
+                                    int64_t cap, int64_t* n_direct, int64_t* n_affected,
+                                    int32_t* change_sizes, void* stream) {
+  if (!e || !e->bound) return STGN_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Scratch& s = e->sc;
+  CUDA_TRY(cudaMemcpyAsync(e->h_res, s.res, sizeof(BatchRes), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  const int64_t nD = e->h_res->nD, nA = e->h_res->nA;
+  if (n_direct) *n_direct = nD;
+  if (n_affected) *n_affected = nA;
+  if (nA > cap) return STGN_ERR_CAPACITY;
+  if (direct && nD) CUDA_TRY(cudaMemcpyAsync(direct, s.alist, 4 * nD, cudaMemcpyDeviceToHost, st));
+  if (affected && nA) CUDA_TRY(cudaMemcpyAsync(affected, s.alist, 4 * nA, cudaMemcpyDeviceToHost, st));
+  if (change_sizes && nA)
+    CUDA_TRY(cudaMemcpyAsync(change_sizes, s.a_size, 4 * nA, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return STGN_OK;
+}
+
+extern "C" int stgn_engine_pred_embeddings(stgn_engine* e, float* out, int64_t n_direct,
+                                           void* stream) {
+  if (!e || !e->bound || !out) return STGN_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_direct <= 0) return STGN_OK;
+  CUDA_TRY(cudaMemcpy2DAsync(out, sizeof(float) * e->g.d, e->sc.dpred, sizeof(float) * e->g.ld_d,
+                             sizeof(float) * e->g.d, n_direct, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return STGN_OK;
+}
+
+// ---------------------------------------------------------------------------
+// operator level
+// ---------------------------------------------------------------------------
+// reference layouts -> packed layouts of stgn.h
+__global__ void k_pack_attn(Geo g, const float* wq, const float* wk, const float* wv,
+                            float* pq, float* pkt, float* pv) {
+  const int64_t nq = (int64_t)g.K * g.H * g.q_in * g.d_k;
+  const int64_t nk = (int64_t)g.K * g.H * g.k_in * g.d_k;
+  GRID_STRIDE(x, nq) {  // (l,h,a,b) -> pq[l][a][h*d_k+b]
+    const int b = (int)(x % g.d_k);
+    int64_t y = x / g.d_k;
+    const int a = (int)(y % g.q_in);
+    y /= g.q_in;
+    const int hh = (int)(y % g.H);
+    const int l = (int)(y / g.H);
+    pq[((int64_t)l * g.q_in + a) * g.HD + hh * g.d_k + b] = wq[x];
+  }
+  GRID_STRIDE(x, nk) {  // (l,h,a,b) -> pkt[l][h][b][a], pv[l][h][a][b]
+    const int b = (int)(x % g.d_k);
+    int64_t y = x / g.d_k;
+    const int a = (int)(y % g.k_in);
+    y /= g.k_in;
+    const int hh = (int)(y % g.H);
+    const int l = (int)(y / g.H);
+    pkt[(((int64_t)l * g.H + hh) * g.d_k + b) * g.k_in + a] = wk[x];
+    pv[x] = wv[x];
+  }
+}
+
+extern "C" int stgn_pipeline_many(const stgn_dims* dims, int64_t N, int64_t E, const float* qbase,
+                                  const int64_t* offsets, const float* payload, const float* feat,
+                                  const double* dt, const double* omega, const float* phi0,
+                                  const float* wq, const float* wk, const float* wv,
+                                  const float* wo, float* out, float* scores, float* values,
+                                  float* maxlog, float* zsum, float* qvecs, void* stream) {
+  if (!dims) return STGN_ERR_INVALID;
+  stgn_config c;
+  memset(&c, 0, sizeof(c));
+  c.fanout = 1;
+  c.max_batch = 1;
+  int rc = validate_dims(dims, &c);
+  if (rc) return rc;
+  if (N < 0 || E < 0) return STGN_ERR_INVALID;
+  if (N == 0) return STGN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Geo g = make_geo(*dims, 1);
+  int dev = 0, sms = 148;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  AttnLaunch al;
+  rc = plan_attn(g, true, sms, &al);
+  if (rc) return rc;
+  const int64_t nq = (int64_t)g.K * g.H * g.q_in * g.d_k;
+  const int64_t nk = (int64_t)g.K * g.H * g.k_in * g.d_k;
+  float* packed = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&packed, sizeof(float) * (nq + 2 * nk), st));
+  k_pack_attn<<<256, 256, 0, st>>>(g, wq, wk, wv, packed, packed + nq, packed + nq + nk);
+  AttnWeights aw;
+  aw.wq = packed;
+  aw.wkt = packed + nq;
+  aw.wv = packed + nq + nk;
+  aw.wo = wo;
+  aw.omega = omega;
+  aw.phi0 = phi0;
+  RingSrc rs;
+  memset(&rs, 0, sizeof(rs));
+  FlatSrc fs;
+  fs.N = N;
+  fs.offsets = offsets;
+  fs.qbase = qbase;
+  fs.payload = payload;
+  fs.feat = feat;
+  fs.dt = dt;
+  fs.out = out;
+  fs.scores = scores;
+  fs.values = values;
+  fs.maxlog = maxlog;
+  fs.zsum = zsum;
+  fs.qvecs = qvecs;
+  const int grid = (int)std::min<int64_t>(cdiv(N, al.T), al.grid);
+  al.fn<<<grid, STGN_THREADS, al.smem, st>>>(g, aw, rs, fs, al.T);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(packed, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return STGN_OK;
+}

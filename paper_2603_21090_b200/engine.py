@@ -1,0 +1,676 @@
+"""GPU-resident drop-in for the reference's IncrementalEngine (exact mode).
+
+Mirrors /root/reference/pkg/src/streamtgn/engine.py:155-453 — same
+constructor (RunConfig, ModelParameters), same `process_batch`,
+`rebuild_nodes`, `full_reference` and the read-side surface the runner and
+tests use (`memory`, `cache`, `nbr_cache`, `store`, `counters`,
+`scheduler`, `last_report`, `last_affected`, `last_pred_embeddings`).
+All state lives on the device in PyTorch-allocated tensors; each batch is
+one call into the C ABI (include/stgn.h), which replays a captured CUDA
+graph of the sm_100a kernels. There is no CPU fallback: without a GPU or
+the built library the constructor raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .config import ConfigError, RunConfig
+from .edges import (DriftContractError, FeatureDimError, MonotonicityError, NeighborEntry,
+                    edges_to_arrays)
+from .params import ModelParameters
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2603_21090_b200 needs a CUDA GPU (B200, sm_100a); "
+                           "there is no CPU fallback")
+    return torch
+
+
+def _rup(x, m):
+    return (x + m - 1) // m * m
+
+
+@dataclass
+class BatchReport:
+    """S/engine.py:32-40."""
+    index: int
+    edges: int
+    t_batch: float
+    direct: int
+    affected: int
+    rebuild: str = "none"
+    rebuild_nodes: int = 0
+
+
+@dataclass
+class ChangeRecordSize:
+    """Size of a node's change record (|added| + |expired| + |updated|)."""
+    size: int
+
+    @property
+    def empty(self) -> bool:
+        return self.size == 0
+
+
+@dataclass
+class AffectedSet:
+    """S/state.py:147-151 (records carry sizes only)."""
+    direct: set
+    all: set
+    records: dict = field(default_factory=dict)
+
+
+class Counters:
+    """S/state.py:209-227."""
+
+    def __init__(self):
+        self.totals: dict[str, float] = {}
+        self.batch: dict[str, float] = {}
+
+    def start_batch(self):
+        self.batch = {}
+
+    def add(self, key, amount=1):
+        self.batch[key] = self.batch.get(key, 0) + amount
+        self.totals[key] = self.totals.get(key, 0) + amount
+
+    def get(self, key):
+        return self.batch.get(key, 0)
+
+    def total(self, key):
+        return self.totals.get(key, 0)
+
+
+_REBUILD_NAMES = {0: "none", 1: "partial", 2: "full"}
+
+
+class _Tables:
+    """PyTorch-allocated device tables bound into the C engine."""
+
+    NODE_I32 = ("ring_cnt", "ring_head", "ring_ccnt", "nodecnt", "nodeadj", "nodefill",
+                "nodeoff", "cum_list")
+
+    def __init__(self, eng, cap_nodes, cap_edges, gpow_len):
+        torch = eng._torch
+        dev = eng.device
+        g = eng
+        self.cap_nodes, self.cap_edges = cap_nodes, cap_edges
+        z = lambda *s, dt=torch.float32: torch.zeros(*s, dtype=dt, device=dev)  # noqa: E731
+        N, L, K = cap_nodes, g.L, g.K
+        self.mem = z(N, g.ld_s)
+        self.last = z(N, dt=torch.float64)
+        self.version = z(N, dt=torch.int64)
+        self.h = z(N, K, g.ld_d)
+        self.valid = z(N, dt=torch.uint8)
+        self.valid_at = torch.full((N,), -math.inf, dtype=torch.float64, device=dev)
+        for name in self.NODE_I32:
+            setattr(self, name, z(N, dt=torch.int32))
+        self.ring_ccnt.fill_(-1)
+        self.ring_nbr = z(N, L, dt=torch.int32)
+        self.ring_eid = z(N, L, dt=torch.int64)
+        self.ring_t = z(N, L, dt=torch.float64)
+        self.ring_pay = z(N, K, L, g.ld_d)
+        self.ring_feat = z(N, L, g.ld_e)
+        self.amark = z(N, dt=torch.int32)
+        self.dmark = z(N, dt=torch.int32)
+        self.cum_mark = z(N, dt=torch.int32)
+        self.drift_acc = z(N, dt=torch.float64)
+        self.drift_touched = z(N, dt=torch.int64)
+        self.adj_head = torch.full((N,), -1, dtype=torch.int64, device=dev)
+        self.adj_deg = z(N, dt=torch.int64)
+        E = cap_edges
+        self.e_src = z(E, dt=torch.int32)
+        self.e_dst = z(E, dt=torch.int32)
+        self.e_t = z(E, dt=torch.float64)
+        self.e_feat = z(E, g.ld_e)
+        self.e_prev = torch.full((2 * E,), -1, dtype=torch.int64, device=dev)
+        self.gpow = torch.tensor([g.cfg.gamma ** k for k in range(gpow_len)],
+                                 dtype=torch.float64, device=dev)
+        self.ctl = z(_rup(C.sizeof(_lib.Ctl), 8) // 8, dt=torch.int64)
+        sb = eng._L.stgn_scratch_bytes(C.byref(eng._dims), C.byref(eng._cfgs), cap_nodes)
+        if sb < 0:
+            raise ConfigError("invalid dims/config for the CUDA engine")
+        self.scratch = z(int(sb), dt=torch.uint8)
+
+    def copy_from(self, old):
+        """Copy the live prefix of every table from a smaller instance."""
+        n, e = old.cap_nodes, old.cap_edges
+        for name, t in vars(old).items():
+            if name in ("cap_nodes", "cap_edges", "scratch"):
+                continue
+            if name == "gpow":
+                continue
+            if name == "ctl":
+                self.ctl.copy_(t)
+                continue
+            dst = getattr(self, name)
+            if name.startswith("e_"):
+                lim = 2 * e if name == "e_prev" else e
+            else:
+                lim = n
+            dst[:lim].copy_(t[:lim])
+
+    def struct(self) -> _lib.State:
+        s = _lib.State()
+        s.cap_nodes, s.cap_edges, s.gpow_len = self.cap_nodes, self.cap_edges, self.gpow.numel()
+        for name in _lib.STATE_PTRS:
+            setattr(s, name, getattr(self, name).data_ptr())
+        return s
+
+
+class _MemoryView:
+    """Read view of NodeMemoryTable (S/state.py:23-48)."""
+
+    def __init__(self, eng):
+        self._e = eng
+
+    @property
+    def states(self):
+        e = self._e
+        return e._tab.mem[:e._cap_view(), :e.dims.d_s].double().cpu().numpy()
+
+    @property
+    def last_interaction(self):
+        e = self._e
+        return e._tab.last[:e._cap_view()].cpu().numpy()
+
+    @property
+    def version(self):
+        e = self._e
+        return e._tab.version[:e._cap_view()].cpu().numpy()
+
+    @property
+    def n(self):
+        return self._e._n_mem
+
+
+class _CacheView:
+    """Read view of LayerCache (S/state.py:91-127)."""
+
+    def __init__(self, eng):
+        self._e = eng
+
+    @property
+    def h(self):
+        e = self._e
+        return e._tab.h[:e._cap_view(), :, :e.dims.d].double().cpu().numpy()
+
+    @property
+    def valid(self):
+        return self._e._tab.valid[:self._e._cap_view()].bool().cpu().numpy()
+
+    @property
+    def valid_at(self):
+        return self._e._tab.valid_at[:self._e._cap_view()].cpu().numpy()
+
+    def embeddings(self, n: int) -> np.ndarray:
+        e = self._e
+        e._ensure_nodes(n)
+        return e._tab.h[:n, e.K - 1, :e.dims.d].double().cpu().numpy()
+
+
+class _NeighborCacheView:
+    """Read view of NeighborCache (S/state.py:154-171): the ring prefix."""
+
+    def __init__(self, eng):
+        self._e = eng
+
+    def _list(self, v, length):
+        e = self._e
+        head = int(e._tab.ring_head[v])
+        slots = [(head + j) % e.L for j in range(length)]
+        nbr = e._tab.ring_nbr[v].cpu().numpy()
+        ts = e._tab.ring_t[v].cpu().numpy()
+        eid = e._tab.ring_eid[v].cpu().numpy()
+        return [NeighborEntry(int(nbr[s]), float(ts[s]), int(eid[s])) for s in slots]
+
+    def get(self, v):
+        e = self._e
+        if v < 0 or v >= e._tab.cap_nodes:
+            return None
+        cc = int(e._tab.ring_ccnt[v])
+        if cc < 0:
+            return None
+        return self._list(v, cc)
+
+    def __contains__(self, v):
+        return self.get(v) is not None
+
+
+class _StoreView:
+    """Read view of TemporalAdjacencyList (S/graph_store.py:102-198)."""
+
+    def __init__(self, eng):
+        self._e = eng
+
+    @property
+    def m(self):
+        return self._e._m
+
+    @property
+    def n(self):
+        return self._e._store_n
+
+    @property
+    def t_now(self):
+        return self._e._t_now
+
+    @property
+    def d_e(self):
+        return self._e.dims.d_e
+
+    def degree(self, v):
+        e = self._e
+        if v >= e._tab.cap_nodes:
+            return 0
+        return int(e._tab.adj_deg[v])
+
+    def _walk(self, v):
+        """Newest-first (nbr, t, eid) along the device chain."""
+        e = self._e
+        if v >= e._tab.cap_nodes:
+            return
+        ent = int(e._tab.adj_head[v])
+        src = e._tab.e_src
+        dst = e._tab.e_dst
+        while ent >= 0:
+            eid, side = ent >> 1, ent & 1
+            s, d = int(src[eid]), int(dst[eid])
+            yield (d if side == 0 else s), float(e._tab.e_t[eid]), eid
+            ent = int(e._tab.e_prev[ent])
+
+    def recent_upto(self, v, limit):
+        out = []
+        if limit <= 0:
+            return out
+        for nbr, t, eid in self._walk(v):
+            out.append(NeighborEntry(nbr, t, eid))
+            if len(out) == limit:
+                break
+        return out
+
+    def get_temporal_neighbors(self, v, t_start, t_end):
+        if t_start > t_end:
+            raise ValueError("t_start must be <= t_end")
+        out = []
+        for nbr, t, eid in self._walk(v):
+            if t > t_end:
+                continue
+            if t < t_start:
+                break
+            out.append(NeighborEntry(nbr, t, eid))
+        return out
+
+    def edge_feature(self, eid):
+        e = self._e
+        if eid >= e._m:
+            raise IndexError(f"edge id {eid} out of range")
+        return e._tab.e_feat[eid, :e.dims.d_e].double().cpu().numpy()
+
+    def feature_table(self):
+        e = self._e
+        return e._tab.e_feat[:e._m, :e.dims.d_e].double().cpu().numpy()
+
+
+class _SchedulerView:
+    """Read view of DriftScheduler (S/drift.py:26-96)."""
+
+    def __init__(self, eng):
+        self._e = eng
+
+    def _ctl(self):
+        raw = self._e._tab.ctl.cpu().numpy().tobytes()
+        return _lib.Ctl.from_buffer_copy(raw[:C.sizeof(_lib.Ctl)])
+
+    @property
+    def tau(self):
+        return int(self._ctl().tau)
+
+    @property
+    def gamma(self):
+        return self._e.cfg.gamma
+
+    def estimator(self, v):
+        e = self._e
+        acc = float(e._tab.drift_acc[v])
+        if acc == 0.0:
+            return 0.0
+        return acc * e.cfg.gamma ** (self.tau - int(e._tab.drift_touched[v]))
+
+    def global_drift(self):
+        ctl = self._ctl()
+        n = int(ctl.cum_count)
+        if n == 0:
+            return 0.0
+        e = self._e
+        ids = e._tab.cum_list[:n].long()
+        acc = e._tab.drift_acc[ids].cpu().numpy()
+        touched = e._tab.drift_touched[ids].cpu().numpy()
+        tau = int(ctl.tau)
+        tot = 0.0
+        for a, t in zip(acc, touched):
+            if a != 0.0:
+                tot += float(a) * e.cfg.gamma ** (tau - int(t))
+        return tot / n
+
+
+class IncrementalEngine:
+    """B200 exact-mode engine; see the module docstring.
+
+    recompute: "affected" recomputes every node of A (the reference's
+    literal exact mode, default); "direct" recomputes V_direct only, which is
+    value-identical when the window is infinite (keys/values come from
+    payloads frozen at insertion, so A minus V_direct has unchanged inputs).
+    """
+
+    def __init__(self, cfg: RunConfig, params: ModelParameters, *, recompute: str = "affected",
+                 max_batch: int | None = None, device: int | None = None):
+        cfg.validate()
+        if cfg.mode != "exact":
+            raise ConfigError("the B200 engine implements exact mode (delta mode is out of scope)")
+        if recompute not in _lib.SCOPE:
+            raise ConfigError(f"recompute must be one of {tuple(_lib.SCOPE)}")
+        self._torch = _torch()
+        torch = self._torch
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.cfg = cfg
+        self.params = params
+        self.dims = dm = params.dims
+        if dm != cfg.dims:
+            raise ConfigError("params.dims must equal cfg.dims")
+        self.K, self.L = dm.layers, cfg.fanout
+        self.ld_s, self.ld_d = _rup(dm.d_s, 4), _rup(dm.d, 4)
+        self.ld_e = _rup(max(dm.d_e, 1), 4)
+        self.recompute = recompute
+        self._L = _lib.lib()
+        self._dims = _lib.dims_struct(dm)
+        self._max_batch = max(int(max_batch or cfg.batch_size), 1)
+        self._handle = None
+        self._make_handle()
+        self._upload_weights()
+        cap_nodes = max(cfg.nodes, 16)
+        self._tab = _Tables(self, cap_nodes, max(1024, 4 * self._max_batch), 4096)
+        self._bind()
+        # host mirrors of the store / scheduler scalars
+        self._m = 0
+        self._t_now = -math.inf
+        self._store_n = 0
+        self._n_mem = cfg.nodes
+        self.batch_index = 0
+        self.counters = Counters()
+        self.last_report: BatchReport | None = None
+        self._last_nD = 0
+        self._last_nA = 0
+        self._affected_cache = None
+        self._pred_cache = None
+        self.memory = _MemoryView(self)
+        self.cache = _CacheView(self)
+        self.nbr_cache = _NeighborCacheView(self)
+        self.store = _StoreView(self)
+        self.scheduler = _SchedulerView(self)
+        self._rep = _lib.Report()
+        self._preds = np.zeros(self._max_batch, dtype=np.float64)
+
+    # -- plumbing -------------------------------------------------------------
+    def _stream(self):
+        return C.c_void_p(self._torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _make_handle(self):
+        cfg = self.cfg
+        self._cfgs = _lib.Config(cfg.fanout, _lib.AGG[cfg.aggregator], _lib.REBUILD[cfg.rebuild],
+                                 int(cfg.rebuild_interval), cfg.gamma, cfg.delta_max, cfg.alpha,
+                                 cfg.window, _lib.SCOPE[self.recompute], self._max_batch)
+        h = C.c_void_p()
+        with self._torch.cuda.device(self.device):
+            _lib.check(self._L.stgn_engine_create(C.byref(self._dims), C.byref(self._cfgs),
+                                                  C.byref(h)), "engine_create")
+        if self._handle is not None:
+            self._L.stgn_engine_destroy(self._handle)
+        self._handle = h
+
+    def _upload_weights(self):
+        torch = self._torch
+        p, dm = self.params, self.dims
+        K, H, d_k = dm.layers, dm.heads, dm.d_k
+        f32 = lambda a: torch.tensor(np.ascontiguousarray(a, dtype=np.float32), device=self.device)  # noqa
+        f64 = lambda a: torch.tensor(np.ascontiguousarray(a, dtype=np.float64), device=self.device)  # noqa
+        W = {
+            "wq": f32(np.transpose(p.w_q, (0, 2, 1, 3)).reshape(K, dm.query_in, H * d_k)),
+            "wkt": f32(np.transpose(p.w_k, (0, 1, 3, 2))),
+            "wv": f32(p.w_v),
+            "wo": f32(p.w_o),
+            "wmsg": f32(np.stack([p.w_msg_src.T, p.w_msg_dst.T])),
+            "bmsg": f32(np.stack([p.b_msg_src, p.b_msg_dst])),
+            "wgru": f32(np.stack([p.w_z.T, p.w_r.T, p.w_h.T])),
+            "ugru": f32(np.stack([p.u_z.T, p.u_r.T, p.u_h.T])),
+            "bgru": f32(np.stack([p.b_z, p.b_r, p.b_h])),
+            "wpred": f64(p.w_pred),
+            "omega": f64(p.omega),
+        }
+        ang = p.omega * 0.0
+        phi0 = np.empty(dm.d_t)
+        phi0[0::2], phi0[1::2] = np.cos(ang), np.sin(ang)
+        W["phi0"] = f32(phi0 * np.sqrt(1.0 / dm.d_t))
+        self._w = W
+        ws = _lib.Weights(**{k: v.data_ptr() for k, v in W.items()}, bpred=float(p.b_pred))
+        _lib.check(self._L.stgn_engine_set_weights(self._handle, C.byref(ws)), "set_weights")
+
+    def _bind(self):
+        self._state = self._tab.struct()
+        _lib.check(self._L.stgn_engine_bind(self._handle, C.byref(self._state)), "bind")
+
+    def _grow(self, need_nodes=0, need_edges=0, need_batch=0, need_gpow=0):
+        tab = self._tab
+        rebuild_handle = need_batch > self._max_batch
+        if rebuild_handle:
+            self._max_batch = max(need_batch, 2 * self._max_batch)
+            self._preds = np.zeros(self._max_batch, dtype=np.float64)
+            self._make_handle()
+            self._upload_weights()
+        n_cap, e_cap, g_len = tab.cap_nodes, tab.cap_edges, tab.gpow.numel()
+        if need_nodes > n_cap or need_edges > e_cap or need_gpow > g_len or rebuild_handle:
+            new_n = max(n_cap, need_nodes if need_nodes <= n_cap else max(need_nodes, 2 * n_cap))
+            new_e = max(e_cap, need_edges if need_edges <= e_cap else max(need_edges, 2 * e_cap))
+            new_g = max(g_len, need_gpow if need_gpow <= g_len else max(need_gpow, 2 * g_len))
+            if (new_n, new_e, new_g) != (n_cap, e_cap, g_len) or rebuild_handle:
+                self._torch.cuda.current_stream(self.device).synchronize()
+                fresh = _Tables(self, new_n, new_e, new_g)
+                fresh.copy_from(tab)
+                self._tab = fresh
+            self._bind()
+
+    def _ensure_nodes(self, n):
+        if n > self._tab.cap_nodes:
+            self._grow(need_nodes=n)
+        self._n_mem = max(self._n_mem, n)
+
+    def _cap_view(self):
+        return min(self._tab.cap_nodes, max(self.node_count, 16))
+
+    def __del__(self):
+        try:
+            if self._handle is not None:
+                self._L.stgn_engine_destroy(self._handle)
+        except Exception:
+            pass
+
+    # -- reference surface ---------------------------------------------------------
+    @property
+    def node_count(self) -> int:
+        return max(self._store_n, self._n_mem, self.cfg.nodes)
+
+    def process_batch(self, batch) -> list[float]:
+        """S/engine.py:400-438."""
+        src, dst, t, feat = edges_to_arrays(batch, self.dims.d_e)
+        return self.process_batch_arrays(src, dst, t, feat).tolist()
+
+    def process_batch_arrays(self, src, dst, t, feat=None) -> np.ndarray:
+        """Array form of process_batch: (B,) ids, (B,) float64 times,
+        (B, d_e) features; returns the (B,) float64 link scores."""
+        self.counters.start_batch()
+        self._affected_cache = None
+        self._pred_cache = None
+        src = np.ascontiguousarray(src, dtype=np.int64)
+        dst = np.ascontiguousarray(dst, dtype=np.int64)
+        t = np.ascontiguousarray(t, dtype=np.float64)
+        B = int(src.shape[0])
+        d_e = self.dims.d_e
+        if feat is None:
+            feat = np.zeros((B, d_e), dtype=np.float32)
+        feat = np.ascontiguousarray(feat, dtype=np.float32)
+        if feat.shape != (B, d_e) and not (d_e == 0 and feat.size == 0):
+            raise FeatureDimError(f"edge features have shape {feat.shape}, expected ({B}, {d_e})")
+        if B == 0:
+            self._last_nD = self._last_nA = 0
+            self.last_report = BatchReport(self.batch_index, 0, self._t_now, 0, 0)
+            return np.zeros(0)
+        if dst.shape[0] != B or t.shape[0] != B:
+            raise ValueError("src, dst and t must have the same length")
+        if (src < 0).any() or (dst < 0).any():
+            raise ValueError("node ids must be non-negative")
+        prev = np.concatenate([[self._t_now], t[:-1]])
+        bad = np.nonzero(t < prev)[0]
+        if bad.size:
+            j = int(bad[0])
+            raise MonotonicityError(
+                f"batch edge at t={t[j]} precedes committed history t={prev[j]}")
+        top = int(max(src.max(), dst.max())) + 1
+        n_after = max(self._n_mem, top, self.cfg.nodes, self._store_n)
+        self._grow(need_nodes=n_after, need_edges=self._m + B, need_batch=B,
+                   need_gpow=self.batch_index + 3)
+        self._n_mem = max(self._n_mem, top)
+        self.batch_index += 1
+        rc = self._L.stgn_engine_process_batch(
+            self._handle, B, src.astype(np.int32).ctypes.data, dst.astype(np.int32).ctypes.data,
+            t.ctypes.data, feat.ctypes.data, self._m, self.batch_index, self.node_count,
+            self._preds.ctypes.data, C.byref(self._rep), self._stream())
+        if rc:
+            self.batch_index -= 1
+            _lib.check(rc, "process_batch")
+        self._after_batch(B, float(t[-1]), top)
+        return self._preds[:B].copy()
+
+    def _after_batch(self, B, t_last, top):
+        r = self._rep
+        dm = self.dims
+        self._m += B
+        self._t_now = t_last
+        self._store_n = max(self._store_n, top)
+        self._last_nD, self._last_nA = int(r.direct), int(r.affected)
+        nD, nA = self._last_nD, self._last_nA
+        c = self.counters
+        c.add("nbr_hit", int(r.nbr_hit))
+        c.add("nbr_miss", int(r.nbr_miss))
+        c.add("embed_predict", nD)
+        c.add("embed_refresh", nA)
+        c.add("rows_gathered", nA + nD)
+        c.add("macs_attention", self._mac_attn(nA, int(r.entries_affected)) +
+              self._mac_attn(nD, int(r.entries_direct)))
+        c.add("messages", 2 * B)
+        c.add("macs_gru", 2 * B * dm.d_m * dm.msg_in +
+              nD * 3 * (dm.d_s * dm.d_m + dm.d_s * dm.d_s))
+        c.add("gru_steps", nD)
+        kind = _REBUILD_NAMES[int(r.rebuild_kind)]
+        rb = int(r.rebuild_nodes)
+        if kind != "none":
+            c.add("rows_gathered", rb)
+            c.add("macs_attention", self._mac_attn(rb, int(r.entries_rebuild)))
+            c.add("rebuild_pipelines", rb)
+            c.add("rebuilds")
+        c.add("direct", nD)
+        c.add("affected", nA)
+        self.last_global_drift = float(r.global_drift)
+        self.last_report = BatchReport(index=self.batch_index, edges=B, t_batch=t_last,
+                                       direct=nD, affected=nA, rebuild=kind, rebuild_nodes=rb)
+
+    def _mac_attn(self, n, e):
+        dm = self.dims
+        per_node = dm.heads * dm.query_in * dm.d_k + dm.heads * dm.d_k * dm.d
+        per_entry = dm.heads * (2 * dm.key_in * dm.d_k + 2 * dm.d_k)
+        return dm.layers * (n * per_node + e * per_entry)
+
+    def _fetch_lists(self):
+        """(direct ids in device order, affected ids, change-record sizes)."""
+        if self._affected_cache is None:
+            nD, nA = self._last_nD, self._last_nA
+            d = np.zeros(max(nD, 1), dtype=np.int32)
+            a = np.zeros(max(nA, 1), dtype=np.int32)
+            sz = np.zeros(max(nA, 1), dtype=np.int32)
+            gd, ga = C.c_int64(), C.c_int64()
+            _lib.check(self._L.stgn_engine_affected(self._handle, d.ctypes.data, a.ctypes.data,
+                                                    a.size, C.byref(gd), C.byref(ga),
+                                                    sz.ctypes.data, self._stream()), "affected")
+            self._affected_cache = (d[:nD], a[:nA], sz[:nA])
+        return self._affected_cache
+
+    @property
+    def last_affected(self) -> AffectedSet | None:
+        if self.last_report is None:
+            return None
+        d, a, sz = self._fetch_lists()
+        recs = {int(v): ChangeRecordSize(int(s)) for v, s in zip(a, sz)}
+        return AffectedSet(set(d.tolist()), set(a.tolist()), recs)
+
+    @property
+    def last_pred_embeddings(self) -> dict:
+        if self._pred_cache is None:
+            nD = self._last_nD
+            self._pred_cache = {}
+            if nD:
+                d, _, _ = self._fetch_lists()
+                out = np.zeros((nD, self.dims.d), dtype=np.float32)
+                _lib.check(self._L.stgn_engine_pred_embeddings(self._handle, out.ctypes.data, nD,
+                                                               self._stream()), "pred_emb")
+                self._pred_cache = {int(v): out[i].astype(np.float64) for i, v in enumerate(d)}
+        return self._pred_cache
+
+    def rebuild_nodes(self, nodes) -> int:
+        """S/engine.py:385-396."""
+        n = self.node_count
+        if nodes is not None:
+            ids = np.array(sorted(nodes), dtype=np.int32)
+            if ids.size == 0:
+                return 0
+            self._ensure_nodes(int(ids.max()) + 1)
+            n = self.node_count
+            ptr, cnt = ids.ctypes.data, ids.size
+        else:
+            if n == 0:
+                return 0
+            self._ensure_nodes(n)
+            ptr, cnt = None, 0
+        out = C.c_int64()
+        valid_at = self._t_now if self._m else 0.0
+        _lib.check(self._L.stgn_engine_rebuild(self._handle, ptr, cnt, n, valid_at, C.byref(out),
+                                               self._stream()), "rebuild")
+        self.counters.add("rebuild_pipelines", int(out.value))
+        return int(out.value)
+
+    def full_reference(self) -> np.ndarray:
+        """S/engine.py:374-381 (read-only)."""
+        torch = self._torch
+        n = self.node_count
+        self._ensure_nodes(n)
+        out = torch.empty((max(n, 1), self.ld_d), dtype=torch.float32, device=self.device)
+        if n:
+            _lib.check(self._L.stgn_engine_full_reference(self._handle, n, out.data_ptr(),
+                                                          self._stream()), "full_reference")
+        return out[:n, :self.dims.d].double().cpu().numpy()
+
+    # convenience for the scheduler API
+    def execute_rebuild(self, decision) -> int:
+        if decision is None:
+            raise DriftContractError("execute_rebuild needs a non-None decision")
+        kind, nodes = decision
+        return self.rebuild_nodes(sorted(nodes) if kind == "partial" else None)
+
+    def sync(self):
+        self._torch.cuda.current_stream(self.device).synchronize()

@@ -1,0 +1,170 @@
+"""GPU parity: the CUDA path through the C ABI against fixtures written by
+the reference (tests/golden) and against the pinned oracle on fresh
+streams. Runs on a B200 under gpurun (`pytest -m gpu`)."""
+
+import numpy as np
+import pytest
+
+from golden_util import batches, case_setup, engine_cases, load, pipeline_cases
+from parity_util import PRED_ATOL, assert_rows_close, row_rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2603_21090_b200 import _lib
+    _lib.lib()
+    return torch
+
+
+@pytest.mark.parametrize("name", pipeline_cases())
+def test_pipeline_many_matches_reference(cuda, name):
+    from paper_2603_21090_b200.kernels import pipeline_many
+    z = load("pipeline_" + name)
+    outs = pipeline_many(z["qbase"], z["offsets"], z["payload"], z["feat"], z["dt"], z["omega"],
+                         z["phi0"], z["wq"], z["wk"], z["wv"], z["wo"])
+    out, scores, values, maxlog, zsum, qvecs = outs
+    N, K = out.shape[:2]
+    assert_rows_close(out.reshape(N * K, -1), z["out"].reshape(N * K, -1), "out")
+    assert_rows_close(qvecs.reshape(N, -1), z["qvecs"].reshape(N, -1), "qvecs")
+    E = values.shape[0]
+    if E:
+        assert_rows_close(values.reshape(E, -1), z["values"].reshape(E, -1), "values")
+        np.testing.assert_allclose(scores, z["scores"], rtol=2e-4, atol=1e-6)
+    fin = np.isfinite(z["maxlog"])
+    assert np.array_equal(fin, np.isfinite(maxlog))
+    np.testing.assert_allclose(maxlog[fin], z["maxlog"][fin], rtol=1e-4, atol=1e-5)
+    np.testing.assert_allclose(zsum, z["zsum"], rtol=1e-4, atol=1e-6)
+
+
+def _run_engine(name, recompute="affected"):
+    from paper_2603_21090_b200.engine import IncrementalEngine
+    z = load("engine_" + name)
+    cfg, params, stream = case_setup(z)
+    eng = IncrementalEngine(cfg, params, recompute=recompute)
+    preds, aff, dirs, kinds, cnts, counters = [], [], [], [], [], []
+    keys = list(z["counter_keys"])
+    for b in batches(stream, cfg.batch_size):
+        preds.extend(eng.process_batch_arrays(b.src, b.dst, b.t, b.feat).tolist())
+        la = eng.last_affected
+        aff.extend(sorted(la.all))
+        dirs.extend(sorted(la.direct))
+        kinds.append({"none": 0, "partial": 1, "full": 2}[eng.last_report.rebuild])
+        cnts.append(eng.last_report.rebuild_nodes)
+        counters.append([eng.counters.get(k) for k in keys])
+    return z, cfg, eng, preds, aff, dirs, kinds, cnts, counters
+
+
+@pytest.mark.parametrize("name", engine_cases())
+def test_engine_matches_reference(cuda, name):
+    z, cfg, eng, preds, aff, dirs, kinds, cnts, counters = _run_engine(name)
+    # integer-exact: affected set, direct set, rebuild decisions, counters
+    assert np.array_equal(np.array(aff), z["affected"]), "affected sets differ"
+    assert np.array_equal(np.array(dirs), z["direct"]), "direct sets differ"
+    assert np.array_equal(np.array(kinds), z["rebuild_kind"]), "rebuild decisions differ"
+    assert np.array_equal(np.array(cnts), z["rebuild_cnt"])
+    np.testing.assert_array_equal(np.array(counters, dtype=np.float64), z["counters"])
+    n = int(z["node_count"])
+    assert eng.node_count == n
+    # sampled neighbour lists (nbr, eid, t), bit-exact
+    for v in range(n):
+        lst = eng.nbr_cache.get(v)
+        c = int(z["cache_cnt"][v])
+        if c < 0:
+            assert lst is None, v
+            continue
+        assert [e.nbr for e in lst] == list(z["cache_nbr"][v, :c]), v
+        assert [e.edge_id for e in lst] == list(z["cache_eid"][v, :c]), v
+        assert [e.t for e in lst] == list(z["cache_t"][v, :c]), v
+    # floating point within the stated tolerance
+    assert np.max(np.abs(np.array(preds) - z["preds"])) <= PRED_ATOL
+    assert_rows_close(eng.memory.states[:n], z["memory"], "memory")
+    np.testing.assert_array_equal(eng.memory.last_interaction[:n], z["last"])
+    np.testing.assert_array_equal(eng.memory.version[:n], z["version"])
+    assert_rows_close(eng.cache.h[:n].reshape(n, -1), z["h"].reshape(n, -1), "layer cache")
+    np.testing.assert_array_equal(eng.cache.valid_at[:n], z["valid_at"])
+    assert_rows_close(eng.full_reference(), z["full_reference"], "full_reference")
+    assert eng.scheduler.tau == int(z["tau"])
+    assert eng.scheduler.global_drift() == pytest.approx(float(z["global_drift"]), rel=1e-12)
+
+
+@pytest.mark.parametrize("name", ["small_mean", "k2_wide_adaptive", "c4_shape_tiny"])
+def test_direct_scope_is_value_identical(cuda, name):
+    a = _run_engine(name, "affected")
+    d = _run_engine(name, "direct")
+    n = int(a[0]["node_count"])
+    assert a[4] == d[4] and a[5] == d[5]
+    assert a[3] == d[3]  # predictions bit-identical
+    np.testing.assert_array_equal(a[2].cache.h[:n], d[2].cache.h[:n])
+    np.testing.assert_array_equal(a[2].memory.states[:n], d[2].memory.states[:n])
+
+
+def test_engine_vs_oracle_fresh_stream(cuda):
+    """C1-shaped widths on a fresh preferential stream, against the oracle."""
+    from oracle.stgn_oracle import Oracle
+    from paper_2603_21090_b200.config import Dims, RunConfig
+    from paper_2603_21090_b200.engine import IncrementalEngine
+    from paper_2603_21090_b200.params import init_params
+    from paper_2603_21090_b200.streamio import generate_stream
+    dims = Dims(d_s=100, d_e=172, d_t=100, d_m=100, d_k=50, heads=2, layers=1)
+    cfg = RunConfig(dims=dims, batch_size=200, fanout=10, nodes=1000)
+    params = init_params(0, dims)
+    stream = generate_stream(0, 1000, 6000, attachment="preferential", d_e=172)
+    eng = IncrementalEngine(cfg, params)
+    orc = Oracle(cfg, params)
+    worst = 0.0
+    for b in batches(stream, 200):
+        p = eng.process_batch_arrays(b.src, b.dst, b.t, b.feat)
+        q = orc.process_batch(b.src, b.dst, b.t, b.feat)
+        assert eng.last_affected.all == orc.last_all
+        worst = max(worst, float(np.max(np.abs(p - np.array(q)))))
+    assert worst <= PRED_ATOL
+    n = orc.node_count
+    assert_rows_close(eng.memory.states[:n], orc.mem[:n], "memory")
+    assert_rows_close(eng.cache.h[:n].reshape(n, -1), orc.h[:n].reshape(n, -1), "h")
+
+
+def test_monotonicity_error_before_mutation(cuda):
+    from paper_2603_21090_b200.config import Dims, RunConfig
+    from paper_2603_21090_b200.edges import MonotonicityError, TemporalEdge
+    from paper_2603_21090_b200.engine import IncrementalEngine
+    from paper_2603_21090_b200.params import init_params
+    dims = Dims(d_s=6, d_e=3, d_t=6, d_m=5, d_k=4, heads=2, layers=1)
+    eng = IncrementalEngine(RunConfig(dims=dims, batch_size=2, fanout=4, nodes=4),
+                            init_params(1, dims))
+    eng.process_batch([TemporalEdge(0, 1, 5.0, np.zeros(3))])
+    mem = eng.memory.states.copy()
+    with pytest.raises(MonotonicityError):
+        eng.process_batch([TemporalEdge(1, 2, 3.0, np.zeros(3))])
+    np.testing.assert_array_equal(eng.memory.states, mem)
+    assert eng.process_batch([]) == []
+    assert eng.counters.get("embed_refresh") == 0
+
+
+def test_rebuild_nodes_api_matches_oracle(cuda):
+    from oracle.stgn_oracle import Oracle
+    from paper_2603_21090_b200.engine import IncrementalEngine
+    z = load("engine_k2_mean_b1")
+    cfg, params, stream = case_setup(z)
+    eng = IncrementalEngine(cfg, params)
+    orc = Oracle(cfg, params)
+    for b in batches(stream, 5):
+        eng.process_batch_arrays(b.src, b.dst, b.t, b.feat)
+        orc.process_batch(b.src, b.dst, b.t, b.feat)
+    assert eng.rebuild_nodes([3, 1, 7]) == orc.rebuild_nodes([3, 1, 7]) == 3
+    assert eng.rebuild_nodes(None) == orc.rebuild_nodes(None)
+    n = orc.node_count
+    assert_rows_close(eng.cache.h[:n].reshape(n, -1), orc.h[:n].reshape(n, -1), "h")
+    for v in range(n):
+        a, b = eng.nbr_cache.get(v), orc.neighbor_list(v)
+        assert (a is None) == (b is None)
+        if a is not None:
+            assert [(e.nbr, e.edge_id) for e in a] == [(x[0], x[2]) for x in b]
+    # the append-only store agrees with the oracle's adjacency
+    for v in range(n):
+        assert [(e.nbr, e.edge_id) for e in eng.store.recent_upto(v, 100)] == \
+               [(x[0], x[2]) for x in orc.store.recent(v, 100)]
