@@ -227,6 +227,9 @@ int stgn_pipeline_many(const stgn_dims* dims, int64_t N, int64_t E, const float*
 /* Library version string and the sm architecture it was built for. */
 const char* stgn_version(void);
 
+/* Description of the last CUDA failure in this thread (file:line: message). */
+const char* stgn_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

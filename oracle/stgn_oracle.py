@@ -331,8 +331,14 @@ class Oracle:
         return out
 
     # -- the batch -----------------------------------------------------------
-    def process_batch(self, src, dst, t, feat):
-        """Arrays in, list of prediction floats out (S/engine.py:400-438)."""
+    def process_batch(self, src, dst, t, feat, compute=True):
+        """Arrays in, list of prediction floats out (S/engine.py:400-438).
+
+        compute=False is a fast-forward used only to position the CPU
+        baseline deep in a stream: topology, caches, memory and drift are
+        updated exactly, the attention recomputes are skipped (their cost
+        depends on topology only, their values feed nothing but h)."""
+        self._compute = compute
         self.counters = {}
         self.last_pred_h = {}
         src = np.asarray(src, dtype=np.int64)
@@ -409,7 +415,7 @@ class Oracle:
             self.cache[v] = kept
         # stages 2-4: recompute sorted(A) with pre-batch memory
         ids = sorted(A)
-        out = self._recompute(ids, t_batch)
+        out = self._recompute(ids, t_batch) if compute else np.zeros((len(ids), K, self.d))
         for v in ids:
             self._count("embed_predict" if v in direct else "embed_refresh")
         hK = {v: out[i, K - 1] for i, v in enumerate(ids)}
@@ -439,7 +445,8 @@ class Oracle:
         self._pending = {}
         dlist = self._memory_step(src, dst, t, feat)
         if dlist:
-            self._recompute(dlist, t_batch)
+            if compute:
+                self._recompute(dlist, t_batch)
             self._count("embed_refresh", len(dlist))
         changes = {}
         for v in A:
@@ -559,7 +566,8 @@ class Oracle:
             if self.cache.get(v) is None:
                 self.cache[v] = self.store.recent(v, self.L)
         self._pending = {}
-        self._recompute(ids, self.t_now if self.m else 0.0)
+        if getattr(self, "_compute", True):
+            self._recompute(ids, self.t_now if self.m else 0.0)
         self._count("rebuild_pipelines", len(ids))
         return len(ids)
 

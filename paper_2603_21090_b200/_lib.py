@@ -21,7 +21,7 @@ SCOPE = {"affected": 0, "direct": 1}
 
 # Symbols include/stgn.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = (
-    "stgn_version", "stgn_scratch_bytes", "stgn_engine_create", "stgn_engine_destroy",
+    "stgn_version", "stgn_last_error", "stgn_scratch_bytes", "stgn_engine_create", "stgn_engine_destroy",
     "stgn_engine_set_weights", "stgn_engine_bind", "stgn_engine_process_batch",
     "stgn_engine_process_batch_dev", "stgn_engine_rebuild", "stgn_engine_full_reference",
     "stgn_engine_affected", "stgn_engine_pred_embeddings", "stgn_pipeline_many",
@@ -87,6 +87,7 @@ def lib():
     vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
     P = C.POINTER
     L.stgn_version.restype = C.c_char_p
+    L.stgn_last_error.restype = C.c_char_p
     L.stgn_scratch_bytes.restype = i64
     L.stgn_scratch_bytes.argtypes = [P(Dims), P(Config), i64]
     L.stgn_engine_create.argtypes = [P(Dims), P(Config), P(vp)]
@@ -103,7 +104,7 @@ def lib():
     L.stgn_engine_pred_embeddings.argtypes = [vp, vp, i64, vp]
     L.stgn_pipeline_many.argtypes = [P(Dims), i64, i64] + [vp] * 18
     for name in EXPORTS:
-        if name not in ("stgn_version", "stgn_scratch_bytes"):
+        if name not in ("stgn_version", "stgn_last_error", "stgn_scratch_bytes"):
             getattr(L, name).restype = C.c_int
     _LIB = L
     return L
@@ -121,7 +122,8 @@ def check(rc: int, what: str = "") -> None:
         raise MonotonicityError(msg)
     if rc == STGN_ERR_CAPACITY:
         raise KernelInputError(msg + " (capacity)")
-    raise RuntimeError(msg + " (CUDA failure)")
+    detail = _LIB.stgn_last_error().decode() if _LIB is not None else ""
+    raise RuntimeError(f"{msg} (CUDA failure: {detail})")
 
 
 def dims_struct(dims) -> Dims:

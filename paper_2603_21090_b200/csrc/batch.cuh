@@ -542,7 +542,7 @@ k_gru(Geo g, StateView st, Scratch s, const float* wgru, const float* ugru, cons
 __global__ void k_drift_record(StateView st, Scratch s) {
   const int nA = s.res->nA;
   const int64_t tau = st.ctl->tau + 1;
-  const uint32_t gen = st.ctl->cum_gen;
+  const uint32_t gen = st.ctl->cum_gen + 1;  // cum_mark starts at 0 = "never"
   GRID_STRIDE(a64, nA) {
     const int a = (int)a64;
     const int v = s.alist[a];

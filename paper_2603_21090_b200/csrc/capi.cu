@@ -111,9 +111,18 @@ static int validate_dims(const stgn_dims* d, const stgn_config* c) {
   return STGN_OK;
 }
 
+static thread_local char g_err[512] = "";
+
+void stgn_set_error(const char* file, int line, cudaError_t e) {
+  snprintf(g_err, sizeof(g_err), "%s:%d: %s (%s)", file, line, cudaGetErrorString(e),
+           cudaGetErrorName(e));
+}
+
 extern "C" {
 
 const char* stgn_version(void) { return STGN_VERSION; }
+
+const char* stgn_last_error(void) { return g_err; }
 
 int64_t stgn_scratch_bytes(const stgn_dims* dims, const stgn_config* cfg, int64_t cap_nodes) {
   if (validate_dims(dims, cfg) != STGN_OK) return -1;
@@ -132,8 +141,10 @@ int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engin
   if (std::isfinite(cfg->window)) e->cfg.scope = STGN_SCOPE_AFFECTED;  // A\D can change
   e->g = make_geo(*dims, cfg->fanout);
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+  cudaError_t ce = cudaGetDevice(&dev);
+  if (ce == cudaSuccess) ce = cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (ce != cudaSuccess) {
+    stgn_set_error(__FILE__, __LINE__, ce);
     delete e;
     return STGN_ERR_CUDA;
   }
@@ -148,21 +159,26 @@ int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engin
     delete e;
     return STGN_ERR_INVALID;
   }
-  if (cudaFuncSetAttribute((const void*)k_messages, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)e->msg_smem) != cudaSuccess ||
-      cudaFuncSetAttribute((const void*)k_gru, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)e->gru_smem) != cudaSuccess) {
+  ce = cudaFuncSetAttribute((const void*)k_messages, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)e->msg_smem);
+  if (ce == cudaSuccess)
+    ce = cudaFuncSetAttribute((const void*)k_gru, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)e->gru_smem);
+  if (ce != cudaSuccess) {
+    stgn_set_error(__FILE__, __LINE__, ce);
     delete e;
     return STGN_ERR_CUDA;
   }
   Scratch tmp;
-  uint8_t* fake = reinterpret_cast<uint8_t*>(0);
-  scratch_layout(e->g, cfg->max_batch, 1, &tmp, fake + 0);
+  uint8_t* fake = reinterpret_cast<uint8_t*>((uintptr_t)4096);  // offsets only
+  scratch_layout(e->g, cfg->max_batch, 1, &tmp, fake);
   e->in_bytes = (int64_t)((uint8_t*)(tmp.in_feat + (int64_t)cfg->max_batch * e->g.ld_e) - fake);
-  if (cudaMallocHost((void**)&e->h_in, e->in_bytes) != cudaSuccess ||
-      cudaMallocHost((void**)&e->h_res, sizeof(BatchRes)) != cudaSuccess ||
-      cudaMallocHost((void**)&e->h_preds, sizeof(double) * cfg->max_batch) != cudaSuccess) {
-    delete e;
+  ce = cudaMallocHost((void**)&e->h_in, e->in_bytes);
+  if (ce == cudaSuccess) ce = cudaMallocHost((void**)&e->h_res, sizeof(BatchRes));
+  if (ce == cudaSuccess) ce = cudaMallocHost((void**)&e->h_preds, sizeof(double) * cfg->max_batch);
+  if (ce != cudaSuccess) {
+    stgn_set_error(__FILE__, __LINE__, ce);
+    stgn_engine_destroy(e);
     return STGN_ERR_CUDA;
   }
   memset(e->h_in, 0, e->in_bytes);

@@ -169,8 +169,14 @@ __device__ __forceinline__ float phi_component(const double* __restrict__ omega,
 
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + expf(-x)); }
 
+// Last CUDA failure (file:line + message), readable through stgn_last_error().
+void stgn_set_error(const char* file, int line, cudaError_t e);
+
 #define CUDA_TRY(expr)                                        \
   do {                                                        \
     cudaError_t _e = (expr);                                  \
-    if (_e != cudaSuccess) return STGN_ERR_CUDA;              \
+    if (_e != cudaSuccess) {                                  \
+      stgn_set_error(__FILE__, __LINE__, _e);                 \
+      return STGN_ERR_CUDA;                                   \
+    }                                                         \
   } while (0)

@@ -548,8 +548,10 @@ class IncrementalEngine:
                    need_gpow=self.batch_index + 3)
         self._n_mem = max(self._n_mem, top)
         self.batch_index += 1
+        src32 = src.astype(np.int32)   # keep the converted arrays alive across the call
+        dst32 = dst.astype(np.int32)
         rc = self._L.stgn_engine_process_batch(
-            self._handle, B, src.astype(np.int32).ctypes.data, dst.astype(np.int32).ctypes.data,
+            self._handle, B, src32.ctypes.data, dst32.ctypes.data,
             t.ctypes.data, feat.ctypes.data, self._m, self.batch_index, self.node_count,
             self._preds.ctypes.data, C.byref(self._rep), self._stream())
         if rc:
