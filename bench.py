@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""Headline benchmark: streamed edges/s and p50/p99 batch latency of the
+StreamTGN exact-mode incremental path (2-layer TGN, 2.6M nodes), B200.
+
+Workload (BASELINE.json metric; SURVEY.md §8d config C4 at B=600):
+  dims d_s=d_m=d_t=100, d_k=50, H=2, K=2, d_e=0, L=10, aggregator last,
+  drift-aware rebuild (adaptive, gamma=0.9, delta_max=0.5, alpha=0.1),
+  init_params(0), synthetic preferential power-law stream
+  generate_stream(seed=2, n=2.6M, ...) (the reference's generator, same
+  edges). The engine first ingests the stream's first 120K edges (the
+  window the reference CPU path is quoted on), then W warm-up batches,
+  then K timed batches of 600 edges.
+
+One JSON line (rank 0). `value` = device-timed throughput with inputs
+already in HBM (CUDA events on the engine stream, max over ranks);
+`e2e` = the same metric through the public host-buffer API
+(process_batch_arrays: H2D of the batch + D2H of the scores per step).
+Inputs are larger than L2 (26 GB of resident state; each batch touches
+fresh rings), so no explicit flush.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "streamed edges/sec and p50/p99 batch latency (2-layer TGN, 2.6M nodes)"
+UNIT = "edges/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=600)
+    ap.add_argument("--nodes", type=int, default=2_600_000)
+    ap.add_argument("--prefix", type=int, default=120_000)
+    ap.add_argument("--seed", type=int, default=2)
+    ap.add_argument("--rebuild", default="adaptive")
+    ap.add_argument("--recompute", default="affected", choices=["affected", "direct"])
+    ap.add_argument("--cpu-batches", type=int, default=6)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-batches", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+def workload(args):
+    from paper_2603_21090_b200.config import Dims, RunConfig
+    from paper_2603_21090_b200.params import init_params
+    dims = Dims(d_s=100, d_e=0, d_t=100, d_x=0, d_m=100, d_k=50, heads=2, layers=2)
+    cfg = RunConfig(dims=dims, batch_size=args.batch, fanout=10, nodes=args.nodes,
+                    aggregator="last", rebuild=args.rebuild, gamma=0.9, delta_max=0.5,
+                    alpha=0.1, seed=0)
+    return dims, cfg, init_params(0, dims)
+
+
+def config_json(args, n_gpus):
+    return {"workload": "C4: TGN 2-layer exact-mode incremental inference, synthetic "
+                        "preferential power-law stream, drift-aware rebuild",
+            "nodes": args.nodes, "batch_edges": args.batch, "fanout_L": 10, "layers_K": 2,
+            "d_memory": 100, "d_time": 100, "heads": 2, "d_k": 50, "d_edge": 0,
+            "stream": f"generate_stream(seed={args.seed}+rank, preferential), first "
+                      f"{args.prefix} edges ingested before warm-up",
+            "rebuild": args.rebuild, "recompute": args.recompute,
+            "parallelism": f"replicas{n_gpus}" if n_gpus > 1 else "single",
+            "l2": "inputs larger than L2 (26 GB resident state), no flush"}
+
+
+def make_stream(args, n_edges, rank):
+    from paper_2603_21090_b200.streamio import generate_stream
+    return generate_stream(args.seed + rank, args.nodes, n_edges, attachment="preferential",
+                           d_e=0)
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.tmp, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.tmp.flush()
+        rows = []
+        with open(self.tmp.name) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.tmp.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({nm for r in rows for nm, v in zip(names, r[5:9]) if v == "Active"})
+        busy = [x for x in sm if x > 0.5 * mx] or sm
+        return {"sm_mhz": float(np.median(busy)), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference(args, B_count, stream_edges=None):
+    """Time the oracle port (the reference algorithm restated in float64,
+    numba kernel like the reference's) on the same stream window: fast-
+    forward the prefix exactly (topology, caches, memory, drift), then time
+    B_count full batches. Returns (edges/s, per-batch seconds, sample)."""
+    from oracle.stgn_oracle import Oracle, pipeline_many
+    dims, cfg, params = workload(args)
+    B = args.batch
+    st = stream_edges or make_stream(args, args.prefix + B_count * B, 0)
+    orc = Oracle(cfg, params)
+    # compile the numba kernel outside the timed batches
+    pipeline_many(np.zeros((1, 100)), np.array([0, 1]), np.zeros((1, 2, 100)), np.zeros((1, 0)),
+                  np.zeros(1), params.omega, np.ones(100), params.w_q, params.w_k, params.w_v,
+                  params.w_o)
+    for lo in range(0, args.prefix, B):
+        orc.process_batch(st.src[lo:lo + B], st.dst[lo:lo + B], st.t[lo:lo + B],
+                          st.feat[lo:lo + B], compute=False)
+    times = []
+    for k in range(B_count):
+        lo = args.prefix + k * B
+        t0 = time.perf_counter()
+        orc.process_batch(st.src[lo:lo + B], st.dst[lo:lo + B], st.t[lo:lo + B],
+                          st.feat[lo:lo + B])
+        times.append(time.perf_counter() - t0)
+    times = np.array(times)
+    sample = (f"oracle port (float64 numpy+numba, 1 thread) on batches {args.prefix // B}.."
+              f"{args.prefix // B + B_count - 1} of the same stream ({B_count} x {B} edges) "
+              f"after an exact fast-forward through the first {args.prefix} edges")
+    return B_count * B / float(times.sum()), times, sample
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    dims, cfg, params = workload(args)
+    steps = max(1, args.cpu_batches)
+    value, times, sample = cpu_reference(args, steps)
+    ms = float(times.mean() * 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": 0, "ms_per_step": ms, "p50_ms": float(np.percentile(times, 50) * 1e3),
+        "p99_ms": float(np.percentile(times, 99) * 1e3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_json(args, 1), "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, world, rank, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_21090_b200.engine import IncrementalEngine
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dims, cfg, params = workload(args)
+    B, W, K = args.batch, args.warmup, args.steps
+    KE = args.e2e_steps if args.e2e_steps is not None else min(K, 100)
+    P = args.profile_batches
+    n_edges = args.prefix + (W + K + KE + P) * B
+    st = make_stream(args, n_edges, rank)
+    eng = IncrementalEngine(cfg, params, recompute=args.recompute)
+    # 1) ingest the prefix through the public API (untimed)
+    for lo in range(0, args.prefix, B):
+        eng.process_batch_arrays(st.src[lo:lo + B], st.dst[lo:lo + B], st.t[lo:lo + B])
+    eng.sync()
+    pos = args.prefix
+    # 2) device-resident inputs for warm-up + timed batches
+    batches = []
+    for k in range(W + K):
+        lo = pos + k * B
+        sl = slice(lo, lo + B)
+        batches.append((torch.tensor(st.src[sl].astype(np.int32), device=dev),
+                        torch.tensor(st.dst[sl].astype(np.int32), device=dev),
+                        torch.tensor(st.t[sl], device=dev),
+                        int(max(st.src[sl].max(), st.dst[sl].max())),
+                        float(st.t[sl][0]), float(st.t[sl][-1])))
+    torch.cuda.synchronize()
+    for k in range(W):
+        s_, d_, t_, mx, t0, t1 = batches[k]
+        eng.process_batch_device(s_, d_, t_, max_id=mx, t_first=t0, t_last=t1)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)  # let the sampler attach before the timed region
+    ev[0].record(stream)
+    for k in range(K):
+        s_, d_, t_, mx, t0, t1 = batches[W + k]
+        eng.process_batch_device(s_, d_, t_, max_id=mx, t_first=t0, t_last=t1)
+        ev[k + 1].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    per = np.array([ev[k].elapsed_time(ev[k + 1]) for k in range(K)])  # ms
+    total_ms = float(ev[0].elapsed_time(ev[K]))
+    if world > 1:
+        tt = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    value = world * K * B / (total_ms / 1e3)
+    pos += (W + K) * B
+
+    # 3) e2e: public host-buffer API, H2D + D2H inside every step
+    e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    host = [(np.ascontiguousarray(st.src[pos + k * B: pos + (k + 1) * B]),
+             np.ascontiguousarray(st.dst[pos + k * B: pos + (k + 1) * B]),
+             np.ascontiguousarray(st.t[pos + k * B: pos + (k + 1) * B])) for k in range(KE)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e_ev[0].record(stream)
+    t_wall = time.perf_counter()
+    e2e_lat = []
+    for s_, d_, t_ in host:
+        t1 = time.perf_counter()
+        eng.process_batch_arrays(s_, d_, t_)
+        e2e_lat.append(time.perf_counter() - t1)
+    e_ev[1].record(stream)
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall
+    e2e_ms = float(e_ev[0].elapsed_time(e_ev[1]))
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = world * KE * B / (e2e_ms / 1e3)
+    pos += KE * B
+
+    # 4) per-stage device times (events, no graph) for the roofline
+    eng.set_profiling(True)
+    stage_acc, attn_bytes, attn_flops, attn_ms, nA_list = {}, [], [], [], []
+    g = dims
+    for k in range(P):
+        sl = slice(pos + k * B, pos + (k + 1) * B)
+        eng.process_batch_arrays(st.src[sl], st.dst[sl], st.t[sl])
+        times, launches = eng.stage_times()
+        for nm, v in times.items():
+            stage_acc.setdefault(nm, []).append(v)
+        r = eng._rep
+        nA, EA = int(r.affected), int(r.entries_affected)
+        # algorithmic bytes: per node mem row + ring meta + K*d output,
+        # per entry K*d frozen payload + d_e feat + 8 B timestamp
+        by = nA * (4 * g.d_s + 4 * g.layers * g.d + 16) + EA * (4 * g.layers * g.d + 4 * g.d_e + 8)
+        # FLOPs of the folded formulation actually executed
+        per_node_l = 2 * (g.query_in * g.heads * g.d_k + g.heads * g.d_k * g.key_in +
+                          g.heads * g.key_in * g.d_k + g.heads * g.d_k * g.d)
+        per_entry_l = 2 * (2 * g.heads * g.key_in)
+        fl = g.layers * (nA * per_node_l + EA * per_entry_l)
+        attn_bytes.append(by)
+        attn_flops.append(fl)
+        attn_ms.append(times["recompute_affected"])
+        nA_list.append(nA)
+    eng.set_profiling(False)
+    stage_ms = {nm: float(np.mean(v)) for nm, v in stage_acc.items()}
+    a_ms = float(np.mean(attn_ms))
+    achieved_gbs = float(np.mean(attn_bytes)) / (a_ms / 1e3) / 1e9
+    peaks = {}
+    pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk_path):
+        with open(pk_path) as fh:
+            peaks = json.load(fh)
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    line = None
+    if rank == 0:
+        h2d = B * (4 + 4 + 8) + 64
+        d2h = B * 8 + 128
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": total_ms / K,
+            "p50_ms": float(np.percentile(per, 50)), "p99_ms": float(np.percentile(per, 99)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference generator, random-init weights)",
+            "config": config_json(args, world),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "p50_ms": float(np.percentile(e2e_lat, 50) * 1e3),
+                    "p99_ms": float(np.percentile(e2e_lat, 99) * 1e3),
+                    "wall_s": t_wall},
+            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": achieved_gbs / hbm_peak, "traffic": None,
+                         "kernel": "attn_kernel (recompute over A)",
+                         "avg_launch_ms": a_ms, "algorithmic_bytes": float(np.mean(attn_bytes)),
+                         "flops": float(np.mean(attn_flops)),
+                         "tflops": float(np.mean(attn_flops)) / (a_ms / 1e3) / 1e12,
+                         "peak_source": peak_src, "mean_affected": float(np.mean(nA_list))},
+            "stage_ms": stage_ms,
+            "gpu_launches": (int(launches) + 1) * K,  # + k_set_hdr per batch
+            "clocks": clk,
+        }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cv, ctimes, sample = cpu_reference(args, max(1, args.cpu_batches), st)
+        line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": sample, "p50_ms": float(np.median(ctimes) * 1e3),
+                                "host_nproc": os.cpu_count()}
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        if args.impl == "ours":
+            import torch
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl")
+        else:
+            if rank != 0:
+                return
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local_rank)
+    if world > 1 and args.impl == "ours":
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

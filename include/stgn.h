@@ -224,6 +224,13 @@ int stgn_pipeline_many(const stgn_dims* dims, int64_t N, int64_t E, const float*
                        float* out, float* scores, float* values, float* maxlog, float* zsum,
                        float* qvecs, void* stream);
 
+/* Per-stage device timing (CUDA events; disables graph replay while on).
+ * stage_times writes up to cap stage durations (ms) of the last batch and
+ * returns how many; *launches = kernel launches per batch. */
+int stgn_engine_set_profiling(stgn_engine* eng, int on);
+int stgn_engine_stage_times(stgn_engine* eng, float* ms, int cap, int64_t* launches);
+const char* stgn_stage_name(int i);
+
 /* Library version string and the sm architecture it was built for. */
 const char* stgn_version(void);
 

@@ -25,6 +25,7 @@ EXPORTS = (
     "stgn_engine_set_weights", "stgn_engine_bind", "stgn_engine_process_batch",
     "stgn_engine_process_batch_dev", "stgn_engine_rebuild", "stgn_engine_full_reference",
     "stgn_engine_affected", "stgn_engine_pred_embeddings", "stgn_pipeline_many",
+    "stgn_engine_set_profiling", "stgn_engine_stage_times", "stgn_stage_name",
 )
 
 
@@ -103,8 +104,13 @@ def lib():
     L.stgn_engine_affected.argtypes = [vp, vp, vp, i64, P(i64), P(i64), vp, vp]
     L.stgn_engine_pred_embeddings.argtypes = [vp, vp, i64, vp]
     L.stgn_pipeline_many.argtypes = [P(Dims), i64, i64] + [vp] * 18
+    L.stgn_engine_set_profiling.argtypes = [vp, C.c_int]
+    L.stgn_engine_stage_times.argtypes = [vp, vp, C.c_int, P(i64)]
+    L.stgn_stage_name.restype = C.c_char_p
+    L.stgn_stage_name.argtypes = [C.c_int]
     for name in EXPORTS:
-        if name not in ("stgn_version", "stgn_last_error", "stgn_scratch_bytes"):
+        if name not in ("stgn_version", "stgn_last_error", "stgn_scratch_bytes",
+                        "stgn_stage_name"):
             getattr(L, name).restype = C.c_int
     _LIB = L
     return L

@@ -57,9 +57,13 @@ __device__ __forceinline__ bool rec_is_adj(const Scratch& s, int r) {
 #define GRID_STRIDE(i, n) \
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
-// Reset per-batch results.
-__global__ void k_begin(Scratch s) {
+// Reset per-batch results; derive t_batch (the last edge's timestamp,
+// S/engine.py:415) and the window cutoff on the device.
+__global__ void k_begin(Scratch s, double window) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
+    BatchHdr* hd = s.hdr;
+    hd->t_batch = s.in_t[hd->B - 1];
+    hd->cutoff = isfinite(window) ? hd->t_batch - window : -INFINITY;
     BatchRes* r = s.res;
     r->nD = 0;
     r->nA = 0;

@@ -90,6 +90,9 @@ struct stgn_engine {
   uint32_t stamp = 0;
   cudaGraphExec_t graph = nullptr;
   bool graph_ok = true;   // capture allowed
+  bool profiling = false;
+  cudaEvent_t ev[16] = {};
+  int64_t launches = 0;
 };
 
 static void drop_graph(stgn_engine* e) {
@@ -189,6 +192,8 @@ int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engin
 int stgn_engine_destroy(stgn_engine* e) {
   if (!e) return STGN_OK;
   drop_graph(e);
+  for (auto& ev : e->ev)
+    if (ev) cudaEventDestroy(ev);
   if (e->h_in) cudaFreeHost(e->h_in);
   if (e->h_res) cudaFreeHost(e->h_res);
   if (e->h_preds) cudaFreeHost(e->h_preds);
@@ -248,7 +253,13 @@ static void launch_attn(const stgn_engine* e, const RingSrc& rs, cudaStream_t st
   e->attn.fn<<<e->attn.grid, STGN_THREADS, e->attn.smem, st>>>(e->g, e->aw, rs, fs, e->attn.T);
 }
 
-// The whole per-batch sequence; every size is read on the device.
+static const char* kStageNames[] = {"group+ring", "affected_bfs", "change_records",
+                                    "recompute_affected", "predict", "messages", "gru",
+                                    "recompute_direct", "drift", "rebuild", "cleanup"};
+#define NSTAGES 11
+
+// The whole per-batch sequence; every size is read on the device. With
+// profiling on, an event is recorded after every stage (no graph).
 static void enqueue_batch(stgn_engine* e, cudaStream_t st) {
   const Geo& g = e->g;
   const StateView& v = e->sv;
@@ -258,19 +269,31 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st) {
   const int g_rec = (int)std::min<int64_t>(cdiv(R, T), 4 * e->num_sms);
   const int g_wide = 4 * e->num_sms;
   const int g_warp = (int)std::min<int64_t>(cdiv(R * 32, T), 8 * e->num_sms);
-
-  k_begin<<<1, 32, 0, st>>>(s);
+  int n = 0;  // kernel launches
+  int stage = 0;
+  auto mark = [&]() {
+    if (e->profiling) cudaEventRecord(e->ev[stage], st);
+    ++stage;
+  };
+  mark();
+  k_begin<<<1, 32, 0, st>>>(s, e->cfg.window);
   k_claim<<<g_rec, T, 0, st>>>(g, v, s);
   k_scan<<<1, 1024, 0, st>>>(g, v, s);
   k_place<<<g_rec, T, 0, st>>>(v, s);
   k_rank<<<g_rec, T, 0, st>>>(v, s);
   k_ring<<<g_warp, T, 0, st>>>(g, v, s);
   k_dupdate<<<g_rec, T, 0, st>>>(g, v, s);
+  n += 7;
+  mark();
   for (int hop = 1; hop <= g.K; ++hop) {
     k_hop<<<g_wide, T, 0, st>>>(g, v, s, hop);
     k_hop_fin<<<1, 32, 0, st>>>(s, hop);
+    n += 2;
   }
+  mark();
   k_records<<<g_wide, T, 0, st>>>(g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
+  n += 1;
+  mark();
   // stages 2-4: recompute with pre-batch memory (A, or V_direct)
   RingSrc rs = ring_src(e);
   rs.list = s.alist;
@@ -281,13 +304,24 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st) {
   rs.dpred_count = &s.res->nD;
   rs.e_count = &s.res->E_A;
   launch_attn(e, rs, st);
-  if (e->cfg.scope == STGN_SCOPE_DIRECT) k_mark_valid<<<g_wide, T, 0, st>>>(v, s);
+  n += 1;
+  mark();
+  if (e->cfg.scope == STGN_SCOPE_DIRECT) {
+    k_mark_valid<<<g_wide, T, 0, st>>>(v, s);
+    n += 1;
+  }
   k_predict<<<g_warp, T, 0, st>>>(g, v, s, e->w.wpred, e->w.bpred);
+  n += 1;
+  mark();
   // stage 5: memory update of V_direct, then refresh with post-batch memory
   k_messages<<<(int)std::min<int64_t>(cdiv(e->cfg.max_batch, 16), 2 * e->num_sms), T,
                e->msg_smem, st>>>(g, v, s, e->w.wmsg, e->w.bmsg, e->w.omega);
+  n += 1;
+  mark();
   k_gru<<<(int)std::min<int64_t>(cdiv(R, 32), 2 * e->num_sms), T, e->gru_smem, st>>>(
       g, v, s, e->w.wgru, e->w.ugru, e->w.bgru, e->cfg.aggregator);
+  n += 1;
+  mark();
   RingSrc rd = ring_src(e);
   rd.list = s.alist;
   rd.count_ptr = &s.res->nD;
@@ -295,10 +329,14 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st) {
   rd.write_valid = 1;
   rd.e_count = &s.res->E_D;
   launch_attn(e, rd, st);
+  n += 1;
+  mark();
   // drift + rebuild policy
   k_drift_record<<<g_wide, T, 0, st>>>(v, s);
   k_drift_decide<<<e->num_sms, T, 0, st>>>(v, s, e->cfg.rebuild, e->cfg.rebuild_interval,
                                            e->cfg.delta_max, e->cfg.alpha);
+  n += 2;
+  mark();
   if (e->cfg.rebuild != STGN_REBUILD_NEVER) {
     // partial: the drifted list; full: all node ids (each is a no-op unless chosen)
     k_rb_fill<<<g_wide, T, 0, st>>>(v, s.drifted, &s.res->rb_partial_n, 0);
@@ -316,11 +354,21 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st) {
     launch_attn(e, rf, st);
     k_drift_reset<<<g_wide, T, 0, st>>>(v, s);
     k_drift_reset_fin<<<1, 32, 0, st>>>(v, s);
+    n += 6;
   }
+  mark();
   k_cleanup<<<g_rec, T, 0, st>>>(v, s);
+  n += 1;
+  mark();
+  e->launches = n;
 }
 
 static int run_sequence(stgn_engine* e, cudaStream_t st) {
+  if (e->profiling) {
+    enqueue_batch(e, st);
+    CUDA_TRY(cudaGetLastError());
+    return STGN_OK;
+  }
   if (e->graph_ok && !e->graph) {
     cudaGraph_t gr = nullptr;
     if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
@@ -340,6 +388,32 @@ static int run_sequence(stgn_engine* e, cudaStream_t st) {
   }
   CUDA_TRY(cudaGetLastError());
   return STGN_OK;
+}
+
+extern "C" int stgn_engine_set_profiling(stgn_engine* e, int on) {
+  if (!e) return STGN_ERR_INVALID;
+  if (on && !e->ev[0]) {
+    for (int i = 0; i <= NSTAGES; ++i) CUDA_TRY(cudaEventCreate(&e->ev[i]));
+  }
+  e->profiling = on != 0;
+  return STGN_OK;
+}
+
+extern "C" int stgn_engine_stage_times(stgn_engine* e, float* ms, int cap, int64_t* launches) {
+  if (!e) return -1;
+  if (launches) *launches = e->launches;
+  if (!e->profiling || !e->ev[0]) return 0;
+  const int n = cap < NSTAGES ? cap : NSTAGES;
+  for (int i = 0; i < n; ++i) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, e->ev[i], e->ev[i + 1]) != cudaSuccess) t = -1.f;
+    ms[i] = t;
+  }
+  return n;
+}
+
+extern "C" const char* stgn_stage_name(int i) {
+  return (i >= 0 && i < NSTAGES) ? kStageNames[i] : "";
 }
 
 static void fill_report(const BatchRes& r, const stgn_ctl* /*unused*/, stgn_report* rep) {
@@ -416,6 +490,8 @@ extern "C" int stgn_engine_process_batch(stgn_engine* e, int32_t B, const int32_
   return STGN_OK;
 }
 
+__global__ void k_set_hdr(BatchHdr* dst, BatchHdr h) { *dst = h; }
+
 __global__ void k_pack_feat(const float* src, float* dst, int64_t B, int d_e, int ld_e) {
   GRID_STRIDE(x, B * d_e) {
     const int64_t i = x / d_e, j = x % d_e;
@@ -433,14 +509,9 @@ extern "C" int stgn_engine_process_batch_dev(stgn_engine* e, int32_t B, const in
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const Scratch& s = e->sc;
-  double t_last = 0.0;
-  // the header needs t_batch on the host: one 8-byte read of the last timestamp
-  CUDA_TRY(cudaMemcpyAsync(&e->h_preds[0], t_dev + (B - 1), sizeof(double),
-                           cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  t_last = e->h_preds[0];
-  fill_hdr(e, (BatchHdr*)e->h_in, B, t_last, m0, batch_index, node_count);
-  CUDA_TRY(cudaMemcpyAsync((void*)s.hdr, e->h_in, sizeof(BatchHdr), cudaMemcpyHostToDevice, st));
+  BatchHdr hdr;  // passed by value: nothing on the host is reused before the copy lands
+  fill_hdr(e, &hdr, B, 0.0, m0, batch_index, node_count);  // t_batch is set on the device
+  k_set_hdr<<<1, 1, 0, st>>>(s.hdr, hdr);
   CUDA_TRY(cudaMemcpyAsync(s.in_src, src_dev, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(s.in_dst, dst_dev, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(s.in_t, t_dev, sizeof(double) * B, cudaMemcpyDeviceToDevice, st));

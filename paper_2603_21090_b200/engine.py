@@ -560,6 +560,60 @@ class IncrementalEngine:
         self._after_batch(B, float(t[-1]), top)
         return self._preds[:B].copy()
 
+    def process_batch_device(self, src, dst, t, feat=None, *, max_id: int, t_last: float,
+                             t_first: float, report: bool = False):
+        """Batch already resident on the device (torch tensors: src/dst int32,
+        t float64, feat float32 (B, d_e)); returns the device float64 score
+        tensor without synchronising. The caller vouches for validity
+        (non-negative ids, non-decreasing times >= t_now) and passes the
+        largest id and the first/last timestamps it already knows."""
+        torch = self._torch
+        B = int(src.shape[0])
+        if B == 0:
+            return torch.zeros(0, dtype=torch.float64, device=self.device)
+        if t_first < self._t_now:
+            raise MonotonicityError(f"batch edge at t={t_first} precedes committed history "
+                                    f"t={self._t_now}")
+        top = int(max_id) + 1
+        self._grow(need_nodes=max(self._n_mem, top, self.cfg.nodes, self._store_n),
+                   need_edges=self._m + B, need_batch=B, need_gpow=self.batch_index + 3)
+        self._n_mem = max(self._n_mem, top)
+        self.batch_index += 1
+        self.counters.start_batch()
+        self._affected_cache = None
+        self._pred_cache = None
+        preds = torch.empty(B, dtype=torch.float64, device=self.device)
+        fptr = feat.data_ptr() if (feat is not None and self.dims.d_e) else None
+        rc = self._L.stgn_engine_process_batch_dev(
+            self._handle, B, src.data_ptr(), dst.data_ptr(), t.data_ptr(), fptr, self._m,
+            self.batch_index, self.node_count, preds.data_ptr(),
+            C.byref(self._rep) if report else None, self._stream())
+        if rc:
+            self.batch_index -= 1
+            _lib.check(rc, "process_batch_device")
+        if report:
+            self._after_batch(B, float(t_last), top)
+        else:
+            self._m += B
+            self._t_now = float(t_last)
+            self._store_n = max(self._store_n, top)
+            self._last_nD = self._last_nA = None  # not fetched
+            self.last_report = None
+        return preds
+
+    # -- profiling ----------------------------------------------------------------
+    def set_profiling(self, on: bool):
+        _lib.check(self._L.stgn_engine_set_profiling(self._handle, int(bool(on))), "profiling")
+
+    def stage_times(self) -> tuple[dict, int]:
+        """Per-stage device milliseconds of the last batch (profiling on) and
+        the number of kernel launches per batch."""
+        buf = (C.c_float * 16)()
+        launches = C.c_int64()
+        n = self._L.stgn_engine_stage_times(self._handle, buf, 16, C.byref(launches))
+        names = [self._L.stgn_stage_name(i).decode() for i in range(max(n, 0))]
+        return {nm: float(buf[i]) for i, nm in enumerate(names)}, int(launches.value)
+
     def _after_batch(self, B, t_last, top):
         r = self._rep
         dm = self.dims
