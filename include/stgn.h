@@ -69,21 +69,24 @@ typedef struct {
 } stgn_config;
 
 /*
- * Device-resident weights, float32, packed by the host shim (row-major):
- *   wq    [K][q_in][H*d_k]      from w_q (K,H,q_in,d_k)
- *   wkt   [K][H][d_k][k_in]     from w_k (K,H,k_in,d_k), transposed per head
- *   wv    [K][H][k_in][d_k]     from w_v
- *   wo    [K][H*d_k][d]         from w_o
- *   wmsg  [2][msg_in][d_m]      from w_msg_src / w_msg_dst (transposed)
+ * Device-resident weights, float32, packed by the host shim (row-major;
+ * every row stride is the column count rounded up to a multiple of 4,
+ * "ld(x)", zero-filled):
+ *   wq    [K][d][ld(H*d_k)]      rows 0..d-1 of w_q (K,H,q_in,d_k) per layer
+ *   bq    [K][H*d_k]             phi(0) . w_q[l, :, d:, :] (the constant query half)
+ *   wkt   [K][H][d_k][ld(k_in)]  w_k (K,H,k_in,d_k) transposed per head
+ *   wv    [K][H][k_in][ld(d_k)]  w_v
+ *   wo    [K][H*d_k][ld(d)]      w_o
+ *   wmsg  [msg_in][2*ld(d_m)]    [w_msg_src^T | w_msg_dst^T] (column blocks)
  *   bmsg  [2][d_m]
- *   wgru  [3][d_m][d_s]         from w_z, w_r, w_h (transposed)
- *   ugru  [3][d_s][d_s]         from u_z, u_r, u_h (transposed)
+ *   wgru  [d_m][3*ld(d_s)]       [w_z^T | w_r^T | w_h^T]
+ *   ugru  [d_s][3*ld(d_s)]       [u_z^T | u_r^T | u_h^T]
  *   bgru  [3][d_s]
- *   wpred [2*d]   bpred (double, host)
+ *   wpred [2*d] double, bpred (host double)
  *   omega [d_t/2] double;  phi0 [d_t] float
  */
 typedef struct {
-  const float *wq, *wkt, *wv, *wo;
+  const float *wq, *bq, *wkt, *wv, *wo;
   const float *wmsg, *bmsg, *wgru, *ugru, *bgru;
   const double *wpred;
   const double *omega;

@@ -43,7 +43,7 @@ class Config(C.Structure):
 
 class Weights(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in
-                ("wq", "wkt", "wv", "wo", "wmsg", "bmsg", "wgru", "ugru", "bgru", "wpred",
+                ("wq", "bq", "wkt", "wv", "wo", "wmsg", "bmsg", "wgru", "ugru", "bgru", "wpred",
                  "omega", "phi0")] + [("bpred", C.c_double)]
 
 

@@ -14,7 +14,7 @@
 //   k_drift_record / k_drift_decide       S/drift.py:52-78, S/engine.py:366-372, 440-453
 #pragma once
 
-#include "attn.cuh"
+#include "attn2.cuh"
 
 struct StateView {
   float* mem;
@@ -420,43 +420,52 @@ __global__ void k_predict(Geo g, StateView st, Scratch s, const double* wpred, d
 }
 
 // Messages: row r = [s_owner || s_other || feat || phi(t - last_owner)],
-// msg = row W_side + b_side. Tile = 16 edges: rows 0..15 src side, 16..31
-// dst side.
+// msg = row W_side + b_side (S/engine_base.py:209-225). Tile = 8 edges:
+// R4 rows 0..7 are the src sides (W_src), rows 8..15 the dst sides (W_dst).
+#define MSG_EDGES 8
 __global__ void __launch_bounds__(STGN_THREADS)
 k_messages(Geo g, StateView st, Scratch s, const float* wmsg, const float* bmsg,
-           const double* omega) {
+           const double* omega, int ld_dm) {
   extern __shared__ float4 smem4[];
-  float* Xr = reinterpret_cast<float*>(smem4);   // [32][msg_in]
-  float* Mo = Xr + 32 * g.msg_in;                // [32][d_m]
+  float* Xr = reinterpret_cast<float*>(smem4);   // R4 [16][msg_in]
+  float* Mo = Xr + 16 * g.msg_in;                // R4 [16][2*ld_dm]
   const int64_t B = s.hdr->B;
-  const int64_t ntiles = cdiv(B, 16);
+  const int64_t ntiles = cdiv(B, MSG_EDGES);
+  const int phi0 = 2 * g.d_s + g.d_e;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t e0 = tile * 16;
-    for (int o = threadIdx.x; o < 32 * g.msg_in; o += blockDim.x) {
+    const int64_t e0 = tile * MSG_EDGES;
+    for (int o = threadIdx.x; o < 16 * g.msg_in; o += blockDim.x) {
       const int row = o / g.msg_in, c = o % g.msg_in;
-      const int side = row >> 4;
-      const int64_t i = e0 + (row & 15);
+      const int side = row >> 3;
+      const int64_t i = e0 + (row & 7);
       float v = 0.f;
       if (i < B) {
         const int own = side ? s.in_dst[i] : s.in_src[i];
         const int oth = side ? s.in_src[i] : s.in_dst[i];
         if (c < g.d_s) v = st.mem[(int64_t)own * g.ld_s + c];
         else if (c < 2 * g.d_s) v = st.mem[(int64_t)oth * g.ld_s + c - g.d_s];
-        else if (c < 2 * g.d_s + g.d_e) v = s.in_feat[i * g.ld_e + (c - 2 * g.d_s)];
-        else v = phi_component(omega, c - 2 * g.d_s - g.d_e, s.in_t[i] - st.last[own], g.phi_amp);
+        else if (c < phi0) v = s.in_feat[i * g.ld_e + (c - 2 * g.d_s)];
+        else {
+          const int p = c - phi0;
+          float sv, cv;
+          phase_sincos(omega[p >> 1], s.in_t[i] - st.last[own], &sv, &cv);
+          v = ((p & 1) ? sv : cv) * g.phi_amp;
+        }
       }
-      Xr[o] = v;
+      Xr[r4(row, c, g.msg_in)] = v;
     }
     __syncthreads();
-    tile_gemm(Xr, g.msg_in, 16, g.msg_in, wmsg, g.d_m, g.d_m, Mo, g.d_m, 1.f);
-    tile_gemm(Xr + 16 * g.msg_in, g.msg_in, 16, g.msg_in, wmsg + (int64_t)g.msg_in * g.d_m,
-              g.d_m, g.d_m, Mo + 16 * g.d_m, g.d_m, 1.f);
+    // one GEMM against [W_src | W_dst]; each row keeps its own side's half
+    gemm_r4(Xr, g.msg_in, 16, g.msg_in, wmsg, 2 * ld_dm, 2 * ld_dm, Mo, 2 * ld_dm, 1.f,
+            nullptr, false, threadIdx.x, blockDim.x);
     __syncthreads();
-    for (int o = threadIdx.x; o < 32 * g.d_m; o += blockDim.x) {
+    for (int o = threadIdx.x; o < 16 * g.d_m; o += blockDim.x) {
       const int row = o / g.d_m, c = o % g.d_m;
-      const int side = row >> 4;
-      const int64_t i = e0 + (row & 15);
-      if (i < B) s.msgs[(2 * i + side) * g.ld_m + c] = Mo[o] + bmsg[side * g.d_m + c];
+      const int side = row >> 3;
+      const int64_t i = e0 + (row & 7);
+      if (i < B)
+        s.msgs[(2 * i + side) * g.ld_m + c] =
+            Mo[r4(row, side * ld_dm + c, 2 * ld_dm)] + bmsg[side * g.d_m + c];
     }
     __syncthreads();
   }
@@ -464,78 +473,80 @@ k_messages(Geo g, StateView st, Scratch s, const float* wmsg, const float* bmsg,
 
 // Aggregate each direct node's messages in message order (mean / last /
 // sum, S/kernels/reference.py:56-74) and apply one GRU step
-// (S/kernels/reference.py:81-90); tile of 32 direct nodes.
+// (S/kernels/reference.py:81-90); tile of 16 direct nodes, R4 GEMMs.
+#define GRU_T 16
 __global__ void __launch_bounds__(STGN_THREADS)
 k_gru(Geo g, StateView st, Scratch s, const float* wgru, const float* ugru, const float* bgru,
-      int aggregator) {
+      int aggregator, int ld_ds) {
   extern __shared__ float4 smem4[];
-  const int T = 32;
-  float* Ag = reinterpret_cast<float*>(smem4);  // [T][d_m]
-  float* Sp = Ag + T * g.d_m;                    // [T][d_s]
-  float* Zg = Sp + T * g.d_s;                    // [T][d_s]
-  float* Rg = Zg + T * g.d_s;                    // [T][d_s]
-  float* Hc = Rg + T * g.d_s;                    // [T][d_s]
-  __shared__ int s_node[32];
-  __shared__ int s_lastrec[32];
+  const int T = GRU_T;
+  float* Ag = reinterpret_cast<float*>(smem4);  // R4 [T][d_m]
+  float* Sp = Ag + T * g.d_m;                    // R4 [T][d_s]
+  float* G = Sp + T * g.d_s;                     // R4 [T][3 ld_ds]  agg x [Wz|Wr|Wh]
+  float* P = G + T * 3 * ld_ds;                  // R4 [T][2 ld_ds]  s x [Uz|Ur]
+  float* Rs = P + T * 2 * ld_ds;                 // R4 [T][d_s]      r * s
+  float* Hh = Rs + T * g.d_s;                    // R4 [T][ld_ds]    (r * s) x Uh
+  __shared__ int s_node[GRU_T];
+  __shared__ int s_lastrec[GRU_T];
   const int nD = s.res->nD;
   const int64_t ntiles = cdiv(nD, T);
-  const int64_t mats = (int64_t)g.d_m * g.d_s, umats = (int64_t)g.d_s * g.d_s;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int L3 = 3 * ld_ds;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int d0 = (int)(tile * T);
-    if (threadIdx.x < T) {
-      const int d = d0 + threadIdx.x;
-      s_node[threadIdx.x] = d < nD ? s.alist[d] : -1;
-      s_lastrec[threadIdx.x] = d < nD ? s.rec_s[s.doff[d + 1] - 1] : -1;
+    if (tid < T) {
+      const int d = d0 + tid;
+      s_node[tid] = d < nD ? s.alist[d] : -1;
+      s_lastrec[tid] = d < nD ? s.rec_s[s.doff[d + 1] - 1] : -1;
     }
     __syncthreads();
-    for (int o = threadIdx.x; o < T * g.d_m; o += blockDim.x) {
+    for (int o = tid; o < T * g.d_m; o += nt) {
       const int i = o / g.d_m, c = o % g.d_m;
       const int d = d0 + i;
       float v = 0.f;
       if (d < nD) {
-        const int lo = s.doff[d], hi = s.doff[d + 1];
         if (aggregator == STGN_AGG_LAST) {
           v = s.msgs[(int64_t)s_lastrec[i] * g.ld_m + c];
         } else {
+          const int lo = s.doff[d], hi = s.doff[d + 1];
           float acc = 0.f;
           for (int q = lo; q < hi; ++q) acc += s.msgs[(int64_t)s.rec_s[q] * g.ld_m + c];
           v = aggregator == STGN_AGG_MEAN ? acc / (float)(hi - lo) : acc;
         }
       }
-      Ag[o] = v;
+      Ag[r4(i, c, g.d_m)] = v;
     }
-    for (int o = threadIdx.x; o < T * g.d_s; o += blockDim.x) {
+    for (int o = tid; o < T * g.d_s; o += nt) {
       const int i = o / g.d_s, c = o % g.d_s;
-      Sp[o] = s_node[i] >= 0 ? st.mem[(int64_t)s_node[i] * g.ld_s + c] : 0.f;
+      Sp[r4(i, c, g.d_s)] = s_node[i] >= 0 ? st.mem[(int64_t)s_node[i] * g.ld_s + c] : 0.f;
     }
     __syncthreads();
-    tile_gemm(Ag, g.d_m, T, g.d_m, wgru, g.d_s, g.d_s, Zg, g.d_s, 1.f);
-    tile_gemm(Ag, g.d_m, T, g.d_m, wgru + mats, g.d_s, g.d_s, Rg, g.d_s, 1.f);
-    tile_gemm(Ag, g.d_m, T, g.d_m, wgru + 2 * mats, g.d_s, g.d_s, Hc, g.d_s, 1.f);
+    gemm_r4(Ag, g.d_m, T, g.d_m, wgru, L3, L3, G, L3, 1.f, nullptr, false, tid, nt);
+    gemm_r4(Sp, g.d_s, T, g.d_s, ugru, L3, 2 * ld_ds, P, 2 * ld_ds, 1.f, nullptr, false, tid, nt);
     __syncthreads();
-    tile_gemm(Sp, g.d_s, T, g.d_s, ugru, g.d_s, g.d_s, Zg, g.d_s, 1.f, true);
-    tile_gemm(Sp, g.d_s, T, g.d_s, ugru + umats, g.d_s, g.d_s, Rg, g.d_s, 1.f, true);
-    __syncthreads();
-    for (int o = threadIdx.x; o < T * g.d_s; o += blockDim.x) {
-      const int c = o % g.d_s;
-      Zg[o] = sigmoidf_(Zg[o] + bgru[c]);
-      Rg[o] = sigmoidf_(Rg[o] + bgru[g.d_s + c]) * Sp[o];  // r * s
+    for (int o = tid; o < T * g.d_s; o += nt) {
+      const int i = o / g.d_s, c = o % g.d_s;
+      const float z = sigmoidf_(G[r4(i, c, L3)] + P[r4(i, c, 2 * ld_ds)] + bgru[c]);
+      const float r = sigmoidf_(G[r4(i, ld_ds + c, L3)] + P[r4(i, ld_ds + c, 2 * ld_ds)] +
+                                bgru[g.d_s + c]);
+      G[r4(i, c, L3)] = z;
+      Rs[r4(i, c, g.d_s)] = r * Sp[r4(i, c, g.d_s)];
     }
     __syncthreads();
-    tile_gemm(Rg, g.d_s, T, g.d_s, ugru + 2 * umats, g.d_s, g.d_s, Hc, g.d_s, 1.f, true);
+    gemm_r4(Rs, g.d_s, T, g.d_s, ugru + 2 * ld_ds, L3, g.d_s, Hh, ld_ds, 1.f, nullptr, false, tid, nt);
     __syncthreads();
-    for (int o = threadIdx.x; o < T * g.d_s; o += blockDim.x) {
+    for (int o = tid; o < T * g.d_s; o += nt) {
       const int i = o / g.d_s, c = o % g.d_s;
       const int v = s_node[i];
       if (v < 0) continue;
-      const float cand = tanhf(Hc[o] + bgru[2 * g.d_s + c]);
-      const float z = Zg[o];
-      st.mem[(int64_t)v * g.ld_s + c] = (1.f - z) * cand + z * Sp[o];
+      const float cand = tanhf(G[r4(i, 2 * ld_ds + c, L3)] + Hh[r4(i, c, ld_ds)] + bgru[2 * g.d_s + c]);
+      const float z = G[r4(i, c, L3)];
+      st.mem[(int64_t)v * g.ld_s + c] = (1.f - z) * cand + z * Sp[r4(i, c, g.d_s)];
     }
-    if (threadIdx.x < T && s_node[threadIdx.x] >= 0) {
-      const int v = s_node[threadIdx.x];
+    if (tid < T && s_node[tid] >= 0) {
+      const int v = s_node[tid];
       st.version[v] = s.hdr->batch_index;
-      st.last[v] = s.in_t[s_lastrec[threadIdx.x] >> 1];  // max t = last message (t non-decreasing)
+      st.last[v] = s.in_t[s_lastrec[tid] >> 1];  // max t = last message (t non-decreasing)
     }
     __syncthreads();
   }

@@ -16,6 +16,7 @@
 // attention launch (template dispatch on the per-lane register widths)
 // ---------------------------------------------------------------------------
 typedef void (*attn_fn_t)(Geo, AttnWeights, RingSrc, FlatSrc, int);
+typedef void (*attn2_fn_t)(Geo, EngW, RingSrc, int, int);
 
 template <bool FLAT>
 static attn_fn_t pick_attn(const Geo& g) {
@@ -80,7 +81,11 @@ struct stgn_engine {
   StateView sv;
   Scratch sc;
   int num_sms = 148;
-  AttnLaunch attn;
+  AttnLaunch attn;            // attn_kernel (reserved for the flat operator path)
+  attn2_fn_t attn2 = nullptr; // engine recompute kernel
+  size_t attn2_smem = 0;
+  int attn2_tmax = 0, attn2_wsm = 0;
+  EngW ew;
   size_t msg_smem = 0, gru_smem = 0;
   // pinned staging mirror of [hdr .. in_feat] and the result area
   uint8_t* h_in = nullptr;
@@ -151,13 +156,44 @@ int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engin
     delete e;
     return STGN_ERR_CUDA;
   }
-  rc = plan_attn(e->g, false, e->num_sms, &e->attn);
-  if (rc) {
+  if (e->g.d > 128 || e->g.d_e > 192 || e->g.half > 64) {  // attn2 register budget
     delete e;
-    return rc;
+    return STGN_ERR_INVALID;
   }
-  e->msg_smem = (size_t)(32 * e->g.msg_in + 32 * e->g.d_m) * sizeof(float);
-  e->gru_smem = (size_t)(32 * (e->g.d_m + 4 * e->g.d_s)) * sizeof(float);
+  e->attn2 = e->g.d_e > 0 ? (e->g.H > 2 ? attn2_kernel<6, 4> : attn2_kernel<6, 2>)
+                          : (e->g.H > 2 ? attn2_kernel<0, 4> : attn2_kernel<0, 2>);
+  {  // tile rows vs staged-weight space within ~220 KB of shared memory
+    const int64_t budget = 220 * 1024 / 4;
+    const int64_t row = attn2_row_floats(e->g), full = attn2_wsm_full(e->g);
+    int64_t tmax = (budget - full) / row / 4 * 4;
+    int64_t wsm;
+    if (tmax >= 8) {
+      if (tmax > A2_TMAX) tmax = A2_TMAX;
+      wsm = budget - tmax * row;
+    } else {  // stage weights in chunks
+      wsm = 16 * 1024;
+      tmax = (budget - wsm) / row / 4 * 4;
+      if (tmax > A2_TMAX) tmax = A2_TMAX;
+      wsm = budget - tmax * row;
+    }
+    const int64_t ldmax = round_up(e->g.k_in > e->g.HD ? e->g.k_in : e->g.HD, 4);
+    if (tmax < 4 || wsm < (int64_t)e->g.H * ldmax) {
+      delete e;
+      return STGN_ERR_INVALID;
+    }
+    e->attn2_tmax = (int)tmax;
+    e->attn2_wsm = (int)(wsm / 4 * 4);
+    e->attn2_smem = (size_t)(tmax * row + e->attn2_wsm) * sizeof(float);
+  }
+  ce = cudaFuncSetAttribute((const void*)e->attn2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)e->attn2_smem);
+  if (ce != cudaSuccess) {
+    stgn_set_error(__FILE__, __LINE__, ce);
+    delete e;
+    return STGN_ERR_CUDA;
+  }
+  e->msg_smem = (size_t)(16 * e->g.msg_in + 32 * round_up(e->g.d_m, 4)) * sizeof(float);
+  e->gru_smem = (size_t)(GRU_T * (e->g.d_m + 2 * e->g.d_s + 6 * round_up(e->g.d_s, 4))) * sizeof(float);
   if (e->msg_smem > 227 * 1024 || e->gru_smem > 227 * 1024) {
     delete e;
     return STGN_ERR_INVALID;
@@ -204,6 +240,16 @@ int stgn_engine_destroy(stgn_engine* e) {
 int stgn_engine_set_weights(stgn_engine* e, const stgn_weights* w) {
   if (!e || !w) return STGN_ERR_INVALID;
   e->w = *w;
+  e->ew.wq = w->wq;
+  e->ew.bq = w->bq;
+  e->ew.wkt = w->wkt;
+  e->ew.wv = w->wv;
+  e->ew.wo = w->wo;
+  e->ew.omega = w->omega;
+  e->ew.ld_hd = (int)round_up(e->g.HD, 4);
+  e->ew.ld_kin = (int)round_up(e->g.k_in, 4);
+  e->ew.ld_dk = (int)round_up(e->g.d_k, 4);
+  e->ew.ld_d = (int)round_up(e->g.d, 4);
   e->aw.wq = w->wq;
   e->aw.wkt = w->wkt;
   e->aw.wv = w->wv;
@@ -248,9 +294,8 @@ static RingSrc ring_src(const stgn_engine* e) {
 }
 
 static void launch_attn(const stgn_engine* e, const RingSrc& rs, cudaStream_t st) {
-  FlatSrc fs;
-  memset(&fs, 0, sizeof(fs));
-  e->attn.fn<<<e->attn.grid, STGN_THREADS, e->attn.smem, st>>>(e->g, e->aw, rs, fs, e->attn.T);
+  e->attn2<<<e->num_sms, A2_THREADS, e->attn2_smem, st>>>(e->g, e->ew, rs, e->attn2_tmax,
+                                                          e->attn2_wsm);
 }
 
 static const char* kStageNames[] = {"group+ring", "affected_bfs", "change_records",
@@ -314,12 +359,13 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st) {
   n += 1;
   mark();
   // stage 5: memory update of V_direct, then refresh with post-batch memory
-  k_messages<<<(int)std::min<int64_t>(cdiv(e->cfg.max_batch, 16), 2 * e->num_sms), T,
-               e->msg_smem, st>>>(g, v, s, e->w.wmsg, e->w.bmsg, e->w.omega);
+  k_messages<<<(int)std::min<int64_t>(cdiv(e->cfg.max_batch, MSG_EDGES), 2 * e->num_sms), T,
+               e->msg_smem, st>>>(g, v, s, e->w.wmsg, e->w.bmsg, e->w.omega,
+                                  (int)round_up(g.d_m, 4));
   n += 1;
   mark();
-  k_gru<<<(int)std::min<int64_t>(cdiv(R, 32), 2 * e->num_sms), T, e->gru_smem, st>>>(
-      g, v, s, e->w.wgru, e->w.ugru, e->w.bgru, e->cfg.aggregator);
+  k_gru<<<(int)std::min<int64_t>(cdiv(R, GRU_T), 2 * e->num_sms), T, e->gru_smem, st>>>(
+      g, v, s, e->w.wgru, e->w.ugru, e->w.bgru, e->cfg.aggregator, (int)round_up(g.d_s, 4));
   n += 1;
   mark();
   RingSrc rd = ring_src(e);

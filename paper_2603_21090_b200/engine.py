@@ -440,25 +440,47 @@ class IncrementalEngine:
         torch = self._torch
         p, dm = self.params, self.dims
         K, H, d_k = dm.layers, dm.heads, dm.d_k
-        f32 = lambda a: torch.tensor(np.ascontiguousarray(a, dtype=np.float32), device=self.device)  # noqa
-        f64 = lambda a: torch.tensor(np.ascontiguousarray(a, dtype=np.float64), device=self.device)  # noqa
-        W = {
-            "wq": f32(np.transpose(p.w_q, (0, 2, 1, 3)).reshape(K, dm.query_in, H * d_k)),
-            "wkt": f32(np.transpose(p.w_k, (0, 1, 3, 2))),
-            "wv": f32(p.w_v),
-            "wo": f32(p.w_o),
-            "wmsg": f32(np.stack([p.w_msg_src.T, p.w_msg_dst.T])),
-            "bmsg": f32(np.stack([p.b_msg_src, p.b_msg_dst])),
-            "wgru": f32(np.stack([p.w_z.T, p.w_r.T, p.w_h.T])),
-            "ugru": f32(np.stack([p.u_z.T, p.u_r.T, p.u_h.T])),
-            "bgru": f32(np.stack([p.b_z, p.b_r, p.b_h])),
-            "wpred": f64(p.w_pred),
-            "omega": f64(p.omega),
-        }
+        def f32(a):  # last dim padded to a multiple of 4 (zero-filled); see stgn.h
+            a = np.asarray(a, dtype=np.float64)
+            pad = _rup(a.shape[-1], 4) - a.shape[-1]
+            if pad:
+                a = np.concatenate([a, np.zeros(a.shape[:-1] + (pad,))], axis=-1)
+            return torch.tensor(np.ascontiguousarray(a, dtype=np.float32), device=self.device)
+
+        def f64(a):
+            return torch.tensor(np.ascontiguousarray(a, dtype=np.float64), device=self.device)
+
+        def catcols(mats):  # [rows][n * ld(cols)]: each block padded to a multiple of 4
+            blocks = []
+            for m in mats:
+                pad = _rup(m.shape[1], 4) - m.shape[1]
+                blocks.append(np.concatenate([m, np.zeros((m.shape[0], pad))], axis=1))
+            return torch.tensor(np.ascontiguousarray(np.concatenate(blocks, axis=1),
+                                                     dtype=np.float32), device=self.device)
+
         ang = p.omega * 0.0
         phi0 = np.empty(dm.d_t)
         phi0[0::2], phi0[1::2] = np.cos(ang), np.sin(ang)
-        W["phi0"] = f32(phi0 * np.sqrt(1.0 / dm.d_t))
+        phi0 *= np.sqrt(1.0 / dm.d_t)
+        wq_full = np.transpose(p.w_q, (0, 2, 1, 3)).reshape(K, dm.query_in, H * d_k)
+        W = {
+            "wq": f32(wq_full[:, :dm.d, :]),
+            "bq": torch.tensor(np.einsum("t,ltc->lc", phi0, wq_full[:, dm.d:, :]),
+                               dtype=torch.float32, device=self.device),
+            "wkt": f32(np.transpose(p.w_k, (0, 1, 3, 2))),
+            "wv": f32(p.w_v),
+            "wo": f32(p.w_o),
+            "wmsg": catcols([p.w_msg_src.T, p.w_msg_dst.T]),
+            "bmsg": torch.tensor(np.stack([p.b_msg_src, p.b_msg_dst]), dtype=torch.float32,
+                                 device=self.device),
+            "wgru": catcols([p.w_z.T, p.w_r.T, p.w_h.T]),
+            "ugru": catcols([p.u_z.T, p.u_r.T, p.u_h.T]),
+            "bgru": torch.tensor(np.stack([p.b_z, p.b_r, p.b_h]), dtype=torch.float32,
+                                 device=self.device),
+            "wpred": f64(p.w_pred),
+            "omega": f64(p.omega),
+            "phi0": torch.tensor(phi0, dtype=torch.float32, device=self.device),
+        }
         self._w = W
         ws = _lib.Weights(**{k: v.data_ptr() for k, v in W.items()}, bpred=float(p.b_pred))
         _lib.check(self._L.stgn_engine_set_weights(self._handle, C.byref(ws)), "set_weights")
