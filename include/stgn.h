@@ -77,7 +77,7 @@ typedef struct {
  *   wkt   [K][H][d_k][ld(k_in)]  w_k (K,H,k_in,d_k) transposed per head
  *   wv    [K][H][k_in][ld(d_k)]  w_v
  *   wo    [K][H*d_k][ld(d)]      w_o
- *   wmsg  [msg_in][2*ld(d_m)]    [w_msg_src^T | w_msg_dst^T] (column blocks)
+ *   wmsg  [2*msg_in][ld(d_m)]    [w_msg_src^T ; w_msg_dst^T] (row blocks)
  *   bmsg  [2][d_m]
  *   wgru  [d_m][3*ld(d_s)]       [w_z^T | w_r^T | w_h^T]
  *   ugru  [d_s][3*ld(d_s)]       [u_z^T | u_r^T | u_h^T]

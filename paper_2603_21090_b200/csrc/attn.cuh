@@ -50,9 +50,26 @@ struct RingSrc {
   float* dpred;                 // nullable: copy last layer of idx < *dpred_count into dpred[idx]
   const int32_t* dpred_count;
   unsigned long long* e_count;  // nullable: sum of entry counts
+  // Fused pre/post pass (engine batch path): rows [0, *pre_n) are list[idx]
+  // with pre-batch memory, rows [*pre_n, *pre_n + *post_n) are list[idx - pre_n]
+  // (the direct set) with post-batch memory mem_post[idx - pre_n]. Pre rows
+  // with idx < *post_n (direct nodes) only feed dpred; everything else writes h.
+  int fused;
+  const int32_t *pre_n, *post_n;
+  const float* mem_post;
+  unsigned long long* e_count_post;
 
-  __device__ int64_t count() const { return count_ptr ? (int64_t)count_ptr[0] : count_const; }
-  __device__ int node(int64_t idx) const { return list ? list[idx] : (int)idx; }
+  __device__ int64_t count() const {
+    if (fused) return (int64_t)pre_n[0] + post_n[0];
+    return count_ptr ? (int64_t)count_ptr[0] : count_const;
+  }
+  __device__ int node(int64_t idx) const {
+    if (fused) {
+      const int p = pre_n[0];
+      return list[idx < p ? idx : idx - p];
+    }
+    return list ? list[idx] : (int)idx;
+  }
 };
 
 struct FlatSrc {

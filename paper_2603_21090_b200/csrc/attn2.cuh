@@ -61,6 +61,7 @@ attn2_kernel(Geo g, EngW w, RingSrc rs, int tmax, int wsm_floats) {
   __shared__ int s_E[A2_TMAX];
   __shared__ int s_head[A2_TMAX];
   __shared__ double s_tref[A2_TMAX];
+  __shared__ int s_mode[A2_TMAX];  // 0 write h, 1 direct pre-pass (dpred only), 2 post-memory row
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -71,7 +72,8 @@ attn2_kernel(Geo g, EngW w, RingSrc rs, int tmax, int wsm_floats) {
   if (T > tmax) T = tmax;
   const int64_t ntiles = cdiv(N, T);
   const int UK = g.H * g.k_in;
-  const int64_t dpred_n = rs.dpred ? (int64_t)rs.dpred_count[0] : 0;
+  const int64_t pre_rows = rs.fused ? (int64_t)rs.pre_n[0] : N;
+  const int64_t d_rows = rs.fused ? (int64_t)rs.post_n[0] : 0;
   const int pay_lines = (g.d * 4 + 127) / 128;
   const int feat_lines = g.d_e ? (g.d_e * 4 + 127) / 128 : 0;
 
@@ -80,10 +82,11 @@ attn2_kernel(Geo g, EngW w, RingSrc rs, int tmax, int wsm_floats) {
     if (tid < A2_TMAX) {  // warps 0-1
       const int i = tid;
       const int64_t idx = base + i;
-      int node = -1, E = 0, head = 0;
+      int node = -1, E = 0, head = 0, mode = 0;
       double tref = 0.0;
       if (i < T && idx < N) {
         node = rs.node(idx);
+        if (rs.fused) mode = idx >= pre_rows ? 2 : (idx < d_rows ? 1 : 0);
         const int cc = rs.ring_ccnt[node];
         E = cc >= 0 ? cc : (rs.use_store ? rs.ring_cnt[node] : 0);
         head = rs.ring_head[node];
@@ -93,11 +96,17 @@ attn2_kernel(Geo g, EngW w, RingSrc rs, int tmax, int wsm_floats) {
       s_E[i] = E;
       s_head[i] = head;
       s_tref[i] = tref;
+      s_mode[i] = mode;
       if (rs.e_count) {
-        unsigned long long e64 = (unsigned long long)E;
+        unsigned long long e_pre = mode == 2 ? 0ull : (unsigned long long)E;
+        unsigned long long e_post = mode == 2 ? (unsigned long long)E : 0ull;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) e64 += __shfl_xor_sync(0xffffffffu, e64, o);
-        if (lane == 0 && e64) atomicAdd(rs.e_count, e64);
+        for (int o = 16; o > 0; o >>= 1) {
+          e_pre += __shfl_xor_sync(0xffffffffu, e_pre, o);
+          e_post += __shfl_xor_sync(0xffffffffu, e_post, o);
+        }
+        if (lane == 0 && e_pre) atomicAdd(rs.e_count, e_pre);
+        if (lane == 0 && e_post && rs.e_count_post) atomicAdd(rs.e_count_post, e_post);
       }
     }
     __syncthreads();
@@ -128,7 +137,11 @@ attn2_kernel(Geo g, EngW w, RingSrc rs, int tmax, int wsm_floats) {
     for (int o = tid; o < T * g.d; o += A2_THREADS) {
       const int i = o / g.d, j = o % g.d;
       const int node = s_node[i];
-      X[r4(i, j, g.d)] = (node >= 0 && j < g.d_s) ? rs.mem[(int64_t)node * g.ld_s + j] : 0.f;
+      float v = 0.f;
+      if (node >= 0 && j < g.d_s)
+        v = s_mode[i] == 2 ? rs.mem_post[(base + i - pre_rows) * g.ld_s + j]
+                           : rs.mem[(int64_t)node * g.ld_s + j];
+      X[r4(i, j, g.d)] = v;
     }
     __syncthreads();
 
@@ -274,16 +287,18 @@ attn2_kernel(Geo g, EngW w, RingSrc rs, int tmax, int wsm_floats) {
         if (node < 0) continue;
         const float v = X[r4(i, j, g.d)];
         const int64_t idx = base + i;
-        if (rs.final_out) {
+        const int mode = s_mode[i];
+        if (mode == 1) {  // direct node, pre-batch memory: prediction embedding only
+          if (last) rs.dpred[idx * g.ld_d + j] = v;
+        } else if (rs.final_out) {
           if (last) rs.final_out[idx * g.ld_d + j] = v;
         } else {
           rs.h[((int64_t)node * g.K + l) * g.ld_d + j] = v;
         }
-        if (last && rs.dpred && idx < dpred_n) rs.dpred[idx * g.ld_d + j] = v;
       }
       if (last && rs.write_valid && tid < T) {
         const int node = s_node[tid];
-        if (node >= 0) {
+        if (node >= 0 && s_mode[tid] != 1) {
           rs.valid[node] = 1;
           rs.valid_at[node] = rs.valid_at_ptr ? rs.valid_at_ptr[0] : rs.valid_at_const;
         }

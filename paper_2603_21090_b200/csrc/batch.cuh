@@ -10,7 +10,8 @@
 //   k_hop                                 affected set S/engine.py:182-212
 //   k_records                             change records S/engine.py:216-243
 //   k_predict                             S/kernels/reference.py:183-186
-//   k_messages / k_gru                    S/engine_base.py:193-247
+//   k_memory (messages+aggregate+GRU)     S/engine_base.py:193-247
+//   k_predict_commit                      S/engine.py:425-426, S/engine_base.py:241-244
 //   k_drift_record / k_drift_decide       S/drift.py:52-78, S/engine.py:366-372, 440-453
 #pragma once
 
@@ -92,6 +93,7 @@ __global__ void k_claim(Geo g, StateView st, Scratch s) {
     if (atomicExch(&st.dmark[node], stamp) != stamp) {
       const int di = atomicAdd(&s.res->nD, 1);
       s.alist[di] = node;
+      s.dmap[node] = di;
       st.amark[node] = stamp;
     }
     atomicAdd(&st.nodecnt[node], 1);
@@ -404,126 +406,155 @@ __global__ void k_mark_valid(StateView st, Scratch s) {
   }
 }
 
-// sigma(w_p . [h_src || h_dst] + b_p) in float64, one warp per edge.
-__global__ void k_predict(Geo g, StateView st, Scratch s, const double* wpred, double bpred) {
+// sigma(w_p . [h_src || h_dst] + b_p) in float64 on the pre-batch-memory
+// embeddings of the endpoints (S/engine.py:425-426), one warp per edge;
+// then commit the post-batch memory of V_direct (S/engine_base.py:241-244).
+__global__ void k_predict_commit(Geo g, StateView st, Scratch s, const double* wpred,
+                                 double bpred) {
   const int64_t B = s.hdr->B;
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < B; i += warps) {
-    const float* hu = st.h + ((int64_t)s.in_src[i] * g.K + (g.K - 1)) * g.ld_d;
-    const float* hv = st.h + ((int64_t)s.in_dst[i] * g.K + (g.K - 1)) * g.ld_d;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int64_t i = gw; i < B; i += warps) {
+    const float* hu = s.dpred + (int64_t)s.dmap[s.in_src[i]] * g.ld_d;
+    const float* hv = s.dpred + (int64_t)s.dmap[s.in_dst[i]] * g.ld_d;
     double acc = 0.0;
     for (int j = lane; j < g.d; j += 32) acc += wpred[j] * (double)hu[j] + wpred[g.d + j] * (double)hv[j];
     acc = warp_sum_d(acc);
     if (lane == 0) s.preds[i] = 1.0 / (1.0 + exp(-(acc + bpred)));
   }
-}
-
-// Messages: row r = [s_owner || s_other || feat || phi(t - last_owner)],
-// msg = row W_side + b_side (S/engine_base.py:209-225). Tile = 8 edges:
-// R4 rows 0..7 are the src sides (W_src), rows 8..15 the dst sides (W_dst).
-#define MSG_EDGES 8
-__global__ void __launch_bounds__(STGN_THREADS)
-k_messages(Geo g, StateView st, Scratch s, const float* wmsg, const float* bmsg,
-           const double* omega, int ld_dm) {
-  extern __shared__ float4 smem4[];
-  float* Xr = reinterpret_cast<float*>(smem4);   // R4 [16][msg_in]
-  float* Mo = Xr + 16 * g.msg_in;                // R4 [16][2*ld_dm]
-  const int64_t B = s.hdr->B;
-  const int64_t ntiles = cdiv(B, MSG_EDGES);
-  const int phi0 = 2 * g.d_s + g.d_e;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t e0 = tile * MSG_EDGES;
-    for (int o = threadIdx.x; o < 16 * g.msg_in; o += blockDim.x) {
-      const int row = o / g.msg_in, c = o % g.msg_in;
-      const int side = row >> 3;
-      const int64_t i = e0 + (row & 7);
-      float v = 0.f;
-      if (i < B) {
-        const int own = side ? s.in_dst[i] : s.in_src[i];
-        const int oth = side ? s.in_src[i] : s.in_dst[i];
-        if (c < g.d_s) v = st.mem[(int64_t)own * g.ld_s + c];
-        else if (c < 2 * g.d_s) v = st.mem[(int64_t)oth * g.ld_s + c - g.d_s];
-        else if (c < phi0) v = s.in_feat[i * g.ld_e + (c - 2 * g.d_s)];
-        else {
-          const int p = c - phi0;
-          float sv, cv;
-          phase_sincos(omega[p >> 1], s.in_t[i] - st.last[own], &sv, &cv);
-          v = ((p & 1) ? sv : cv) * g.phi_amp;
-        }
-      }
-      Xr[r4(row, c, g.msg_in)] = v;
+  const int nD = s.res->nD;
+  GRID_STRIDE(x, (int64_t)nD * g.d_s) {
+    const int d = (int)(x / g.d_s), c = (int)(x % g.d_s);
+    const int v = s.alist[d];
+    st.mem[(int64_t)v * g.ld_s + c] = s.mem_new[(int64_t)d * g.ld_s + c];
+    if (c == 0) {
+      st.version[v] = s.hdr->batch_index;
+      st.last[v] = s.in_t[s.rec_s[s.doff[d + 1] - 1] >> 1];  // latest message (t non-decreasing)
     }
-    __syncthreads();
-    // one GEMM against [W_src | W_dst]; each row keeps its own side's half
-    gemm_r4(Xr, g.msg_in, 16, g.msg_in, wmsg, 2 * ld_dm, 2 * ld_dm, Mo, 2 * ld_dm, 1.f,
-            nullptr, false, threadIdx.x, blockDim.x);
-    __syncthreads();
-    for (int o = threadIdx.x; o < 16 * g.d_m; o += blockDim.x) {
-      const int row = o / g.d_m, c = o % g.d_m;
-      const int side = row >> 3;
-      const int64_t i = e0 + (row & 7);
-      if (i < B)
-        s.msgs[(2 * i + side) * g.ld_m + c] =
-            Mo[r4(row, side * ld_dm + c, 2 * ld_dm)] + bmsg[side * g.d_m + c];
-    }
-    __syncthreads();
   }
 }
 
-// Aggregate each direct node's messages in message order (mean / last /
-// sum, S/kernels/reference.py:56-74) and apply one GRU step
-// (S/kernels/reference.py:81-90); tile of 16 direct nodes, R4 GEMMs.
+// Memory update of V_direct, fused: messages (S/kernels/reference.py:32-53),
+// per-node aggregation (:56-74) and one GRU step (:81-90). Messages are
+// linear in their input row, so the aggregate is formed on the inputs:
+//   agg = ([sum_src x || sum_dst x] [W_src; W_dst] + n_src b_src + n_dst b_dst) / (n if mean)
+// with x = [s_v || s_other || feat || phi(t - last_v)]; for `last` only the
+// node's last message (its own side) enters. The new memory goes to
+// mem_new (committed after the recompute, which still reads pre-batch memory).
+#define MG_THREADS 512
 #define GRU_T 16
-__global__ void __launch_bounds__(STGN_THREADS)
-k_gru(Geo g, StateView st, Scratch s, const float* wgru, const float* ugru, const float* bgru,
-      int aggregator, int ld_ds) {
+#define MEM_SREC 256  // records staged per pass
+__global__ void __launch_bounds__(MG_THREADS)
+k_memory(Geo g, StateView st, Scratch s, const float* wmsg2, const float* bmsg,
+         const double* omega, const float* wgru, const float* ugru, const float* bgru,
+         int aggregator, int ld_dm, int ld_ds, int wsm) {
   extern __shared__ float4 smem4[];
   const int T = GRU_T;
-  float* Ag = reinterpret_cast<float*>(smem4);  // R4 [T][d_m]
-  float* Sp = Ag + T * g.d_m;                    // R4 [T][d_s]
+  const int MI2 = 2 * g.msg_in;
+  float* X2 = reinterpret_cast<float*>(smem4);  // R4 [T][2 msg_in]
+  float* Ag = X2 + T * MI2;                      // R4 [T][ld_dm]
+  float* Sp = Ag + T * ld_dm;                    // R4 [T][d_s]
   float* G = Sp + T * g.d_s;                     // R4 [T][3 ld_ds]  agg x [Wz|Wr|Wh]
   float* P = G + T * 3 * ld_ds;                  // R4 [T][2 ld_ds]  s x [Uz|Ur]
   float* Rs = P + T * 2 * ld_ds;                 // R4 [T][d_s]      r * s
   float* Hh = Rs + T * g.d_s;                    // R4 [T][ld_ds]    (r * s) x Uh
-  __shared__ int s_node[GRU_T];
-  __shared__ int s_lastrec[GRU_T];
+  float* Wsm = Hh + T * ld_ds;                   // staged weight rows
+  __shared__ int s_node[GRU_T], s_lo[GRU_T], s_hi[GRU_T], s_last[GRU_T], s_n0[GRU_T], s_n1[GRU_T];
+  __shared__ int s_re[MEM_SREC], s_rside[MEM_SREC], s_roth[MEM_SREC];
+  __shared__ double s_rdt[MEM_SREC];
   const int nD = s.res->nD;
   const int64_t ntiles = cdiv(nD, T);
   const int tid = threadIdx.x, nt = blockDim.x;
   const int L3 = 3 * ld_ds;
+  const int phi0 = 2 * g.d_s + g.d_e;
+  const bool last_agg = aggregator == STGN_AGG_LAST;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int d0 = (int)(tile * T);
     if (tid < T) {
       const int d = d0 + tid;
-      s_node[tid] = d < nD ? s.alist[d] : -1;
-      s_lastrec[tid] = d < nD ? s.rec_s[s.doff[d + 1] - 1] : -1;
-    }
-    __syncthreads();
-    for (int o = tid; o < T * g.d_m; o += nt) {
-      const int i = o / g.d_m, c = o % g.d_m;
-      const int d = d0 + i;
-      float v = 0.f;
+      int v = -1, lo = 0, hi = 0, lr = -1, n0 = 0, n1 = 0;
       if (d < nD) {
-        if (aggregator == STGN_AGG_LAST) {
-          v = s.msgs[(int64_t)s_lastrec[i] * g.ld_m + c];
-        } else {
-          const int lo = s.doff[d], hi = s.doff[d + 1];
-          float acc = 0.f;
-          for (int q = lo; q < hi; ++q) acc += s.msgs[(int64_t)s.rec_s[q] * g.ld_m + c];
-          v = aggregator == STGN_AGG_MEAN ? acc / (float)(hi - lo) : acc;
+        v = s.alist[d];
+        lo = s.doff[d];
+        hi = s.doff[d + 1];
+        lr = s.rec_s[hi - 1];
+        for (int q = lo; q < hi; ++q) {
+          if (s.rec_s[q] & 1) ++n1; else ++n0;
         }
       }
-      Ag[r4(i, c, g.d_m)] = v;
+      s_node[tid] = v; s_lo[tid] = lo; s_hi[tid] = hi; s_last[tid] = lr;
+      s_n0[tid] = n0; s_n1[tid] = n1;
+    }
+    __syncthreads();
+    // aggregated message inputs [sum_src x || sum_dst x]; the tile's records
+    // are one contiguous range of rec_s, staged (edge, other end, dt) in smem
+    // so the column sweep issues independent loads only
+    for (int o = tid; o < T * MI2; o += nt) X2[o] = 0.f;
+    const int rlo = s.doff[d0], rhi = s.doff[d0 + T < nD ? d0 + T : nD];
+    for (int rc0 = rlo; rc0 < rhi; rc0 += MEM_SREC) {
+      const int rcn = rhi - rc0 < MEM_SREC ? rhi - rc0 : MEM_SREC;
+      __syncthreads();
+      for (int q = tid; q < rcn; q += nt) {
+        const int r = s.rec_s[rc0 + q];
+        const int64_t e = r >> 1;
+        const int own = (r & 1) ? s.in_dst[e] : s.in_src[e];
+        s_re[q] = (int)e;
+        s_rside[q] = r & 1;
+        s_roth[q] = (r & 1) ? s.in_src[e] : s.in_dst[e];
+        s_rdt[q] = s.in_t[e] - st.last[own];
+      }
+      __syncthreads();
+      for (int o = tid; o < T * MI2; o += nt) {
+        const int i = o / MI2, c = o - i * MI2;
+        const int v = s_node[i];
+        if (v < 0) continue;
+        const int side = c >= g.msg_in;
+        const int cc = c - side * g.msg_in;
+        int qa = (last_agg ? s_hi[i] - 1 : s_lo[i]) - rc0, qb = s_hi[i] - rc0;
+        if (qa < 0) qa = 0;
+        if (qb > rcn) qb = rcn;
+        float acc = 0.f;
+        for (int q = qa; q < qb; ++q) {
+          if (s_rside[q] != side) continue;
+          float x;
+          if (cc < g.d_s) x = st.mem[(int64_t)v * g.ld_s + cc];
+          else if (cc < 2 * g.d_s) x = st.mem[(int64_t)s_roth[q] * g.ld_s + cc - g.d_s];
+          else if (cc < phi0) x = s.in_feat[(int64_t)s_re[q] * g.ld_e + (cc - 2 * g.d_s)];
+          else {
+            const int p = cc - phi0;
+            float sv, cv;
+            phase_sincos(omega[p >> 1], s_rdt[q], &sv, &cv);
+            x = ((p & 1) ? sv : cv) * g.phi_amp;
+          }
+          acc += x;
+        }
+        X2[r4(i, c, MI2)] += acc;
+      }
     }
     for (int o = tid; o < T * g.d_s; o += nt) {
       const int i = o / g.d_s, c = o % g.d_s;
       Sp[r4(i, c, g.d_s)] = s_node[i] >= 0 ? st.mem[(int64_t)s_node[i] * g.ld_s + c] : 0.f;
     }
     __syncthreads();
-    gemm_r4(Ag, g.d_m, T, g.d_m, wgru, L3, L3, G, L3, 1.f, nullptr, false, tid, nt);
-    gemm_r4(Sp, g.d_s, T, g.d_s, ugru, L3, 2 * ld_ds, P, 2 * ld_ds, 1.f, nullptr, false, tid, nt);
+    gemm_staged<2>(X2, MI2, 0, T, MI2, wmsg2, ld_dm, 0, g.d_m, 1, Ag, ld_dm, 0, 1.f, nullptr, 0,
+                   false, Wsm, wsm);
+    for (int o = tid; o < T * g.d_m; o += nt) {  // biases and the mean
+      const int i = o / g.d_m, c = o % g.d_m;
+      if (s_node[i] < 0) continue;
+      float& a = Ag[r4(i, c, ld_dm)];
+      if (last_agg) {
+        a += bmsg[(s_last[i] & 1) * g.d_m + c];
+      } else {
+        a += (float)s_n0[i] * bmsg[c] + (float)s_n1[i] * bmsg[g.d_m + c];
+        if (aggregator == STGN_AGG_MEAN) a /= (float)(s_n0[i] + s_n1[i]);
+      }
+    }
     __syncthreads();
+    gemm_staged<2>(Ag, ld_dm, 0, T, g.d_m, wgru, L3, 0, L3, 1, G, L3, 0, 1.f, nullptr, 0, false,
+                   Wsm, wsm);
+    gemm_staged<2>(Sp, g.d_s, 0, T, g.d_s, ugru, L3, 0, 2 * ld_ds, 1, P, 2 * ld_ds, 0, 1.f,
+                   nullptr, 0, false, Wsm, wsm);
     for (int o = tid; o < T * g.d_s; o += nt) {
       const int i = o / g.d_s, c = o % g.d_s;
       const float z = sigmoidf_(G[r4(i, c, L3)] + P[r4(i, c, 2 * ld_ds)] + bgru[c]);
@@ -533,20 +564,14 @@ k_gru(Geo g, StateView st, Scratch s, const float* wgru, const float* ugru, cons
       Rs[r4(i, c, g.d_s)] = r * Sp[r4(i, c, g.d_s)];
     }
     __syncthreads();
-    gemm_r4(Rs, g.d_s, T, g.d_s, ugru + 2 * ld_ds, L3, g.d_s, Hh, ld_ds, 1.f, nullptr, false, tid, nt);
-    __syncthreads();
+    gemm_staged<2>(Rs, g.d_s, 0, T, g.d_s, ugru + 2 * ld_ds, L3, 0, g.d_s, 1, Hh, ld_ds, 0, 1.f,
+                   nullptr, 0, false, Wsm, wsm);
     for (int o = tid; o < T * g.d_s; o += nt) {
       const int i = o / g.d_s, c = o % g.d_s;
-      const int v = s_node[i];
-      if (v < 0) continue;
+      if (s_node[i] < 0) continue;
       const float cand = tanhf(G[r4(i, 2 * ld_ds + c, L3)] + Hh[r4(i, c, ld_ds)] + bgru[2 * g.d_s + c]);
       const float z = G[r4(i, c, L3)];
-      st.mem[(int64_t)v * g.ld_s + c] = (1.f - z) * cand + z * Sp[r4(i, c, g.d_s)];
-    }
-    if (tid < T && s_node[tid] >= 0) {
-      const int v = s_node[tid];
-      st.version[v] = s.hdr->batch_index;
-      st.last[v] = s.in_t[s_lastrec[tid] >> 1];  // max t = last message (t non-decreasing)
+      s.mem_new[(int64_t)(d0 + i) * g.ld_s + c] = (1.f - z) * cand + z * Sp[r4(i, c, g.d_s)];
     }
     __syncthreads();
   }

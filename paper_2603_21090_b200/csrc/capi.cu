@@ -86,7 +86,8 @@ struct stgn_engine {
   size_t attn2_smem = 0;
   int attn2_tmax = 0, attn2_wsm = 0;
   EngW ew;
-  size_t msg_smem = 0, gru_smem = 0;
+  size_t mem_smem = 0;
+  int mem_wsm = 0;
   // pinned staging mirror of [hdr .. in_feat] and the result area
   uint8_t* h_in = nullptr;
   int64_t in_bytes = 0;
@@ -192,17 +193,19 @@ int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engin
     delete e;
     return STGN_ERR_CUDA;
   }
-  e->msg_smem = (size_t)(16 * e->g.msg_in + 32 * round_up(e->g.d_m, 4)) * sizeof(float);
-  e->gru_smem = (size_t)(GRU_T * (e->g.d_m + 2 * e->g.d_s + 6 * round_up(e->g.d_s, 4))) * sizeof(float);
-  if (e->msg_smem > 227 * 1024 || e->gru_smem > 227 * 1024) {
-    delete e;
-    return STGN_ERR_INVALID;
+  {  // k_memory: activations + staged weights within ~200 KB
+    const int64_t budget = 200 * 1024 / 4;
+    const int64_t ld_dm = round_up(e->g.d_m, 4), ld_ds = round_up(e->g.d_s, 4);
+    const int64_t act = GRU_T * (2 * e->g.msg_in + ld_dm + 2 * e->g.d_s + 6 * ld_ds);
+    e->mem_wsm = (int)((budget - act) / 4 * 4);
+    if (e->mem_wsm < 3 * ld_ds || e->mem_wsm < ld_dm) {
+      delete e;
+      return STGN_ERR_INVALID;
+    }
+    e->mem_smem = (size_t)(act + e->mem_wsm) * sizeof(float);
   }
-  ce = cudaFuncSetAttribute((const void*)k_messages, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)e->msg_smem);
-  if (ce == cudaSuccess)
-    ce = cudaFuncSetAttribute((const void*)k_gru, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)e->gru_smem);
+  ce = cudaFuncSetAttribute((const void*)k_memory, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)e->mem_smem);
   if (ce != cudaSuccess) {
     stgn_set_error(__FILE__, __LINE__, ce);
     delete e;
@@ -299,9 +302,9 @@ static void launch_attn(const stgn_engine* e, const RingSrc& rs, cudaStream_t st
 }
 
 static const char* kStageNames[] = {"group+ring", "affected_bfs", "change_records",
-                                    "recompute_affected", "predict", "messages", "gru",
-                                    "recompute_direct", "drift", "rebuild", "cleanup"};
-#define NSTAGES 11
+                                    "memory_update", "recompute", "predict+commit", "drift",
+                                    "rebuild", "cleanup"};
+#define NSTAGES 9
 
 // The whole per-batch sequence; every size is read on the device. With
 // profiling on, an event is recorded after every stage (no graph).
@@ -321,6 +324,7 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st) {
     ++stage;
   };
   mark();
+  // ingest: direct set, per-node record order, ring insert with payload freeze, store append
   k_begin<<<1, 32, 0, st>>>(s, e->cfg.window);
   k_claim<<<g_rec, T, 0, st>>>(g, v, s);
   k_scan<<<1, 1024, 0, st>>>(g, v, s);
@@ -339,42 +343,33 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st) {
   k_records<<<g_wide, T, 0, st>>>(g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
   n += 1;
   mark();
-  // stages 2-4: recompute with pre-batch memory (A, or V_direct)
+  // stage 5 (memory update of V_direct) into mem_new; commits after the recompute
+  k_memory<<<(int)std::min<int64_t>(cdiv(R, GRU_T), e->num_sms), MG_THREADS, e->mem_smem, st>>>(
+      g, v, s, e->w.wmsg, e->w.bmsg, e->w.omega, e->w.wgru, e->w.ugru, e->w.bgru,
+      e->cfg.aggregator, (int)round_up(g.d_m, 4), (int)round_up(g.d_s, 4), e->mem_wsm);
+  n += 1;
+  mark();
+  // stages 2-4 and the post-commit refresh in one launch: rows = A (or V_direct)
+  // with pre-batch memory, then V_direct with post-batch memory
   RingSrc rs = ring_src(e);
   rs.list = s.alist;
-  rs.count_ptr = e->cfg.scope == STGN_SCOPE_DIRECT ? &s.res->nD : &s.res->nA;
+  rs.fused = 1;
+  rs.pre_n = e->cfg.scope == STGN_SCOPE_DIRECT ? &s.res->nD : &s.res->nA;
+  rs.post_n = &s.res->nD;
+  rs.mem_post = s.mem_new;
   rs.valid_at_ptr = &s.hdr->t_batch;
   rs.write_valid = 1;
   rs.dpred = s.dpred;
-  rs.dpred_count = &s.res->nD;
   rs.e_count = &s.res->E_A;
+  rs.e_count_post = &s.res->E_D;
   launch_attn(e, rs, st);
   n += 1;
-  mark();
   if (e->cfg.scope == STGN_SCOPE_DIRECT) {
     k_mark_valid<<<g_wide, T, 0, st>>>(v, s);
     n += 1;
   }
-  k_predict<<<g_warp, T, 0, st>>>(g, v, s, e->w.wpred, e->w.bpred);
-  n += 1;
   mark();
-  // stage 5: memory update of V_direct, then refresh with post-batch memory
-  k_messages<<<(int)std::min<int64_t>(cdiv(e->cfg.max_batch, MSG_EDGES), 2 * e->num_sms), T,
-               e->msg_smem, st>>>(g, v, s, e->w.wmsg, e->w.bmsg, e->w.omega,
-                                  (int)round_up(g.d_m, 4));
-  n += 1;
-  mark();
-  k_gru<<<(int)std::min<int64_t>(cdiv(R, GRU_T), 2 * e->num_sms), T, e->gru_smem, st>>>(
-      g, v, s, e->w.wgru, e->w.ugru, e->w.bgru, e->cfg.aggregator, (int)round_up(g.d_s, 4));
-  n += 1;
-  mark();
-  RingSrc rd = ring_src(e);
-  rd.list = s.alist;
-  rd.count_ptr = &s.res->nD;
-  rd.valid_at_ptr = &s.hdr->t_batch;
-  rd.write_valid = 1;
-  rd.e_count = &s.res->E_D;
-  launch_attn(e, rd, st);
+  k_predict_commit<<<g_warp, T, 0, st>>>(g, v, s, e->w.wpred, e->w.bpred);
   n += 1;
   mark();
   // drift + rebuild policy

@@ -62,6 +62,8 @@ struct BatchRes {
   int64_t rebuild_kind, rebuild_nodes;
   double global_drift;
   int32_t rb_partial_n, rb_full_n;   // rebuild work sizes (0 unless that kind fired)
+  int32_t nAD;                       // rows of the fused recompute (A pre + D post)
+  int32_t pad3;
   uint32_t ticket;                   // last-block-done counter of k_drift_decide
   int32_t pad2;
 };
@@ -87,6 +89,8 @@ struct Scratch {
   int32_t* drifted;         // [cap_nodes]
   double* partials;         // [1024]
   int32_t* rb_ids;          // [cap_nodes] host-provided rebuild list
+  int32_t* dmap;            // [cap_nodes] node -> direct index (valid for this batch's D)
+  float* mem_new;           // [2Bmax][ld_s] post-batch memory of D (committed after recompute)
 };
 
 static inline int64_t carve(int64_t& off, int64_t bytes) {
@@ -115,6 +119,8 @@ static inline int64_t scratch_layout(const Geo& g, int64_t Bmax, int64_t cap_nod
   int64_t o_drift = carve(off, cap_nodes * 4);
   int64_t o_part = carve(off, 1024 * 8);
   int64_t o_rb = carve(off, cap_nodes * 4);
+  int64_t o_dmap = carve(off, cap_nodes * 4);
+  int64_t o_mnew = carve(off, R * g.ld_s * 4);
   if (s && base) {
     s->hdr = (BatchHdr*)(base + o_hdr);
     s->res = (BatchRes*)(base + o_res);
@@ -138,6 +144,8 @@ static inline int64_t scratch_layout(const Geo& g, int64_t Bmax, int64_t cap_nod
     s->drifted = (int32_t*)(base + o_drift);
     s->partials = (double*)(base + o_part);
     s->rb_ids = (int32_t*)(base + o_rb);
+    s->dmap = (int32_t*)(base + o_dmap);
+    s->mem_new = (float*)(base + o_mnew);
   }
   return off;
 }

@@ -99,7 +99,8 @@ __device__ __forceinline__ void gemm_staged(const float* A, int lda, int a_hoff,
   const int ncp = (N + 1) >> 1;
   const int per_g = ncp * (T >> 2);
   const int items = G * per_g;
-  int KC = wsm_floats / (G * ldw);
+  const int wc = (N + 3) & ~3;  // staged columns per weight row (row stride in Wsm)
+  int KC = wsm_floats / (G * wc);
   if (KC > kd) KC = kd;
   for (int base = 0; base < items; base += MAXI * nt) {
     float acc[MAXI][8];
@@ -110,13 +111,18 @@ __device__ __forceinline__ void gemm_staged(const float* A, int lda, int a_hoff,
     for (int k0 = 0; k0 < kd; k0 += KC) {
       const int kc = kd - k0 < KC ? kd - k0 : KC;
       __syncthreads();  // previous chunk fully consumed
-      const int row4 = ldw >> 2;
+      const int row4 = wc >> 2;
       const int per_g4 = kc * row4;
+      // cp.async: every thread fires all of its 16-byte copies, then waits once
+      const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(Wsm);
       for (int x = tid; x < G * per_g4; x += nt) {
         const int g = x / per_g4, rem = x - g * per_g4;
-        reinterpret_cast<float4*>(Wsm)[x] =
-            __ldg(reinterpret_cast<const float4*>(W + g * w_hstride + (int64_t)k0 * ldw) + rem);
+        const int r = rem / row4, c4 = rem - r * row4;
+        const float* src = W + g * w_hstride + (int64_t)(k0 + r) * ldw + 4 * c4;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + 16u * x),
+                     "l"(src));
       }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
       __syncthreads();
 #pragma unroll
       for (int it = 0; it < MAXI; ++it) {
@@ -125,13 +131,13 @@ __device__ __forceinline__ void gemm_staged(const float* A, int lda, int a_hoff,
           const int g = o / per_g, rem = o - g * per_g;
           const int cp = rem % ncp, rg = rem / ncp;
           const float4* a4 = reinterpret_cast<const float4*>(A) + (int64_t)rg * lda + g * a_hoff + k0;
-          const float2* w2 = reinterpret_cast<const float2*>(Wsm + g * kc * ldw) + cp;
+          const float2* w2 = reinterpret_cast<const float2*>(Wsm + g * kc * wc) + cp;
           float c00 = acc[it][0], c01 = acc[it][1], c10 = acc[it][2], c11 = acc[it][3];
           float c20 = acc[it][4], c21 = acc[it][5], c30 = acc[it][6], c31 = acc[it][7];
 #pragma unroll 4
           for (int k = 0; k < kc; ++k) {
             const float4 a = a4[k];
-            const float2 w = w2[k * (ldw >> 1)];
+            const float2 w = w2[k * (wc >> 1)];
             c00 = fmaf(a.x, w.x, c00); c01 = fmaf(a.x, w.y, c01);
             c10 = fmaf(a.y, w.x, c10); c11 = fmaf(a.y, w.y, c11);
             c20 = fmaf(a.z, w.x, c20); c21 = fmaf(a.z, w.y, c21);

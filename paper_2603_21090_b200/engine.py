@@ -93,70 +93,104 @@ _REBUILD_NAMES = {0: "none", 1: "partial", 2: "full"}
 
 
 class _Tables:
-    """PyTorch-allocated device tables bound into the C engine."""
+    """PyTorch-allocated device tables bound into the C engine. Node tables,
+    edge tables, the gamma^k table and the scratch grow independently."""
 
     NODE_I32 = ("ring_cnt", "ring_head", "ring_ccnt", "nodecnt", "nodeadj", "nodefill",
-                "nodeoff", "cum_list")
+                "nodeoff", "cum_list", "amark", "dmark", "cum_mark")
+    EDGE = ("e_src", "e_dst", "e_t", "e_feat", "e_prev")
 
     def __init__(self, eng, cap_nodes, cap_edges, gpow_len):
+        self.eng = eng
         torch = eng._torch
-        dev = eng.device
-        g = eng
-        self.cap_nodes, self.cap_edges = cap_nodes, cap_edges
-        z = lambda *s, dt=torch.float32: torch.zeros(*s, dtype=dt, device=dev)  # noqa: E731
-        N, L, K = cap_nodes, g.L, g.K
+        self.ctl = torch.zeros(_rup(C.sizeof(_lib.Ctl), 8) // 8, dtype=torch.int64,
+                               device=eng.device)
+        self.cap_nodes = self.cap_edges = 0
+        self._alloc_nodes(cap_nodes)
+        self._alloc_edges(cap_edges)
+        self._alloc_gpow(gpow_len)
+        self.new_scratch()
+
+    def _z(self, *shape, dt=None, fill=0):
+        torch = self.eng._torch
+        t = torch.empty(*shape, dtype=dt or torch.float32, device=self.eng.device)
+        return t.fill_(fill)
+
+    def _alloc_nodes(self, N):
+        torch, g = self.eng._torch, self.eng
+        old = {k: getattr(self, k) for k in self._node_names()} if self.cap_nodes else {}
+        n0 = self.cap_nodes
+        z = self._z
         self.mem = z(N, g.ld_s)
         self.last = z(N, dt=torch.float64)
         self.version = z(N, dt=torch.int64)
-        self.h = z(N, K, g.ld_d)
+        self.h = z(N, g.K, g.ld_d)
         self.valid = z(N, dt=torch.uint8)
-        self.valid_at = torch.full((N,), -math.inf, dtype=torch.float64, device=dev)
+        self.valid_at = z(N, dt=torch.float64, fill=-math.inf)
         for name in self.NODE_I32:
             setattr(self, name, z(N, dt=torch.int32))
         self.ring_ccnt.fill_(-1)
-        self.ring_nbr = z(N, L, dt=torch.int32)
-        self.ring_eid = z(N, L, dt=torch.int64)
-        self.ring_t = z(N, L, dt=torch.float64)
-        self.ring_pay = z(N, K, L, g.ld_d)
-        self.ring_feat = z(N, L, g.ld_e)
-        self.amark = z(N, dt=torch.int32)
-        self.dmark = z(N, dt=torch.int32)
-        self.cum_mark = z(N, dt=torch.int32)
+        self.ring_nbr = z(N, g.L, dt=torch.int32)
+        self.ring_eid = z(N, g.L, dt=torch.int64)
+        self.ring_t = z(N, g.L, dt=torch.float64)
+        self.ring_pay = z(N, g.K, g.L, g.ld_d)
+        self.ring_feat = z(N, g.L, g.ld_e)
         self.drift_acc = z(N, dt=torch.float64)
         self.drift_touched = z(N, dt=torch.int64)
-        self.adj_head = torch.full((N,), -1, dtype=torch.int64, device=dev)
+        self.adj_head = z(N, dt=torch.int64, fill=-1)
         self.adj_deg = z(N, dt=torch.int64)
-        E = cap_edges
+        for k, t in old.items():
+            getattr(self, k)[:n0].copy_(t[:n0])
+        self.cap_nodes = N
+
+    def _node_names(self):
+        return ("mem", "last", "version", "h", "valid", "valid_at", *self.NODE_I32, "ring_nbr",
+                "ring_eid", "ring_t", "ring_pay", "ring_feat", "drift_acc", "drift_touched",
+                "adj_head", "adj_deg")
+
+    def _alloc_edges(self, E):
+        torch, g = self.eng._torch, self.eng
+        old = {k: getattr(self, k) for k in self.EDGE} if self.cap_edges else {}
+        e0 = self.cap_edges
+        z = self._z
         self.e_src = z(E, dt=torch.int32)
         self.e_dst = z(E, dt=torch.int32)
         self.e_t = z(E, dt=torch.float64)
         self.e_feat = z(E, g.ld_e)
-        self.e_prev = torch.full((2 * E,), -1, dtype=torch.int64, device=dev)
-        self.gpow = torch.tensor([g.cfg.gamma ** k for k in range(gpow_len)],
-                                 dtype=torch.float64, device=dev)
-        self.ctl = z(_rup(C.sizeof(_lib.Ctl), 8) // 8, dt=torch.int64)
-        sb = eng._L.stgn_scratch_bytes(C.byref(eng._dims), C.byref(eng._cfgs), cap_nodes)
+        self.e_prev = z(2 * E, dt=torch.int64, fill=-1)
+        for k, t in old.items():
+            lim = 2 * e0 if k == "e_prev" else e0
+            getattr(self, k)[:lim].copy_(t[:lim])
+        self.cap_edges = E
+
+    def _alloc_gpow(self, G):
+        torch, g = self.eng._torch, self.eng
+        self.gpow = torch.tensor([g.cfg.gamma ** k for k in range(G)], dtype=torch.float64,
+                                 device=g.device)
+
+    def new_scratch(self):
+        eng = self.eng
+        sb = eng._L.stgn_scratch_bytes(C.byref(eng._dims), C.byref(eng._cfgs), self.cap_nodes)
         if sb < 0:
             raise ConfigError("invalid dims/config for the CUDA engine")
-        self.scratch = z(int(sb), dt=torch.uint8)
+        self.scratch = self._z(int(sb), dt=eng._torch.uint8)
 
-    def copy_from(self, old):
-        """Copy the live prefix of every table from a smaller instance."""
-        n, e = old.cap_nodes, old.cap_edges
-        for name, t in vars(old).items():
-            if name in ("cap_nodes", "cap_edges", "scratch"):
-                continue
-            if name == "gpow":
-                continue
-            if name == "ctl":
-                self.ctl.copy_(t)
-                continue
-            dst = getattr(self, name)
-            if name.startswith("e_"):
-                lim = 2 * e if name == "e_prev" else e
-            else:
-                lim = n
-            dst[:lim].copy_(t[:lim])
+    def grow(self, nodes=0, edges=0, gpow=0, scratch=False):
+        """Grow what is too small (doubling); returns True if anything moved."""
+        moved = False
+        if nodes > self.cap_nodes:
+            self._alloc_nodes(max(nodes, 2 * self.cap_nodes))
+            moved = scratch = True
+        if edges > self.cap_edges:
+            self._alloc_edges(max(edges, 2 * self.cap_edges))
+            moved = True
+        if gpow > self.gpow.numel():
+            self._alloc_gpow(max(gpow, 2 * self.gpow.numel()))
+            moved = True
+        if scratch:
+            self.new_scratch()
+            moved = True
+        return moved
 
     def struct(self) -> _lib.State:
         s = _lib.State()
@@ -470,7 +504,7 @@ class IncrementalEngine:
             "wkt": f32(np.transpose(p.w_k, (0, 1, 3, 2))),
             "wv": f32(p.w_v),
             "wo": f32(p.w_o),
-            "wmsg": catcols([p.w_msg_src.T, p.w_msg_dst.T]),
+            "wmsg": f32(np.concatenate([p.w_msg_src.T, p.w_msg_dst.T], axis=0)),
             "bmsg": torch.tensor(np.stack([p.b_msg_src, p.b_msg_dst]), dtype=torch.float32,
                                  device=self.device),
             "wgru": catcols([p.w_z.T, p.w_r.T, p.w_h.T]),
@@ -497,17 +531,16 @@ class IncrementalEngine:
             self._preds = np.zeros(self._max_batch, dtype=np.float64)
             self._make_handle()
             self._upload_weights()
-        n_cap, e_cap, g_len = tab.cap_nodes, tab.cap_edges, tab.gpow.numel()
-        if need_nodes > n_cap or need_edges > e_cap or need_gpow > g_len or rebuild_handle:
-            new_n = max(n_cap, need_nodes if need_nodes <= n_cap else max(need_nodes, 2 * n_cap))
-            new_e = max(e_cap, need_edges if need_edges <= e_cap else max(need_edges, 2 * e_cap))
-            new_g = max(g_len, need_gpow if need_gpow <= g_len else max(need_gpow, 2 * g_len))
-            if (new_n, new_e, new_g) != (n_cap, e_cap, g_len) or rebuild_handle:
-                self._torch.cuda.current_stream(self.device).synchronize()
-                fresh = _Tables(self, new_n, new_e, new_g)
-                fresh.copy_from(tab)
-                self._tab = fresh
+        if (need_nodes > tab.cap_nodes or need_edges > tab.cap_edges or
+                need_gpow > tab.gpow.numel() or rebuild_handle):
+            self._torch.cuda.current_stream(self.device).synchronize()
+            tab.grow(nodes=need_nodes, edges=need_edges, gpow=need_gpow, scratch=rebuild_handle)
             self._bind()
+
+    def reserve(self, nodes: int = 0, edges: int = 0, batch: int = 0, batches: int = 0):
+        """Pre-size the device tables (avoids regrowth copies mid-stream)."""
+        self._grow(need_nodes=nodes, need_edges=edges, need_batch=batch,
+                   need_gpow=self.batch_index + batches + 3 if batches else 0)
 
     def _ensure_nodes(self, n):
         if n > self._tab.cap_nodes:
