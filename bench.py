@@ -287,7 +287,9 @@ def run_ours(args, world, rank, local_rank):
         for nm, v in times.items():
             stage_acc.setdefault(nm, []).append(v)
         r = eng._rep
-        nA, EA = int(r.affected), int(r.entries_affected)
+        # one launch recomputes A (pre-batch memory) and V_direct (post-batch memory)
+        nA = int(r.affected) + (int(r.direct) if args.recompute == "affected" else 0)
+        EA = int(r.entries_affected) + int(r.entries_direct)
         # algorithmic bytes: per node mem row + ring meta + K*d output,
         # per entry K*d frozen payload + d_e feat + 8 B timestamp
         by = nA * (4 * g.d_s + 4 * g.layers * g.d + 16) + EA * (4 * g.layers * g.d + 4 * g.d_e + 8)
