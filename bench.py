@@ -340,6 +340,7 @@ def run_ours(args, world, rank, local_rank):
             "stage_ms": stage_ms,
             "gpu_launches": (int(launches) + 1) * K,  # + k_set_hdr per batch
             "clocks": clk,
+            "engine": eng.info(),
         }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cv, ctimes, sample = cpu_reference(args, max(1, args.cpu_batches), st)

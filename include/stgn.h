@@ -234,6 +234,12 @@ int stgn_engine_set_profiling(stgn_engine* eng, int on);
 int stgn_engine_stage_times(stgn_engine* eng, float* ms, int cap, int64_t* launches);
 const char* stgn_stage_name(int i);
 
+/* Engine facts, up to n of: [graph replay active, rebuild block is a
+ * device-side conditional graph node, kernel launches per batch, attention
+ * tile rows, staged-weight floats, SM count, attention smem bytes,
+ * memory-update smem bytes]. */
+int stgn_engine_info(stgn_engine* eng, int64_t* info, int n);
+
 /* Library version string and the sm architecture it was built for. */
 const char* stgn_version(void);
 

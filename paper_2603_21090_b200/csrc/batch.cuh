@@ -605,7 +605,7 @@ __global__ void k_drift_record(StateView st, Scratch s) {
 // the policy decision (S/drift.py:16-23, 72-78; S/engine.py:440-453) is
 // made by the last block to finish. rebuild: 0 never, 1 fixed, 2 adaptive.
 __global__ void k_drift_decide(StateView st, Scratch s, int rebuild, int64_t interval,
-                               double delta_max, double alpha) {
+                               double delta_max, double alpha, cudaGraphConditionalHandle cond) {
   __shared__ double red[32];
   __shared__ bool is_last;
   const int64_t tau = st.ctl->tau + 1;
@@ -659,6 +659,7 @@ __global__ void k_drift_decide(StateView st, Scratch s, int rebuild, int64_t int
     s.res->rb_full_n = kind == 2 ? (int32_t)s.hdr->node_count : 0;
     s.res->rebuild_nodes = kind == 1 ? s.res->n_drifted : (kind == 2 ? s.hdr->node_count : 0);
     st.ctl->tau = tau;
+    if (cond) cudaGraphSetConditional(cond, kind != 0 ? 1u : 0u);
   }
 }
 

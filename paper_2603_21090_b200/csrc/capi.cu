@@ -99,6 +99,11 @@ struct stgn_engine {
   bool profiling = false;
   cudaEvent_t ev[16] = {};
   int64_t launches = 0;
+  cudaStream_t aux = nullptr;   // captures the conditional rebuild body
+  bool capture_failed = false;
+  bool cond_used = false;       // rebuild block is a device-side conditional graph node
+  cudaStream_t work = nullptr;  // the batch sequence / graph runs here
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
 };
 
 static void drop_graph(stgn_engine* e) {
@@ -224,6 +229,15 @@ int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engin
     return STGN_ERR_CUDA;
   }
   memset(e->h_in, 0, e->in_bytes);
+  ce = cudaStreamCreateWithFlags(&e->aux, cudaStreamNonBlocking);
+  if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&e->work, cudaStreamNonBlocking);
+  if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming);
+  if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e->ev_out, cudaEventDisableTiming);
+  if (ce != cudaSuccess) {
+    stgn_set_error(__FILE__, __LINE__, ce);
+    stgn_engine_destroy(e);
+    return STGN_ERR_CUDA;
+  }
   *out = e;
   return STGN_OK;
 }
@@ -231,6 +245,10 @@ int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engin
 int stgn_engine_destroy(stgn_engine* e) {
   if (!e) return STGN_OK;
   drop_graph(e);
+  if (e->aux) cudaStreamDestroy(e->aux);
+  if (e->work) cudaStreamDestroy(e->work);
+  if (e->ev_in) cudaEventDestroy(e->ev_in);
+  if (e->ev_out) cudaEventDestroy(e->ev_out);
   for (auto& ev : e->ev)
     if (ev) cudaEventDestroy(ev);
   if (e->h_in) cudaFreeHost(e->h_in);
@@ -308,7 +326,7 @@ static const char* kStageNames[] = {"group+ring", "affected_bfs", "change_record
 
 // The whole per-batch sequence; every size is read on the device. With
 // profiling on, an event is recorded after every stage (no graph).
-static void enqueue_batch(stgn_engine* e, cudaStream_t st) {
+static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalHandle cond) {
   const Geo& g = e->g;
   const StateView& v = e->sv;
   const Scratch& s = e->sc;
@@ -375,27 +393,63 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st) {
   // drift + rebuild policy
   k_drift_record<<<g_wide, T, 0, st>>>(v, s);
   k_drift_decide<<<e->num_sms, T, 0, st>>>(v, s, e->cfg.rebuild, e->cfg.rebuild_interval,
-                                           e->cfg.delta_max, e->cfg.alpha);
+                                           e->cfg.delta_max, e->cfg.alpha, cond);
   n += 2;
   mark();
   if (e->cfg.rebuild != STGN_REBUILD_NEVER) {
-    // partial: the drifted list; full: all node ids (each is a no-op unless chosen)
-    k_rb_fill<<<g_wide, T, 0, st>>>(v, s.drifted, &s.res->rb_partial_n, 0);
-    k_rb_fill<<<g_wide, T, 0, st>>>(v, nullptr, &s.res->rb_full_n, 0);
+    // Inside a captured graph the rebuild block is the body of a conditional
+    // IF node whose flag k_drift_decide sets on the device; eager launches
+    // (profiling) run it unconditionally (each kernel is a no-op unless chosen).
+    cudaStream_t rs = st;
+    bool body = false;
+    if (cond) {
+      cudaStreamCaptureStatus cs;
+      cudaGraph_t gcap = nullptr;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t ndeps = 0;
+      if (cudaStreamGetCaptureInfo(st, &cs, nullptr, &gcap, &deps, &ndeps) == cudaSuccess &&
+          cs == cudaStreamCaptureStatusActive) {
+        alignas(cudaGraphNodeParams) unsigned char cp_buf[sizeof(cudaGraphNodeParams)] = {};
+        cudaGraphNodeParams& cp = *reinterpret_cast<cudaGraphNodeParams*>(cp_buf);
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = cond;
+        cp.conditional.type = cudaGraphCondTypeIf;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cnode;
+        if (cudaGraphAddNode(&cnode, gcap, deps, ndeps, &cp) == cudaSuccess &&
+            cudaStreamUpdateCaptureDependencies(st, &cnode, 1,
+                                                cudaStreamSetCaptureDependencies) == cudaSuccess &&
+            cudaStreamBeginCaptureToGraph(e->aux, cp.conditional.phGraph_out[0], nullptr, nullptr,
+                                          0, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+          rs = e->aux;
+          body = true;
+          e->cond_used = true;
+        } else {
+          e->capture_failed = true;
+        }
+      }
+    }
+    // partial: the drifted list; full: all node ids
+    k_rb_fill<<<g_wide, T, 0, rs>>>(v, s.drifted, &s.res->rb_partial_n, 0);
+    k_rb_fill<<<g_wide, T, 0, rs>>>(v, nullptr, &s.res->rb_full_n, 0);
     RingSrc rp = ring_src(e);
     rp.list = s.drifted;
     rp.count_ptr = &s.res->rb_partial_n;
     rp.valid_at_ptr = &s.hdr->t_batch;
     rp.write_valid = 1;
     rp.e_count = &s.res->E_R;
-    launch_attn(e, rp, st);
+    launch_attn(e, rp, rs);
     RingSrc rf = rp;
     rf.list = nullptr;
     rf.count_ptr = &s.res->rb_full_n;
-    launch_attn(e, rf, st);
-    k_drift_reset<<<g_wide, T, 0, st>>>(v, s);
-    k_drift_reset_fin<<<1, 32, 0, st>>>(v, s);
+    launch_attn(e, rf, rs);
+    k_drift_reset<<<g_wide, T, 0, rs>>>(v, s);
+    k_drift_reset_fin<<<1, 32, 0, rs>>>(v, s);
     n += 6;
+    if (body) {
+      cudaGraph_t bg = nullptr;
+      if (cudaStreamEndCapture(e->aux, &bg) != cudaSuccess) e->capture_failed = true;
+    }
   }
   mark();
   k_cleanup<<<g_rec, T, 0, st>>>(v, s);
@@ -404,17 +458,42 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st) {
   e->launches = n;
 }
 
-static int run_sequence(stgn_engine* e, cudaStream_t st) {
+// The sequence runs on the engine's own stream (graph capture is illegal on
+// the legacy default stream callers often use), ordered after and before
+// the caller's stream by events.
+static int run_on_work(stgn_engine* e, cudaStream_t st);
+
+static int run_sequence(stgn_engine* e, cudaStream_t caller) {
+  CUDA_TRY(cudaEventRecord(e->ev_in, caller));
+  CUDA_TRY(cudaStreamWaitEvent(e->work, e->ev_in, 0));
+  int rc = run_on_work(e, e->work);
+  if (rc) return rc;
+  CUDA_TRY(cudaEventRecord(e->ev_out, e->work));
+  CUDA_TRY(cudaStreamWaitEvent(caller, e->ev_out, 0));
+  return STGN_OK;
+}
+
+static int run_on_work(stgn_engine* e, cudaStream_t st) {
   if (e->profiling) {
-    enqueue_batch(e, st);
+    enqueue_batch(e, st, 0);
     CUDA_TRY(cudaGetLastError());
     return STGN_OK;
   }
   if (e->graph_ok && !e->graph) {
     cudaGraph_t gr = nullptr;
     if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
-      enqueue_batch(e, st);
-      if (cudaStreamEndCapture(st, &gr) == cudaSuccess && gr) {
+      cudaGraphConditionalHandle cond = 0;
+      cudaStreamCaptureStatus cs;
+      cudaGraph_t gcap = nullptr;
+      if (e->cfg.rebuild != STGN_REBUILD_NEVER &&
+          cudaStreamGetCaptureInfo(st, &cs, nullptr, &gcap, nullptr, nullptr) == cudaSuccess) {
+        if (cudaGraphConditionalHandleCreate(&cond, gcap, 0, cudaGraphCondAssignDefault) !=
+            cudaSuccess)
+          cond = 0;
+      }
+      e->capture_failed = false;
+      enqueue_batch(e, st, cond);
+      if (cudaStreamEndCapture(st, &gr) == cudaSuccess && gr && !e->capture_failed) {
         if (cudaGraphInstantiate(&e->graph, gr, 0) != cudaSuccess) e->graph = nullptr;
         cudaGraphDestroy(gr);
       }
@@ -425,7 +504,7 @@ static int run_sequence(stgn_engine* e, cudaStream_t st) {
   if (e->graph) {
     CUDA_TRY(cudaGraphLaunch(e->graph, st));
   } else {
-    enqueue_batch(e, st);
+    enqueue_batch(e, st, 0);
   }
   CUDA_TRY(cudaGetLastError());
   return STGN_OK;
@@ -733,5 +812,13 @@ extern "C" int stgn_pipeline_many(const stgn_dims* dims, int64_t N, int64_t E, c
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaFreeAsync(packed, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  return STGN_OK;
+}
+
+extern "C" int stgn_engine_info(stgn_engine* e, int64_t* info, int n) {
+  if (!e || !info) return STGN_ERR_INVALID;
+  const int64_t v[8] = {e->graph ? 1 : 0, e->cond_used ? 1 : 0, e->launches, e->attn2_tmax,
+                        e->attn2_wsm, e->num_sms, (int64_t)e->attn2_smem, (int64_t)e->mem_smem};
+  for (int i = 0; i < n && i < 8; ++i) info[i] = v[i];
   return STGN_OK;
 }

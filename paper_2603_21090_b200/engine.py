@@ -669,6 +669,14 @@ class IncrementalEngine:
         names = [self._L.stgn_stage_name(i).decode() for i in range(max(n, 0))]
         return {nm: float(buf[i]) for i, nm in enumerate(names)}, int(launches.value)
 
+    def info(self) -> dict:
+        """Engine facts from the C ABI (graph replay, conditional rebuild, tiles)."""
+        buf = (C.c_int64 * 8)()
+        _lib.check(self._L.stgn_engine_info(self._handle, buf, 8), "info")
+        keys = ("graph_active", "conditional_rebuild", "launches_per_batch", "attn_tile_rows",
+                "attn_staged_weight_floats", "num_sms", "attn_smem_bytes", "memory_smem_bytes")
+        return {k: int(buf[i]) for i, k in enumerate(keys)}
+
     def _after_batch(self, B, t_last, top):
         r = self._rep
         dm = self.dims
