@@ -127,10 +127,11 @@ typedef struct {
   float    *ring_feat;  /* [cap_nodes][L][ld_e] */
   uint32_t *amark, *dmark;                      /* [cap_nodes] batch stamps */
   int32_t  *nodecnt, *nodeadj, *nodefill, *nodeoff;  /* [cap_nodes] scratch */
-  double   *drift_acc;  /* [cap_nodes] */
-  int64_t  *drift_touched; /* [cap_nodes] */
-  uint32_t *cum_mark;   /* [cap_nodes] */
-  int32_t  *cum_list;   /* [cap_nodes] */
+  double   *drift_acc;  /* [cap_nodes] estimator, indexed by cumulative-set position */
+  int64_t  *drift_touched; /* [cap_nodes] tau of last touch, same indexing */
+  uint32_t *cum_mark;   /* [cap_nodes] node is in the cumulative affected set (generation stamp) */
+  int32_t  *cum_list;   /* [cap_nodes] position -> node */
+  int32_t  *cum_pos;    /* [cap_nodes] node -> position */
   int32_t  *e_src, *e_dst;  /* [cap_edges]   append-only temporal store */
   double   *e_t;            /* [cap_edges] */
   float    *e_feat;         /* [cap_edges][ld_e] */

@@ -34,6 +34,7 @@ struct StateView {
   int64_t* drift_touched;
   uint32_t* cum_mark;
   int32_t* cum_list;
+  int32_t* cum_pos;
   int32_t *e_src, *e_dst;
   double* e_t;
   float* e_feat;
@@ -394,6 +395,72 @@ __global__ void k_records(Geo g, StateView st, Scratch s, int finite_window) {
   }
 }
 
+// Same records with one warp per node and one lane per list position
+// (L <= 32): the window prefix is a ballot, the distinct direct
+// neighbours a __match_any_sync, so a node costs a few parallel loads.
+__global__ void k_records_warp(Geo g, StateView st, Scratch s, int finite_window) {
+  const int nA = s.res->nA, nD = s.res->nD;
+  const uint32_t stamp = s.hdr->stamp;
+  const double cutoff = s.hdr->cutoff;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  unsigned long long hit = 0, miss = 0, changed = 0;
+  for (int64_t a64 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a64 < nA;
+       a64 += warps) {
+    const int a = (int)a64;
+    const int v = s.alist[a];
+    int added = 0, expired = 0, len, was_cached;
+    if (a < nD) {
+      const int kadj = st.nodeadj[v];
+      was_cached = s.d_wascached[a];
+      const int merged = kadj + s.d_baselen[a];
+      len = merged < g.L ? merged : g.L;
+      expired = was_cached ? (merged > g.L ? merged - g.L : 0) : 0;
+      added = kadj;
+    } else {
+      const int cc = st.ring_ccnt[v];
+      was_cached = cc >= 0;
+      len = was_cached ? cc : st.ring_cnt[v];
+    }
+    int n_new = added < len ? added : len;
+    int slot = st.ring_head[v] + lane;
+    if (slot >= g.L) slot -= g.L;
+    const int64_t rs = (int64_t)v * g.L + slot;
+    const bool in_list = lane < len;
+    if (finite_window) {
+      const unsigned old = __ballot_sync(0xffffffffu, in_list && st.ring_t[rs] < cutoff);
+      const int keep = old ? __ffs(old) - 1 : len;
+      expired += len - keep;
+      len = keep;
+      if (n_new > len) n_new = len;
+    }
+    const bool cand = lane >= n_new && lane < len;
+    const int u = cand ? st.ring_nbr[rs] : -1 - lane;  // distinct dummies off-range
+    const bool dir = cand && st.dmark[u] == stamp;
+    const unsigned peers = __match_any_sync(0xffffffffu, u);
+    const bool first = (__ffs(peers) - 1) == lane;  // lowest position holding this id
+    const int upd = __popc(__ballot_sync(0xffffffffu, dir && first));
+    if (lane == 0) {
+      const int size = added + expired + upd;
+      s.a_size[a] = size;
+      s.a_len[a] = len;
+      st.ring_ccnt[v] = len;
+      if (was_cached) ++hit; else ++miss;
+      if (size > 0 && len > 0) ++changed;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    hit += __shfl_xor_sync(0xffffffffu, hit, o);
+    miss += __shfl_xor_sync(0xffffffffu, miss, o);
+    changed += __shfl_xor_sync(0xffffffffu, changed, o);
+  }
+  if (lane == 0) {
+    if (hit) atomicAdd(&s.res->nbr_hit, hit);
+    if (miss) atomicAdd(&s.res->nbr_miss, miss);
+    if (changed) atomicAdd(&s.res->changed, changed);
+  }
+}
+
 // valid / valid_at for A \ D when only V_direct is recomputed.
 __global__ void k_mark_valid(StateView st, Scratch s) {
   const int nA = s.res->nA, nD = s.res->nD;
@@ -579,6 +646,9 @@ k_memory(Geo g, StateView st, Scratch s, const float* wmsg2, const float* bmsg,
 
 // Drift estimators: acc_v <- gamma^(tau - touched_v) acc_v + |dN_v| / |N_v|
 // for nodes with a non-empty change record; cumulative affected set.
+// Estimators live at the node's position in the cumulative set (a nonzero
+// estimator implies membership), so the per-batch global mean streams
+// contiguous arrays and a reset only forgets the set.
 __global__ void k_drift_record(StateView st, Scratch s) {
   const int nA = s.res->nA;
   const int64_t tau = st.ctl->tau + 1;
@@ -587,16 +657,25 @@ __global__ void k_drift_record(StateView st, Scratch s) {
     const int a = (int)a64;
     const int v = s.alist[a];
     const int sz = s.a_size[a], len = s.a_len[a];
-    if (sz > 0 && len > 0) {
-      const double acc = st.drift_acc[v];
-      const double dec = acc == 0.0 ? 0.0 : acc * st.gpow[tau - st.drift_touched[v]];
-      st.drift_acc[v] = dec + (double)sz / (double)len;
-      st.drift_touched[v] = tau;
-    }
+    int pos;
+    bool fresh = false;
     if (st.cum_mark[v] != gen) {
       st.cum_mark[v] = gen;
-      const long long pos = atomicAdd((unsigned long long*)&st.ctl->cum_count, 1ull);
+      pos = (int)atomicAdd((unsigned long long*)&st.ctl->cum_count, 1ull);
       st.cum_list[pos] = v;
+      st.cum_pos[v] = pos;
+      fresh = true;
+    } else {
+      pos = st.cum_pos[v];
+    }
+    if (sz > 0 && len > 0) {
+      const double acc = fresh ? 0.0 : st.drift_acc[pos];
+      const double dec = acc == 0.0 ? 0.0 : acc * st.gpow[tau - st.drift_touched[pos]];
+      st.drift_acc[pos] = dec + (double)sz / (double)len;
+      st.drift_touched[pos] = tau;
+    } else if (fresh) {
+      st.drift_acc[pos] = 0.0;
+      st.drift_touched[pos] = 0;
     }
   }
 }
@@ -616,13 +695,12 @@ __global__ void k_drift_decide(StateView st, Scratch s, int rebuild, int64_t int
     const int64_t per = cdiv(n, gridDim.x);
     const int64_t lo = blockIdx.x * per, hi = lo + per < n ? lo + per : n;
     for (int64_t q = lo + threadIdx.x; q < hi; q += blockDim.x) {
-      const int v = st.cum_list[q];
-      const double acc = st.drift_acc[v];
-      const double dec = acc == 0.0 ? 0.0 : acc * st.gpow[tau - st.drift_touched[v]];
+      const double acc = st.drift_acc[q];
+      const double dec = acc == 0.0 ? 0.0 : acc * st.gpow[tau - st.drift_touched[q]];
       part += dec;
       if (dec > delta_max) {
         const int pos = atomicAdd(&s.res->n_drifted, 1);
-        s.drifted[pos] = v;
+        s.drifted[pos] = st.cum_list[q];
       }
     }
   }
@@ -674,17 +752,8 @@ __global__ void k_rb_fill(StateView st, const int32_t* list, const int32_t* coun
   }
 }
 
-// Scheduler reset after an executed rebuild (S/drift.py:92-96).
-__global__ void k_drift_reset(StateView st, Scratch s) {
-  if (s.res->rebuild_kind == 0) return;
-  const int64_t n = st.ctl->cum_count;
-  GRID_STRIDE(q, n) {
-    const int v = st.cum_list[q];
-    st.drift_acc[v] = 0.0;
-    st.drift_touched[v] = 0;
-  }
-}
-
+// Scheduler reset after an executed rebuild (S/drift.py:92-96): forgetting
+// the cumulative set clears every estimator (they are indexed by position).
 __global__ void k_drift_reset_fin(StateView st, Scratch s) {
   if (threadIdx.x || blockIdx.x) return;
   if (s.res->rebuild_kind == 0) return;

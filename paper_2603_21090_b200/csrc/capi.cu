@@ -293,6 +293,7 @@ int stgn_engine_bind(stgn_engine* e, const stgn_state* s) {
   v.amark = s->amark; v.dmark = s->dmark; v.nodecnt = s->nodecnt; v.nodeadj = s->nodeadj;
   v.nodefill = s->nodefill; v.nodeoff = s->nodeoff; v.drift_acc = s->drift_acc;
   v.drift_touched = s->drift_touched; v.cum_mark = s->cum_mark; v.cum_list = s->cum_list;
+  v.cum_pos = s->cum_pos;
   v.e_src = s->e_src; v.e_dst = s->e_dst; v.e_t = s->e_t; v.e_feat = s->e_feat;
   v.e_prev = s->e_prev; v.adj_head = s->adj_head; v.adj_deg = s->adj_deg;
   v.gpow = s->gpow; v.gpow_len = s->gpow_len; v.ctl = s->ctl;
@@ -358,7 +359,10 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
     n += 2;
   }
   mark();
-  k_records<<<g_wide, T, 0, st>>>(g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
+  if (g.L <= 32)
+    k_records_warp<<<8 * e->num_sms, T, 0, st>>>(g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
+  else
+    k_records<<<g_wide, T, 0, st>>>(g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
   n += 1;
   mark();
   // stage 5 (memory update of V_direct) into mem_new; commits after the recompute
@@ -443,9 +447,8 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
     rf.list = nullptr;
     rf.count_ptr = &s.res->rb_full_n;
     launch_attn(e, rf, rs);
-    k_drift_reset<<<g_wide, T, 0, rs>>>(v, s);
     k_drift_reset_fin<<<1, 32, 0, rs>>>(v, s);
-    n += 6;
+    n += 5;
     if (body) {
       cudaGraph_t bg = nullptr;
       if (cudaStreamEndCapture(e->aux, &bg) != cudaSuccess) e->capture_failed = true;

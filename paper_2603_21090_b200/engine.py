@@ -97,7 +97,7 @@ class _Tables:
     edge tables, the gamma^k table and the scratch grow independently."""
 
     NODE_I32 = ("ring_cnt", "ring_head", "ring_ccnt", "nodecnt", "nodeadj", "nodefill",
-                "nodeoff", "cum_list", "amark", "dmark", "cum_mark")
+                "nodeoff", "cum_list", "amark", "dmark", "cum_mark", "cum_pos")
     EDGE = ("e_src", "e_dst", "e_t", "e_feat", "e_prev")
 
     def __init__(self, eng, cap_nodes, cap_edges, gpow_len):
@@ -374,10 +374,14 @@ class _SchedulerView:
 
     def estimator(self, v):
         e = self._e
-        acc = float(e._tab.drift_acc[v])
+        ctl = self._ctl()
+        if v >= e._tab.cap_nodes or int(e._tab.cum_mark[v]) != int(ctl.cum_gen) + 1:
+            return 0.0
+        pos = int(e._tab.cum_pos[v])
+        acc = float(e._tab.drift_acc[pos])
         if acc == 0.0:
             return 0.0
-        return acc * e.cfg.gamma ** (self.tau - int(e._tab.drift_touched[v]))
+        return acc * e.cfg.gamma ** (int(ctl.tau) - int(e._tab.drift_touched[pos]))
 
     def global_drift(self):
         ctl = self._ctl()
@@ -385,9 +389,8 @@ class _SchedulerView:
         if n == 0:
             return 0.0
         e = self._e
-        ids = e._tab.cum_list[:n].long()
-        acc = e._tab.drift_acc[ids].cpu().numpy()
-        touched = e._tab.drift_touched[ids].cpu().numpy()
+        acc = e._tab.drift_acc[:n].cpu().numpy()
+        touched = e._tab.drift_touched[:n].cpu().numpy()
         tau = int(ctl.tau)
         tot = 0.0
         for a, t in zip(acc, touched):
