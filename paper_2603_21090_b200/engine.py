@@ -787,6 +787,32 @@ class IncrementalEngine:
                                                           self._stream()), "full_reference")
         return out[:n, :self.dims.d].double().cpu().numpy()
 
+    def rebuild_range(self, lo: int, hi: int):
+        """Exact recompute of node ids [lo, hi); returns their layer-cache rows
+        (device tensor [hi-lo, K, d])."""
+        if hi > lo:
+            self.rebuild_nodes(range(lo, hi))
+        return self._tab.h[lo:hi, :, :self.dims.d]
+
+    def distributed_full_rebuild(self, group=None) -> int:
+        """rebuild_nodes(None) split by node-id range over the ranks of
+        `group` (every rank holds the same state: replicas). Each rank
+        recomputes its shard; an all-gather of the layer-cache rows leaves
+        every replica identical to a single-device full rebuild."""
+        from .dist import sharded_rebuild
+        n = self.node_count
+        if n == 0:
+            return 0
+        self._ensure_nodes(n)
+        rows = sharded_rebuild(self.rebuild_range, n, group)
+        tab = self._tab
+        tab.h[:n, :, :self.dims.d] = rows
+        cc = tab.ring_ccnt[:n]
+        tab.ring_ccnt[:n] = self._torch.where(cc < 0, tab.ring_cnt[:n], cc)
+        tab.valid[:n] = 1
+        tab.valid_at[:n] = self._t_now if self._m else 0.0
+        return n
+
     # convenience for the scheduler API
     def execute_rebuild(self, decision) -> int:
         if decision is None:

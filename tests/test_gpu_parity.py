@@ -128,6 +128,37 @@ def test_engine_vs_oracle_fresh_stream(cuda):
     assert_rows_close(eng.cache.h[:n].reshape(n, -1), orc.h[:n].reshape(n, -1), "h")
 
 
+def test_distributed_full_rebuild_nccl_world1(cuda):
+    """The sharded-rebuild path over NCCL (one rank here) equals rebuild_nodes(None)."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+    from paper_2603_21090_b200.engine import IncrementalEngine
+    z = load("engine_k2_wide_adaptive")
+    cfg, params, stream = case_setup(z)
+    cfg = cfg.with_(rebuild="never")
+    a = IncrementalEngine(cfg, params)
+    b = IncrementalEngine(cfg, params)
+    for bt in batches(stream, cfg.batch_size):
+        a.process_batch_arrays(bt.src, bt.dst, bt.t, bt.feat)
+        b.process_batch_arrays(bt.src, bt.dst, bt.t, bt.feat)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        assert a.distributed_full_rebuild() == a.node_count
+    finally:
+        dist.destroy_process_group()
+    b.rebuild_nodes(None)
+    n = a.node_count
+    np.testing.assert_array_equal(a.cache.h[:n], b.cache.h[:n])
+    np.testing.assert_array_equal(a.cache.valid_at[:n], b.cache.valid_at[:n])
+
+
 def test_monotonicity_error_before_mutation(cuda):
     from paper_2603_21090_b200.config import Dims, RunConfig
     from paper_2603_21090_b200.edges import MonotonicityError, TemporalEdge
