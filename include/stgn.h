@@ -241,6 +241,12 @@ const char* stgn_stage_name(int i);
  * memory-update smem bytes]. */
 int stgn_engine_info(stgn_engine* eng, int64_t* info, int n);
 
+/* Tensor-core self-test: D[N][F] = X[N][K] W[K][F] (device f32 buffers)
+ * through the split-TF32 tcgen05 path (F <= 128, N <= 256). mode 0 = the
+ * GEMM; bits: 1 pre-fill TMEM with a sentinel, 2 skip the MMA, 4 accumulate. */
+int stgn_debug_tc_gemm(int F, int N, int K, const float* W, const float* X, float* D, int mode,
+                       void* stream);
+
 /* Library version string and the sm architecture it was built for. */
 const char* stgn_version(void);
 

@@ -7,6 +7,7 @@
 #include <new>
 
 #include "batch.cuh"
+#include "tc.cuh"
 
 #ifndef STGN_VERSION
 #define STGN_VERSION "stgn 0.1.0 sm_100a"
@@ -823,5 +824,19 @@ extern "C" int stgn_engine_info(stgn_engine* e, int64_t* info, int n) {
   const int64_t v[8] = {e->graph ? 1 : 0, e->cond_used ? 1 : 0, e->launches, e->attn2_tmax,
                         e->attn2_wsm, e->num_sms, (int64_t)e->attn2_smem, (int64_t)e->mem_smem};
   for (int i = 0; i < n && i < 8; ++i) info[i] = v[i];
+  return STGN_OK;
+}
+
+extern "C" int stgn_debug_tc_gemm(int F, int N, int K, const float* W, const float* X, float* D,
+                                  int mode, void* stream) {
+  if (F < 1 || F > 128 || N < 1 || N > 256 || K < 1) return STGN_ERR_INVALID;
+  const int Kp = (K + 7) & ~7, Np = (N + 15) & ~15;
+  const size_t smem = (size_t)(256 * Kp + 2 * Np * Kp) * sizeof(float);
+  if (smem > 220 * 1024) return STGN_ERR_INVALID;
+  CUDA_TRY(cudaFuncSetAttribute((const void*)k_tc_gemm_test,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_tc_gemm_test<<<1, 128, smem, (cudaStream_t)stream>>>(F, N, K, W, X, D, mode);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
   return STGN_OK;
 }
