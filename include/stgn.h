@@ -92,6 +92,15 @@ typedef struct {
   const double *omega;
   const float *phi0;
   double bpred;
+  /* Tensor-core operands (optional; NULL = FFMA path). Each GEMM is a
+   * K-major B operand [Np][Kp] in 8x4 core matrices (element (n,k) at
+   * ((n/8)*(Kp/4) + k/4)*32 + (n%8)*4 + k%4), hi block then lo block
+   * (lo = value - trunc_tf32(value)); Np = round_up(N,16), Kp = round_up(K,8):
+   *   tcq [K]    N = H*d_k, K = d      (w_q rows 0..d-1)
+   *   tck [K][H] N = k_in,  K = d_k    (w_k[l,h] as is)
+   *   tcv [K][H] N = d_k,   K = k_in   (w_v[l,h] transposed)
+   *   tco [K]    N = d,     K = H*d_k  (w_o[l] transposed) */
+  const float *tcq, *tck, *tcv, *tco;
 } stgn_weights;
 
 /* Persistent control block (device). */

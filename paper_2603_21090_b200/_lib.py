@@ -45,7 +45,8 @@ class Config(C.Structure):
 class Weights(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in
                 ("wq", "bq", "wkt", "wv", "wo", "wmsg", "bmsg", "wgru", "ugru", "bgru", "wpred",
-                 "omega", "phi0")] + [("bpred", C.c_double)]
+                 "omega", "phi0")] + [("bpred", C.c_double)] + \
+               [(n, C.c_void_p) for n in ("tcq", "tck", "tcv", "tco")]
 
 
 class Ctl(C.Structure):

@@ -6,8 +6,10 @@
 #include <cstring>
 #include <new>
 
+#include <algorithm>
+
 #include "batch.cuh"
-#include "tc.cuh"
+#include "attn3.cuh"
 
 #ifndef STGN_VERSION
 #define STGN_VERSION "stgn 0.1.0 sm_100a"
@@ -18,6 +20,7 @@
 // ---------------------------------------------------------------------------
 typedef void (*attn_fn_t)(Geo, AttnWeights, RingSrc, FlatSrc, int);
 typedef void (*attn2_fn_t)(Geo, EngW, RingSrc, int, int);
+typedef void (*attn3_fn_t)(Geo, TcW, RingSrc, int);
 
 template <bool FLAT>
 static attn_fn_t pick_attn(const Geo& g) {
@@ -86,6 +89,11 @@ struct stgn_engine {
   attn2_fn_t attn2 = nullptr; // engine recompute kernel
   size_t attn2_smem = 0;
   int attn2_tmax = 0, attn2_wsm = 0;
+  attn3_fn_t attn3 = nullptr;  // tcgen05 recompute kernel (when the TMEM plan fits)
+  size_t attn3_smem = 0;
+  int attn3_tmax = 0;
+  TcW tcw;
+  bool tc_ok = false, use_tc = false;
   EngW ew;
   size_t mem_smem = 0;
   int mem_wsm = 0;
@@ -192,6 +200,23 @@ int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engin
     e->attn2_wsm = (int)(wsm / 4 * 4);
     e->attn2_smem = (size_t)(tmax * row + e->attn2_wsm) * sizeof(float);
   }
+  memset(&e->tcw, 0, sizeof(e->tcw));
+  if (tc_plan(e->g, &e->tcw)) {  // tcgen05 path: q~/ubar rows + c rows + one staged block
+    const int64_t budget = 220 * 1024 / 4;
+    const int64_t wbuf = attn3_wbuf_floats(e->g, e->tcw) + 32;
+    int64_t tmax = (budget - wbuf) / attn3_row_floats(e->g);
+    if (tmax > A2_TMAX) tmax = A2_TMAX;
+    if (tmax >= 8) {
+      e->attn3_tmax = (int)tmax;
+      e->attn3_smem = (size_t)(tmax * attn3_row_floats(e->g) + wbuf) * sizeof(float);
+      e->attn3 = e->g.d_e > 0 ? (e->g.H > 2 ? attn3_kernel<6, 4> : attn3_kernel<6, 2>)
+                              : (e->g.H > 2 ? attn3_kernel<0, 4> : attn3_kernel<0, 2>);
+      e->tc_ok = cudaFuncSetAttribute((const void*)e->attn3,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)e->attn3_smem) == cudaSuccess;
+      cudaGetLastError();
+    }
+  }
   ce = cudaFuncSetAttribute((const void*)e->attn2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)e->attn2_smem);
   if (ce != cudaSuccess) {
@@ -272,6 +297,15 @@ int stgn_engine_set_weights(stgn_engine* e, const stgn_weights* w) {
   e->ew.ld_kin = (int)round_up(e->g.k_in, 4);
   e->ew.ld_dk = (int)round_up(e->g.d_k, 4);
   e->ew.ld_d = (int)round_up(e->g.d, 4);
+  e->use_tc = e->tc_ok && w->tcq && w->tck && w->tcv && w->tco;
+  if (e->use_tc) {
+    e->tcw.wq = w->tcq;
+    e->tcw.wk = w->tck;
+    e->tcw.wv = w->tcv;
+    e->tcw.wo = w->tco;
+    e->tcw.bq = w->bq;
+    e->tcw.omega = w->omega;
+  }
   e->aw.wq = w->wq;
   e->aw.wkt = w->wkt;
   e->aw.wv = w->wv;
@@ -317,8 +351,11 @@ static RingSrc ring_src(const stgn_engine* e) {
 }
 
 static void launch_attn(const stgn_engine* e, const RingSrc& rs, cudaStream_t st) {
-  e->attn2<<<e->num_sms, A2_THREADS, e->attn2_smem, st>>>(e->g, e->ew, rs, e->attn2_tmax,
-                                                          e->attn2_wsm);
+  if (e->use_tc)
+    e->attn3<<<e->num_sms, A3_THREADS, e->attn3_smem, st>>>(e->g, e->tcw, rs, e->attn3_tmax);
+  else
+    e->attn2<<<e->num_sms, A2_THREADS, e->attn2_smem, st>>>(e->g, e->ew, rs, e->attn2_tmax,
+                                                            e->attn2_wsm);
 }
 
 static const char* kStageNames[] = {"group+ring", "affected_bfs", "change_records",
@@ -821,9 +858,10 @@ extern "C" int stgn_pipeline_many(const stgn_dims* dims, int64_t N, int64_t E, c
 
 extern "C" int stgn_engine_info(stgn_engine* e, int64_t* info, int n) {
   if (!e || !info) return STGN_ERR_INVALID;
-  const int64_t v[8] = {e->graph ? 1 : 0, e->cond_used ? 1 : 0, e->launches, e->attn2_tmax,
-                        e->attn2_wsm, e->num_sms, (int64_t)e->attn2_smem, (int64_t)e->mem_smem};
-  for (int i = 0; i < n && i < 8; ++i) info[i] = v[i];
+  const int64_t v[10] = {e->graph ? 1 : 0, e->cond_used ? 1 : 0, e->launches, e->attn2_tmax,
+                         e->attn2_wsm, e->num_sms, (int64_t)e->attn2_smem, (int64_t)e->mem_smem,
+                         e->use_tc ? 1 : 0, e->attn3_tmax};
+  for (int i = 0; i < n && i < 10; ++i) info[i] = v[i];
   return STGN_OK;
 }
 

@@ -409,7 +409,8 @@ class IncrementalEngine:
     """
 
     def __init__(self, cfg: RunConfig, params: ModelParameters, *, recompute: str = "affected",
-                 max_batch: int | None = None, device: int | None = None):
+                 max_batch: int | None = None, device: int | None = None,
+                 tensor_cores: bool = True):
         cfg.validate()
         if cfg.mode != "exact":
             raise ConfigError("the B200 engine implements exact mode (delta mode is out of scope)")
@@ -427,6 +428,7 @@ class IncrementalEngine:
         self.ld_s, self.ld_d = _rup(dm.d_s, 4), _rup(dm.d, 4)
         self.ld_e = _rup(max(dm.d_e, 1), 4)
         self.recompute = recompute
+        self.tensor_cores = bool(tensor_cores)  # tcgen05 split-TF32 GEMMs where the plan fits
         self._L = _lib.lib()
         self._dims = _lib.dims_struct(dm)
         self._max_batch = max(int(max_batch or cfg.batch_size), 1)
@@ -518,9 +520,34 @@ class IncrementalEngine:
             "omega": f64(p.omega),
             "phi0": torch.tensor(phi0, dtype=torch.float32, device=self.device),
         }
+        if self.tensor_cores:
+            wqx = wq_full[:, :dm.d, :].transpose(0, 2, 1)            # (K, HD, d)   [n][k]
+            W["tcq"] = self._pack_kmajor(wqx)
+            W["tck"] = self._pack_kmajor(p.w_k)                         # (K, H, k_in, d_k)
+            W["tcv"] = self._pack_kmajor(np.transpose(p.w_v, (0, 1, 3, 2)))  # (K, H, d_k, k_in)
+            W["tco"] = self._pack_kmajor(np.transpose(p.w_o, (0, 2, 1)))     # (K, d, HD)
         self._w = W
         ws = _lib.Weights(**{k: v.data_ptr() for k, v in W.items()}, bpred=float(p.b_pred))
         _lib.check(self._L.stgn_engine_set_weights(self._handle, C.byref(ws)), "set_weights")
+
+    def _pack_kmajor(self, B):
+        """(..., N, K) float64 -> (..., 2*Np*Kp) float32 tensor: the K-major
+        tcgen05 B operand (8x4 core matrices), hi block then lo block."""
+        B = np.asarray(B, dtype=np.float64)
+        *lead, N, K = B.shape
+        Np, Kp = _rup(N, 16), _rup(K, 8)
+        Bp = np.zeros((*lead, Np, Kp))
+        Bp[..., :N, :K] = B
+        hi = Bp.astype(np.float32)
+        trunc = (hi.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+        lo = (Bp - trunc.astype(np.float64)).astype(np.float32)
+        n, k = np.meshgrid(np.arange(Np), np.arange(Kp), indexing="ij")
+        idx = (((n // 8) * (Kp // 4) + k // 4) * 32 + (n % 8) * 4 + k % 4).ravel()
+        out = np.zeros((*lead, 2, Np * Kp), dtype=np.float32)
+        out[..., 0, idx] = hi.reshape(*lead, Np * Kp)
+        out[..., 1, idx] = lo.reshape(*lead, Np * Kp)
+        return self._torch.tensor(np.ascontiguousarray(out.reshape(*lead, 2 * Np * Kp)),
+                                  device=self.device)
 
     def _bind(self):
         self._state = self._tab.struct()
@@ -674,10 +701,11 @@ class IncrementalEngine:
 
     def info(self) -> dict:
         """Engine facts from the C ABI (graph replay, conditional rebuild, tiles)."""
-        buf = (C.c_int64 * 8)()
-        _lib.check(self._L.stgn_engine_info(self._handle, buf, 8), "info")
+        buf = (C.c_int64 * 10)()
+        _lib.check(self._L.stgn_engine_info(self._handle, buf, 10), "info")
         keys = ("graph_active", "conditional_rebuild", "launches_per_batch", "attn_tile_rows",
-                "attn_staged_weight_floats", "num_sms", "attn_smem_bytes", "memory_smem_bytes")
+                "attn_staged_weight_floats", "num_sms", "attn_smem_bytes", "memory_smem_bytes",
+                "tensor_cores", "tc_tile_rows")
         return {k: int(buf[i]) for i, k in enumerate(keys)}
 
     def _after_batch(self, B, t_last, top):

@@ -1,5 +1,6 @@
 """tcgen05 split-TF32 GEMM self-test (descriptor/layout/TMEM round trip)
-against a float64 numpy product; tolerance 2e-6 relative to sum|x||w|."""
+against a float64 numpy product; tolerance 2e-6 relative to sum|x||w|.
+Also checks the engine's tensor-core recompute against its FFMA twin."""
 
 import ctypes as C
 
@@ -9,8 +10,9 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("mode", [8, 40], ids=["smem-smem", "tmem-A"])
 @pytest.mark.parametrize("F,N,K", [(100, 48, 96), (128, 16, 8), (7, 33, 50), (64, 64, 100)])
-def test_tc_split_tf32_gemm(F, N, K):
+def test_tc_split_tf32_gemm(F, N, K, mode):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
@@ -23,9 +25,34 @@ def test_tc_split_tf32_gemm(F, N, K):
     tW, tX = torch.tensor(W, device=dev), torch.tensor(X, device=dev)
     tD = torch.zeros((N, F), dtype=torch.float32, device=dev)
     stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-    _lib.check(L.stgn_debug_tc_gemm(F, N, K, tW.data_ptr(), tX.data_ptr(), tD.data_ptr(), 0,
+    # mode 8: both operands K-major in shared memory; 40: A (rows of X) in TMEM
+    _lib.check(L.stgn_debug_tc_gemm(F, N, K, tW.data_ptr(), tX.data_ptr(), tD.data_ptr(), mode,
                                     stream), "tc_gemm")
     ref = X.astype(np.float64) @ W.astype(np.float64)
     scale = np.abs(X).astype(np.float64) @ np.abs(W).astype(np.float64)
     err = np.max(np.abs(tD.cpu().numpy() - ref) / scale)
     assert err < 2e-6, f"split-TF32 relative error {err:.3e}"
+
+
+@pytest.mark.parametrize("name", ["c4_shape_tiny", "k2_sum_window", "selfloops_dups"])
+def test_engine_tensor_core_path_vs_ffma(name):
+    """Both recompute kernels meet the reference tolerances; the tcgen05 one is
+    actually selected for these widths."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from golden_util import batches, case_setup, load
+    from parity_util import assert_rows_close
+    from paper_2603_21090_b200.engine import IncrementalEngine
+    z = load("engine_" + name)
+    cfg, params, stream = case_setup(z)
+    n = int(z["node_count"])
+    for tc in (True, False):
+        eng = IncrementalEngine(cfg, params, tensor_cores=tc)
+        preds = []
+        for b in batches(stream, cfg.batch_size):
+            preds.extend(eng.process_batch_arrays(b.src, b.dst, b.t, b.feat).tolist())
+        assert eng.info()["tensor_cores"] == int(tc)
+        assert np.max(np.abs(np.array(preds) - z["preds"])) <= 1e-5
+        assert_rows_close(eng.cache.h[:n].reshape(n, -1), z["h"].reshape(n, -1), f"h tc={tc}")
+        assert_rows_close(eng.memory.states[:n], z["memory"], f"memory tc={tc}")
