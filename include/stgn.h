@@ -256,6 +256,18 @@ int stgn_engine_info(stgn_engine* eng, int64_t* info, int n);
 int stgn_debug_tc_gemm(int F, int N, int K, const float* W, const float* X, float* D, int mode,
                        void* stream);
 
+/*
+ * Native synthetic stream generator: the reference's generate_stream
+ * (S/streamio.py:86-145) for d_e = 0, edge for edge. rng_state[6] is the
+ * numpy PCG64 bit-generator state of default_rng(seed) as
+ * {state_hi, state_lo, inc_hi, inc_lo, has_uint32, uinteger}; the state after
+ * the last draw goes to rng_state_out (may be NULL). Host buffers src, dst
+ * (int64) and t (float64) of length m.
+ */
+int stgn_generate_stream(const uint64_t* rng_state, int64_t n, int64_t m, int32_t preferential,
+                         double burstiness, int64_t* src, int64_t* dst, double* t,
+                         uint64_t* rng_state_out);
+
 /* Library version string and the sm architecture it was built for. */
 const char* stgn_version(void);
 

@@ -16,8 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "_stgn.so")
-SOURCES = ["capi.cu"]
-DEPS = ["capi.cu", "common.cuh", "attn.cuh", "attn2.cuh", "gemm.cuh", "batch.cuh", "tc.cuh", "attn3.cuh"]
+SOURCES = ["capi.cu", "gen.cpp"]
+DEPS = ["capi.cu", "common.cuh", "attn.cuh", "attn2.cuh", "gemm.cuh", "batch.cuh", "tc.cuh", "attn3.cuh", "gen.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",

@@ -54,10 +54,23 @@ class EdgeArrays:
 
 
 def generate_stream(seed: int, n: int, m: int, attachment: str = "uniform",
-                    burstiness: float = 1.0, d_e: int = 4) -> EdgeArrays:
+                    burstiness: float = 1.0, d_e: int = 4,
+                    native: bool | None = None) -> EdgeArrays:
     """Integer-tick synthetic stream; alternating cold/hot epochs of 50 ticks
     (hot epochs draw endpoints from the first 10% of ids when bursty), and
-    degree-biased destinations under `preferential` (p = 0.8)."""
+    degree-biased destinations under `preferential` (p = 0.8).
+
+    native (default: when d_e == 0) runs the C generator of the in-tree
+    library (csrc/gen.cpp), which replays numpy's PCG64 draws and yields the
+    same edges as the loop below (tests/test_streamio_native.py); streams with
+    edge features always use the loop (numpy's normal sampler is not
+    restated natively)."""
+    if native is None:
+        native = d_e == 0
+    if native and d_e != 0:
+        raise ValueError("the native generator covers d_e = 0 streams only")
+    if native:
+        return _generate_native(seed, n, m, attachment, burstiness)
     if n < 2:
         raise ValueError("need at least 2 nodes")
     if m < 1:
@@ -107,6 +120,39 @@ def generate_stream(seed: int, n: int, m: int, attachment: str = "uniform",
             k += 1
         tick += 1
     return EdgeArrays(src, dst, ts, feat)
+
+
+def _check_gen_args(n, m, attachment, burstiness):
+    if n < 2:
+        raise ValueError("need at least 2 nodes")
+    if m < 1:
+        raise ValueError("need at least 1 edge")
+    if attachment not in ("uniform", "preferential"):
+        raise ValueError(f"unknown attachment {attachment!r}")
+    if burstiness < 1.0:
+        raise ValueError("burstiness must be >= 1")
+
+
+def _generate_native(seed, n, m, attachment, burstiness) -> EdgeArrays:
+    import ctypes as C
+
+    from . import _lib
+    _check_gen_args(n, m, attachment, burstiness)
+    st = np.random.default_rng(seed).bit_generator.state
+    mask = (1 << 64) - 1
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    rs = np.array([s >> 64, s & mask, inc >> 64, inc & mask, st["has_uint32"], st["uinteger"]],
+                  dtype=np.uint64)
+    src = np.empty(m, dtype=np.int64)
+    dst = np.empty(m, dtype=np.int64)
+    ts = np.empty(m, dtype=np.float64)
+    vp = C.c_void_p
+    rc = _lib.lib().stgn_generate_stream(vp(rs.ctypes.data), int(n), int(m),
+                                         int(attachment == "preferential"), float(burstiness),
+                                         vp(src.ctypes.data), vp(dst.ctypes.data),
+                                         vp(ts.ctypes.data), None)
+    _lib.check(rc, "stgn_generate_stream")
+    return EdgeArrays(src, dst, ts, np.empty((m, 0), dtype=np.float64))
 
 
 def serialize_stream(edges: EdgeArrays, d_e: int) -> str:

@@ -29,6 +29,9 @@ def main():
     ap.add_argument("--nodes", type=int, default=2_600_000)
     ap.add_argument("--recompute", default="affected")
     ap.add_argument("--rebuild", default="adaptive")
+    ap.add_argument("--graph", action="store_true",
+                    help="keep CUDA-graph replay (ncu cannot profile kernels of a graph "
+                         "with conditional nodes; the default runs the same kernels eagerly)")
     a = ap.parse_args()
     dims = Dims(d_s=100, d_e=0, d_t=100, d_m=100, d_k=50, heads=2, layers=2)
     cfg = RunConfig(dims=dims, batch_size=a.batch, fanout=10, nodes=a.nodes, aggregator="last",
@@ -36,6 +39,8 @@ def main():
     B = a.batch
     st = generate_stream(2, a.nodes, a.prefix + a.batches * B, attachment="preferential", d_e=0)
     eng = IncrementalEngine(cfg, init_params(0, dims), recompute=a.recompute)
+    if not a.graph:
+        eng.set_profiling(True)
     for lo in range(0, a.prefix + a.batches * B, B):
         eng.process_batch_arrays(st.src[lo:lo + B], st.dst[lo:lo + B], st.t[lo:lo + B])
     torch.cuda.synchronize()
