@@ -6,17 +6,20 @@ Workload (BASELINE.json metric; SURVEY.md §8d config C4 at B=600):
   dims d_s=d_m=d_t=100, d_k=50, H=2, K=2, d_e=0, L=10, aggregator last,
   drift-aware rebuild (adaptive, gamma=0.9, delta_max=0.5, alpha=0.1),
   init_params(0), synthetic preferential power-law stream
-  generate_stream(seed=2, n=2.6M, ...) (the reference's generator, same
-  edges). The engine first ingests the stream's first 120K edges (the
-  window the reference CPU path is quoted on), then W warm-up batches,
-  then K timed batches of 600 edges.
+  generate_stream(seed=2, n=2.6M, m=30M) (the reference's generator, same
+  edges, replayed natively). The engine fast-forwards through the stream
+  (device-resident batches, one graph replay each) and times the LAST
+  batches of the 30M-edge stream: W warm-up, K timed, then the e2e leg and
+  the per-stage profile. On the way it also times 100 batches right after
+  the first 120K edges: the window the CPU reference is timed on
+  ("window"); at the end it sweeps the batch size over 100..10K ("sweep").
 
 One JSON line (rank 0). `value` = device-timed throughput with inputs
 already in HBM (CUDA events on the engine stream, max over ranks);
 `e2e` = the same metric through the public host-buffer API
 (process_batch_arrays: H2D of the batch + D2H of the scores per step).
-Inputs are larger than L2 (26 GB of resident state; each batch touches
-fresh rings), so no explicit flush.
+Inputs are larger than L2 (26 GB of resident state; a batch at the end of
+the stream touches ~1 GB of rings), so no explicit flush.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
@@ -48,7 +51,13 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=600)
     ap.add_argument("--nodes", type=int, default=2_600_000)
-    ap.add_argument("--prefix", type=int, default=120_000)
+    ap.add_argument("--edges", type=int, default=30_000_000,
+                    help="stream length; the timed batches are the last ones of it")
+    ap.add_argument("--prefix", type=int, default=120_000,
+                    help="CPU-reference window: edges fast-forwarded before its timed batches")
+    ap.add_argument("--window-steps", type=int, default=100)
+    ap.add_argument("--sweep", default="100,300,1000,3000,10000")
+    ap.add_argument("--sweep-steps", type=int, default=30)
     ap.add_argument("--seed", type=int, default=2)
     ap.add_argument("--rebuild", default="adaptive")
     ap.add_argument("--recompute", default="affected", choices=["affected", "direct"])
@@ -69,13 +78,17 @@ def workload(args):
     return dims, cfg, init_params(0, dims)
 
 
-def config_json(args, n_gpus):
+def config_json(args, n_gpus, pos0=None):
     return {"workload": "C4: TGN 2-layer exact-mode incremental inference, synthetic "
                         "preferential power-law stream, drift-aware rebuild",
             "nodes": args.nodes, "batch_edges": args.batch, "fanout_L": 10, "layers_K": 2,
             "d_memory": 100, "d_time": 100, "heads": 2, "d_k": 50, "d_edge": 0,
-            "stream": f"generate_stream(seed={args.seed}+rank, preferential), first "
-                      f"{args.prefix} edges ingested before warm-up",
+            "edges": args.edges,
+            "stream": (f"generate_stream(seed={args.seed}+rank, n={args.nodes}, m={args.edges}, "
+                       f"preferential, d_e=0); timed batches are the last of the stream, after "
+                       f"{pos0} edges are ingested" if pos0 is not None else
+                       f"generate_stream(seed={args.seed}, preferential, d_e=0); timed batches "
+                       f"start after the first {args.prefix} edges"),
             "rebuild": args.rebuild, "recompute": args.recompute,
             "parallelism": f"replicas{n_gpus}" if n_gpus > 1 else "single",
             "l2": "inputs larger than L2 (26 GB resident state), no flush"}
@@ -189,68 +202,90 @@ def run_reference(args, world, rank):
 
 
 # ---------------------------------------------------------------------------
+def _timed_batches(torch, stream, feed, k0, K):
+    """Feed batches k0..k0+K-1 of a DeviceStream, one CUDA event after each;
+    returns (total ms, per-batch ms)."""
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    for k in range(K):
+        feed.batch(k0 + k)
+        ev[k + 1].record(stream)
+    torch.cuda.synchronize()
+    per = np.array([ev[k].elapsed_time(ev[k + 1]) for k in range(K)])
+    return float(ev[0].elapsed_time(ev[K])), per
+
+
+def _max_over_ranks(torch, dist, world, dev, x):
+    if world == 1:
+        return x
+    tt = torch.tensor([x], device=dev, dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return float(tt.item())
+
+
 def run_ours(args, world, rank, local_rank):
     import torch
     import torch.distributed as dist
 
     from paper_2603_21090_b200.engine import IncrementalEngine
+    from paper_2603_21090_b200.feeder import DeviceStream
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dims, cfg, params = workload(args)
     B, W, K = args.batch, args.warmup, args.steps
     KE = args.e2e_steps if args.e2e_steps is not None else min(K, 100)
     P = args.profile_batches
-    n_edges = args.prefix + (W + K + KE + P) * B
-    st = make_stream(args, n_edges, rank)
+    sweep = [int(x) for x in args.sweep.split(",") if x] if args.sweep else []
+    SW = args.sweep_steps
+    tail = (W + K + KE + P) * B
+    total = max(args.edges, tail + B)
+    n_sweep = sum((3 + SW) * b for b in sweep)
+    t_gen = time.perf_counter()
+    st = make_stream(args, total + n_sweep, rank)
+    t_gen = time.perf_counter() - t_gen
     eng = IncrementalEngine(cfg, params, recompute=args.recompute)
-    eng.reserve(nodes=args.nodes, edges=n_edges + B, batch=B, batches=n_edges // B + 8)
-    # 1) ingest the prefix through the public API (untimed)
-    for lo in range(0, args.prefix, B):
-        eng.process_batch_arrays(st.src[lo:lo + B], st.dst[lo:lo + B], st.t[lo:lo + B])
+    eng.reserve(nodes=args.nodes, edges=total + n_sweep + B, batch=B,
+                batches=(total + n_sweep) // min([B] + sweep) + 8)
+    stream = eng._torch.cuda.current_stream(dev)
+    pos0 = total - tail            # the timed batches are the last ones of the stream
+    t_ff = time.perf_counter()
+    feed = DeviceStream(eng, st, B, 0, pos0)
+    # 0) fast-forward; on the way, time the window the CPU reference is measured on
+    win = None
+    wk0 = args.prefix // B
+    if args.prefix and wk0 + args.window_steps <= feed.n_batches:
+        feed.run(0, wk0, report_last=False)
+        w_ms, w_per = _timed_batches(torch, stream, feed, wk0, args.window_steps)
+        win = {"value": args.window_steps * B / (w_ms / 1e3), "unit": UNIT,
+               "p50_ms": float(np.percentile(w_per, 50)), "p99_ms": float(np.percentile(w_per, 99)),
+               "stream_position": f"edges {wk0 * B}..{(wk0 + args.window_steps) * B}",
+               "steps": args.window_steps}
+        feed.run(wk0 + args.window_steps, None, report_last=True)
+    else:
+        feed.run(0, None, report_last=True)
     eng.sync()
-    pos = args.prefix
-    # 2) device-resident inputs for warm-up + timed batches
-    batches = []
-    for k in range(W + K):
-        lo = pos + k * B
-        sl = slice(lo, lo + B)
-        batches.append((torch.tensor(st.src[sl].astype(np.int32), device=dev),
-                        torch.tensor(st.dst[sl].astype(np.int32), device=dev),
-                        torch.tensor(st.t[sl], device=dev),
-                        int(max(st.src[sl].max(), st.dst[sl].max())),
-                        float(st.t[sl][0]), float(st.t[sl][-1])))
-    torch.cuda.synchronize()
-    for k in range(W):
-        s_, d_, t_, mx, t0, t1 = batches[k]
-        eng.process_batch_device(s_, d_, t_, max_id=mx, t_first=t0, t_last=t1)
-    torch.cuda.synchronize()
-    stream = torch.cuda.current_stream(dev)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+    t_ff = time.perf_counter() - t_ff
+    del feed
+    # 1) device-resident inputs for warm-up + timed batches
+    feed = DeviceStream(eng, st, B, pos0, pos0 + (W + K) * B)
+    feed.run(0, W, report_last=True)
+    rep_nA = int(eng._rep.affected)
     if world > 1:
         dist.barrier()
-    torch.cuda.synchronize()
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)  # let the sampler attach before the timed region
-    ev[0].record(stream)
-    for k in range(K):
-        s_, d_, t_, mx, t0, t1 = batches[W + k]
-        eng.process_batch_device(s_, d_, t_, max_id=mx, t_first=t0, t_last=t1)
-        ev[k + 1].record(stream)
-    torch.cuda.synchronize()
+    total_ms, per = _timed_batches(torch, stream, feed, W, K)
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
-    per = np.array([ev[k].elapsed_time(ev[k + 1]) for k in range(K)])  # ms
-    total_ms = float(ev[0].elapsed_time(ev[K]))
-    if world > 1:
-        tt = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
+    total_ms = _max_over_ranks(torch, dist, world, dev, total_ms)
     value = world * K * B / (total_ms / 1e3)
-    pos += (W + K) * B
+    pos = pos0 + (W + K) * B
+    del feed
 
-    # 3) e2e: public host-buffer API, H2D + D2H inside every step
+    # 2) e2e: public host-buffer API, H2D + D2H inside every step
     e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     host = [(np.ascontiguousarray(st.src[pos + k * B: pos + (k + 1) * B]),
              np.ascontiguousarray(st.dst[pos + k * B: pos + (k + 1) * B]),
@@ -268,17 +303,13 @@ def run_ours(args, world, rank, local_rank):
     e_ev[1].record(stream)
     torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall
-    e2e_ms = float(e_ev[0].elapsed_time(e_ev[1]))
-    if world > 1:
-        tt = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+    e2e_ms = _max_over_ranks(torch, dist, world, dev, float(e_ev[0].elapsed_time(e_ev[1])))
     e2e_value = world * KE * B / (e2e_ms / 1e3)
     pos += KE * B
 
-    # 4) per-stage device times (events, no graph) for the roofline
+    # 3) per-stage device times (events, no graph) for the roofline
     eng.set_profiling(True)
-    stage_acc, attn_bytes, attn_flops, attn_ms, nA_list = {}, [], [], [], []
+    stage_acc, attn_bytes, attn_flops, attn_ms, nA_list, eA_list = {}, [], [], [], [], []
     g = dims
     for k in range(P):
         sl = slice(pos + k * B, pos + (k + 1) * B)
@@ -290,19 +321,13 @@ def run_ours(args, world, rank, local_rank):
         # one launch recomputes A (pre-batch memory) and V_direct (post-batch memory)
         nA = int(r.affected) + (int(r.direct) if args.recompute == "affected" else 0)
         EA = int(r.entries_affected) + int(r.entries_direct)
-        # algorithmic bytes: per node mem row + ring meta + K*d output,
-        # per entry K*d frozen payload + d_e feat + 8 B timestamp
-        by = nA * (4 * g.d_s + 4 * g.layers * g.d + 16) + EA * (4 * g.layers * g.d + 4 * g.d_e + 8)
-        # FLOPs of the folded formulation actually executed
-        per_node_l = 2 * (g.query_in * g.heads * g.d_k + g.heads * g.d_k * g.key_in +
-                          g.heads * g.key_in * g.d_k + g.heads * g.d_k * g.d)
-        per_entry_l = 2 * (2 * g.heads * g.key_in)
-        fl = g.layers * (nA * per_node_l + EA * per_entry_l)
-        attn_bytes.append(by)
-        attn_flops.append(fl)
+        attn_bytes.append(recompute_bytes(g, nA, EA))
+        attn_flops.append(recompute_flops(g, nA, EA))
         attn_ms.append(times["recompute"])
         nA_list.append(nA)
+        eA_list.append(EA)
     eng.set_profiling(False)
+    pos += P * B
     stage_ms = {nm: float(np.mean(v)) for nm, v in stage_acc.items()}
     a_ms = float(np.mean(attn_ms))
     achieved_gbs = float(np.mean(attn_bytes)) / (a_ms / 1e3) / 1e9
@@ -312,19 +337,36 @@ def run_ours(args, world, rank, local_rank):
         with open(pk_path) as fh:
             peaks = json.load(fh)
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else \
+        "fallback (B200_PROFILING.md)"
+    info = eng.info()
+
+    # 4) batch-size sweep (C4: 100..10K edges/batch) at the end-of-stream state
+    sweep_out = []
+    for b in sweep:
+        sf = DeviceStream(eng, st, b, pos, pos + (3 + SW) * b)
+        sf.run(0, 3, report_last=True)
+        s_ms, s_per = _timed_batches(torch, stream, sf, 3, SW)
+        s_ms = _max_over_ranks(torch, dist, world, dev, s_ms)
+        sweep_out.append({"batch_edges": b, "value": world * SW * b / (s_ms / 1e3),
+                          "p50_ms": float(np.percentile(s_per, 50)),
+                          "p99_ms": float(np.percentile(s_per, 99)),
+                          "affected_last": int(eng._rep.affected)})
+        pos += (3 + SW) * b
+        del sf
 
     line = None
     if rank == 0:
         h2d = B * (4 + 4 + 8) + 64
         d2h = B * 8 + 128
+        kname = "attn3_kernel (tcgen05)" if info.get("tensor_cores") else "attn2_kernel"
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": total_ms / K,
             "p50_ms": float(np.percentile(per, 50)), "p99_ms": float(np.percentile(per, 99)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (reference generator, random-init weights)",
-            "config": config_json(args, world),
+            "data": "synthetic (reference generator, native replay; random-init weights)",
+            "config": config_json(args, world, pos0),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "p50_ms": float(np.percentile(e2e_lat, 50) * 1e3),
@@ -332,15 +374,21 @@ def run_ours(args, world, rank, local_rank):
                     "wall_s": t_wall},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak,
                          "unit": "GB/s", "frac": achieved_gbs / hbm_peak, "traffic": None,
-                         "kernel": "attn2_kernel (recompute: A with pre-batch memory + V_direct with post-batch memory)",
+                         "kernel": kname + ": recompute of A (pre-batch memory) + V_direct "
+                                           "(post-batch memory), one launch",
                          "avg_launch_ms": a_ms, "algorithmic_bytes": float(np.mean(attn_bytes)),
                          "flops": float(np.mean(attn_flops)),
                          "tflops": float(np.mean(attn_flops)) / (a_ms / 1e3) / 1e12,
-                         "peak_source": peak_src, "mean_affected": float(np.mean(nA_list))},
+                         "peak_source": peak_src, "rows_per_launch": float(np.mean(nA_list)),
+                         "entries_per_launch": float(np.mean(eA_list))},
             "stage_ms": stage_ms,
+            "affected_per_batch": rep_nA,
             "gpu_launches": (int(launches) + 1) * K,  # + k_set_hdr per batch
             "clocks": clk,
-            "engine": eng.info(),
+            "engine": info,
+            "window": win,
+            "sweep": sweep_out,
+            "setup_s": {"generate": t_gen, "fast_forward": t_ff},
         }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cv, ctimes, sample = cpu_reference(args, max(1, args.cpu_batches), st)
@@ -349,6 +397,22 @@ def run_ours(args, world, rank, local_rank):
                                 "host_nproc": os.cpu_count()}
     if line is not None:
         print(json.dumps(line), flush=True)
+
+
+def recompute_bytes(g, rows, entries):
+    """Algorithmic HBM bytes of one recompute launch: per row
+    the memory row, ring meta and the K*d output; per ring entry the K*d
+    frozen payload, d_e features and the 8 B timestamp."""
+    return rows * (4 * g.d_s + 4 * g.layers * g.d + 16) + \
+        entries * (4 * g.layers * g.d + 4 * g.d_e + 8)
+
+
+def recompute_flops(g, rows, entries):
+    """FLOPs of the folded formulation the kernel executes."""
+    per_node_l = 2 * (g.query_in * g.heads * g.d_k + g.heads * g.d_k * g.key_in +
+                      g.heads * g.key_in * g.d_k + g.heads * g.d_k * g.d)
+    per_entry_l = 2 * (2 * g.heads * g.key_in)
+    return g.layers * (rows * per_node_l + entries * per_entry_l)
 
 
 def main():
