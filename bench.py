@@ -359,7 +359,9 @@ def run_ours(args, world, rank, local_rank):
     if rank == 0:
         h2d = B * (4 + 4 + 8) + 64
         d2h = B * 8 + 128
-        kname = "attn3_kernel (tcgen05)" if info.get("tensor_cores") else "attn2_kernel"
+        kname = ("attn4_kernel (tcgen05 bf16x3, 128-row tiles)" if info.get("bf16x3") else
+                 "attn3_kernel (tcgen05 split-TF32)" if info.get("tensor_cores") else
+                 "attn2_kernel (FFMA)")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": total_ms / K,

@@ -101,6 +101,18 @@ typedef struct {
    *   tcv [K][H] N = d_k,   K = k_in   (w_v[l,h] transposed)
    *   tco [K]    N = d,     K = H*d_k  (w_o[l] transposed) */
   const float *tcq, *tck, *tcv, *tco;
+  /* bf16x3 tensor-core operands of the 128-row recompute kernel (optional;
+   * used when H = 2 and the TMEM plan fits, else the split-TF32 ones): K-major
+   * bf16 B operands [Np][Kp] in 8x8 core matrices (element (n,k) at
+   * ((n/8)*(Kp/8) + k/8)*64 + (n%8)*8 + k%8), hi block then lo block
+   * (lo = bf16(w - hi)); Kp = round_up(K,16), Np = round_up(N,16), Kq = round_up(d_k,16):
+   *   t4q [K]    N = H*Kq (head h at rows h*Kq), K = d            (w_q rows 0..d-1)
+   *   t4k [K][H] N = k_in, K = d_k   w_k / sqrt(d_k), time-encoding rows * sqrt(1/d_t)
+   *   t4v [K][H] N = d_k,  K = k_in  w_v^T, time-encoding columns * sqrt(1/d_t)
+   *   t4o [K]    N = d,    K = H*Kq (head h at h*Kq)               w_o^T
+   *   t4bq [K][H][Kq] float   phi(0) . w_q[l, h, d:, :] (zero padded) */
+  const uint16_t *t4q, *t4k, *t4v, *t4o;
+  const float *t4bq;
 } stgn_weights;
 
 /* Persistent control block (device). */
@@ -247,7 +259,8 @@ const char* stgn_stage_name(int i);
 /* Engine facts, up to n of: [graph replay active, rebuild block is a
  * device-side conditional graph node, kernel launches per batch, attention
  * tile rows, staged-weight floats, SM count, attention smem bytes,
- * memory-update smem bytes]. */
+ * memory-update smem bytes, split-TF32 tensor-core kernel active, its tile
+ * rows, bf16x3 128-row kernel active, its smem bytes]. */
 int stgn_engine_info(stgn_engine* eng, int64_t* info, int n);
 
 /* Tensor-core self-test: D[N][F] = X[N][K] W[K][F] (device f32 buffers)

@@ -46,7 +46,8 @@ class Weights(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in
                 ("wq", "bq", "wkt", "wv", "wo", "wmsg", "bmsg", "wgru", "ugru", "bgru", "wpred",
                  "omega", "phi0")] + [("bpred", C.c_double)] + \
-               [(n, C.c_void_p) for n in ("tcq", "tck", "tcv", "tco")]
+               [(n, C.c_void_p) for n in ("tcq", "tck", "tcv", "tco", "t4q", "t4k", "t4v", "t4o",
+                                          "t4bq")]
 
 
 class Ctl(C.Structure):

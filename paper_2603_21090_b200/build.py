@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "_stgn.so")
 SOURCES = ["capi.cu", "gen.cpp"]
-DEPS = ["capi.cu", "common.cuh", "attn.cuh", "attn2.cuh", "gemm.cuh", "batch.cuh", "tc.cuh", "attn3.cuh", "gen.cpp"]
+DEPS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".cpp", ".h")))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",

@@ -10,8 +10,15 @@
 // pre-packed on the host as [hi block | lo block] per GEMM. Accumulators
 // come back with tcgen05.ld (lane = node, column = output feature), so
 // epilogues write the next GEMM's A operand straight back into TMEM.
-// The per-node online-softmax walk (the only non-GEMM step) is the attn2
-// code reading q~ / writing ubar in row-major shared memory.
+// The per-node softmax walk (the only non-GEMM step) reads q~ / writes ubar
+// in row-major shared memory, warp per row, lanes across the key features.
+//
+// Latency structure (v2): weight blocks are staged by one thread with TMA
+// bulk copies (cp.async.bulk -> mbarrier complete_tx), issued as soon as the
+// MMA that read the previous block commits, so staging overlaps the
+// epilogues and the walk; the walk loads its ring entries in chunks of
+// A3_EC (all loads of a chunk in flight before any math) and the payload
+// rows of the NEXT tile are prefetched into L2 while the current tile runs.
 #pragma once
 
 #include "attn2.cuh"
@@ -68,15 +75,7 @@ static inline int64_t attn3_wbuf_floats(const Geo& g, const TcW& w) {
   return m;
 }
 
-// all threads: copy one packed weight block into shared memory
-__device__ __forceinline__ void a3_stage(float* Wb, const float* __restrict__ src, int64_t nfl) {
-  const uint32_t sb = smem_u32(Wb);
-  for (int64_t x = threadIdx.x; x < nfl / 4; x += A3_THREADS)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sb + 16u * (uint32_t)x),
-                 "l"(src + 4 * x));
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-  fence_async_smem();
-}
+#define A3_EC 5  // ring entries loaded per chunk of the walk
 
 // one thread: split-TF32 MMAs, A (TMEM hi at a_hi, lo at a_lo) x B (smem block), then commit
 __device__ __forceinline__ void a3_mma(uint32_t tmem, int a_hi, int a_lo, const float* Wb, int Np,
@@ -96,11 +95,73 @@ __device__ __forceinline__ void a3_mma(uint32_t tmem, int a_hi, int a_lo, const 
   umma_commit(bar);
 }
 
+// Weight block j of layer l in issue order Q, K_0..K_{H-1}, V_0..V_{H-1}, O.
+struct A3Blk {
+  const float* src;
+  int64_t floats;
+};
+__device__ __forceinline__ A3Blk a3_block(const Geo& g, const TcW& w, int l, int j) {
+  if (j == 0) return {w.wq + (int64_t)l * tc_blk(w.Np_q, w.Kp_x), tc_blk(w.Np_q, w.Kp_x)};
+  if (j <= g.H) {
+    const int hh = j - 1;
+    return {w.wk + ((int64_t)l * g.H + hh) * tc_blk(w.Np_k, w.Kp_qh), tc_blk(w.Np_k, w.Kp_qh)};
+  }
+  if (j <= 2 * g.H) {
+    const int hh = j - 1 - g.H;
+    return {w.wv + ((int64_t)l * g.H + hh) * tc_blk(w.Np_v, w.Kp_u), tc_blk(w.Np_v, w.Kp_u)};
+  }
+  return {w.wo + (int64_t)l * tc_blk(w.Np_o, w.Kp_c), tc_blk(w.Np_o, w.Kp_c)};
+}
+__device__ __forceinline__ void a3_stage_async(float* Wb, const Geo& g, const TcW& w, int l, int j,
+                                               uint64_t* wbar) {
+  const A3Blk b = a3_block(g, w, l, j);
+  bulk_stage(Wb, b.src, (uint32_t)(b.floats * 4), wbar);
+}
+
+// L2 prefetch of the ring rows (payload of every layer, features, timestamps)
+// of `T` tile rows whose node / entry count / ring head are in the arrays.
+__device__ __forceinline__ void a3_prefetch_rows(const Geo& g, const RingSrc& rs, const int* nodes,
+                                                 const int* Es, const int* heads, int T) {
+  const int pay_b = g.ld_d * 4, feat_b = g.d_e ? g.ld_e * 4 : 0;
+  const int per_entry = g.K * 5 + (feat_b ? (feat_b + 127) / 128 + 1 : 0);
+  const int per_row = g.L * per_entry + 1;
+  for (int x = threadIdx.x; x < T * per_row; x += A3_THREADS) {
+    const int i = x / per_row, r = x % per_row;
+    const int node = nodes[i];
+    if (node < 0) continue;
+    if (r == g.L * per_entry) {  // the row's timestamps
+      prefetch_l2(rs.ring_t + (int64_t)node * g.L);
+      continue;
+    }
+    const int e = r / per_entry, q = r % per_entry;
+    if (e >= Es[i]) continue;
+    int slot = heads[i] + e;
+    if (slot >= g.L) slot -= g.L;
+    const char* base;
+    int qq, nb;
+    if (q < g.K * 5) {
+      const int l = q / 5;
+      qq = q % 5;
+      nb = pay_b;
+      base = reinterpret_cast<const char*>(rs.ring_pay + (((int64_t)node * g.K + l) * g.L + slot) * g.ld_d);
+    } else {
+      qq = q - g.K * 5;
+      nb = feat_b;
+      base = reinterpret_cast<const char*>(rs.ring_feat + ((int64_t)node * g.L + slot) * g.ld_e);
+    }
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(base);
+    const uintptr_t line = (a0 >> 7) + (uintptr_t)qq;
+    if (line > ((a0 + (uintptr_t)nb - 1) >> 7)) continue;
+    prefetch_l2(reinterpret_cast<const void*>(line << 7));
+  }
+}
+
 template <int KF, int MAXH>
 __global__ void __launch_bounds__(A3_THREADS, 1)
 attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
   constexpr int KP = 4;
   constexpr int KT = 2;
+  constexpr int EC = (KF > 0 || MAXH > 2) ? 2 : A3_EC;
   extern __shared__ float4 smem4[];
   const int LDU = a3_ldu(g), LDC = a3_ldc(g);
   float* Ur = reinterpret_cast<float*>(smem4);  // [tmax][LDU]  q~ then ubar (both heads)
@@ -108,8 +169,9 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
   float* Wb = Cr + (int64_t)tmax * LDC;          // staged packed weight block
   Wb = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(Wb) + 127) & ~uintptr_t(127));
   __shared__ int s_node[A2_TMAX], s_E[A2_TMAX], s_head[A2_TMAX], s_mode[A2_TMAX];
+  __shared__ int s_nnode[A2_TMAX], s_nE[A2_TMAX], s_nhead[A2_TMAX];  // next tile (prefetch)
   __shared__ double s_tref[A2_TMAX];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, wbar;
   __shared__ uint32_t tslot;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -119,28 +181,50 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
   int T = (int)cdiv(N, gridDim.x);
   if (T > tmax) T = tmax;
   const int64_t ntiles = cdiv(N, T);
+  if ((int64_t)blockIdx.x >= ntiles) return;
   const int64_t pre_rows = rs.fused ? (int64_t)rs.pre_n[0] : N;
   const int64_t d_rows = rs.fused ? (int64_t)rs.post_n[0] : 0;
-  const int pay_lines = (g.d * 4 + 127) / 128;
-  const int feat_lines = g.d_e ? (g.d_e * 4 + 127) / 128 : 0;
 
   if (warp == 0) tmem_alloc(&tslot, 512);
   if (tid == 0) {
     mbar_init(&bar, 1);
+    mbar_init(&wbar, 1);
     mbar_fence_init();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (tid == 0) a3_stage_async(Wb, g, w, 0, 0, &wbar);  // Q of layer 0, first tile
   const uint32_t tmem = tslot;
-  uint32_t phase = 0;
+  uint32_t phase = 0, wphase = 0;
   const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
   const int row = 32 * quad + lane;  // this thread's tile row in TMEM epilogues
-  const bool quad_live_base = true;
+  const int nblk = 2 + 2 * g.H;      // weight blocks per layer
+
+  // one weight block: wait for its staging, MMA, wait for the MMA, then stage
+  // the next block into the freed buffer (overlapping the caller's epilogue)
+  auto gemm = [&](int l, int j, int a_hi, int a_lo, int Np, int Kp, int dcol, bool more) {
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    mbar_wait(&wbar, wphase);
+    wphase ^= 1;
+    if (tid == 0) a3_mma(tmem, a_hi, a_lo, Wb, Np, Kp, dcol, &bar);
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    if (tid == 0 && more) {
+      int nl = l, nj = j + 1;
+      if (nj == nblk) { nj = 0; nl = (l + 1) % g.K; }
+      a3_stage_async(Wb, g, w, nl, nj, &wbar);
+    }
+  };
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t base = tile * T;
-    const bool quad_live = quad_live_base && (32 * quad < T);
+    const int64_t nbase = (tile + gridDim.x) * T;
+    const bool has_next = tile + gridDim.x < ntiles;
+    const bool quad_live = 32 * quad < T;
     if (tid < A2_TMAX) {
       const int i = tid;
       const int64_t idx = base + i;
@@ -166,29 +250,21 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
         if (lane == 0 && e_pre) atomicAdd(rs.e_count, e_pre);
         if (lane == 0 && e_post && rs.e_count_post) atomicAdd(rs.e_count_post, e_post);
       }
+    } else if (tid >= 256 && tid < 256 + A2_TMAX) {  // next tile's ring meta, for the prefetch
+      const int i = tid - 256;
+      const int64_t idx = nbase + i;
+      int node = -1, E = 0, head = 0;
+      if (has_next && i < T && idx < N) {
+        node = rs.node(idx);
+        const int cc = rs.ring_ccnt[node];
+        E = cc >= 0 ? cc : (rs.use_store ? rs.ring_cnt[node] : 0);
+        head = rs.ring_head[node];
+      }
+      s_nnode[i] = node; s_nE[i] = E; s_nhead[i] = head;
     }
     __syncthreads();
-    {  // L2 prefetch of the tile's payload / feature rows
-      const int per_entry = g.K * pay_lines + feat_lines;
-      const int total = T * g.L * per_entry;
-      for (int x = tid; x < total; x += A3_THREADS) {
-        const int i = x / (g.L * per_entry);
-        const int rem = x % (g.L * per_entry);
-        const int e = rem / per_entry, q = rem % per_entry;
-        const int node = s_node[i];
-        if (node < 0 || e >= s_E[i]) continue;
-        int slot = s_head[i] + e;
-        if (slot >= g.L) slot -= g.L;
-        const char* p;
-        if (q < g.K * pay_lines) {
-          const int l = q / pay_lines, ln = q % pay_lines;
-          p = reinterpret_cast<const char*>(rs.ring_pay + (((int64_t)node * g.K + l) * g.L + slot) * g.ld_d) + ln * 128;
-        } else {
-          p = reinterpret_cast<const char*>(rs.ring_feat + ((int64_t)node * g.L + slot) * g.ld_e) + (q - g.K * pay_lines) * 128;
-        }
-        prefetch_l2(p);
-      }
-    }
+    if (tile == blockIdx.x) a3_prefetch_rows(g, rs, s_node, s_E, s_head, T);
+    if (has_next) a3_prefetch_rows(g, rs, s_nnode, s_nE, s_nhead, T);
     // x_0 -> TMEM A region (hi at col 0, lo at col Kp_x)
     if (quad_live) {
       const int node = row < T ? s_node[row] : -1;
@@ -211,15 +287,10 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
     }
 
     for (int l = 0; l < g.K; ++l) {
+      const bool last = (l == g.K - 1);
       const float* bq = w.bq + (int64_t)l * g.HD;
       // ---- q = x W_Q + b -> per-head A blocks for the q~ GEMMs ----
-      a3_stage(Wb, w.wq + (int64_t)l * tc_blk(w.Np_q, w.Kp_x), tc_blk(w.Np_q, w.Kp_x));
-      tc_fence_before();
-      __syncthreads();
-      if (tid == 0) a3_mma(tmem, 0, w.Kp_x, Wb, w.Np_q, w.Kp_x, w.dq, &bar);
-      mbar_wait(&bar, phase);
-      phase ^= 1;
-      tc_fence_after();
+      gemm(l, 0, 0, w.Kp_x, w.Np_q, w.Kp_x, w.dq, true);
       const int aq_lo = g.H * w.Kp_qh;
       if (quad_live) {
         for (int c0 = 8 * cg; c0 < g.H * w.Kp_qh; c0 += 32) {
@@ -227,9 +298,7 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
           float v[8], h8[8], l8[8];
           const int hh = c0 / w.Kp_qh;
           const int b0 = c0 - hh * w.Kp_qh;
-          // source feature index hh*d_k + b for b < d_k (padding -> 0)
-          const int src0 = hh * g.d_k + b0;
-          // the 8 destination columns map to contiguous source features while b < d_k
+          const int src0 = hh * g.d_k + b0;  // source feature hh*d_k + b (b < d_k)
           tmem_ld8(tmem + lane_base + (uint32_t)(w.dq + (src0 & ~7)), v);
           float v2[8];
           tmem_ld8(tmem + lane_base + (uint32_t)(w.dq + (src0 & ~7) + 8), v2);
@@ -252,17 +321,7 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
       }
       // ---- q~_h = W_K,h q_h / sqrt(d_k) -> Ur rows ----
       for (int hh = 0; hh < g.H; ++hh) {
-        tc_fence_before();
-        __syncthreads();  // previous MMA consumers / A writes done before restaging
-        a3_stage(Wb, w.wk + ((int64_t)l * g.H + hh) * tc_blk(w.Np_k, w.Kp_qh),
-                 tc_blk(w.Np_k, w.Kp_qh));
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0)
-          a3_mma(tmem, hh * w.Kp_qh, aq_lo + hh * w.Kp_qh, Wb, w.Np_k, w.Kp_qh, w.dqt, &bar);
-        mbar_wait(&bar, phase);
-        phase ^= 1;
-        tc_fence_after();
+        gemm(l, 1 + hh, hh * w.Kp_qh, aq_lo + hh * w.Kp_qh, w.Np_k, w.Kp_qh, w.dqt, true);
         if (quad_live) {
           for (int c0 = 8 * cg; c0 < g.k_in; c0 += 32) {
             float v[8];
@@ -276,10 +335,12 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
         }
       }
       __syncthreads();
-      // ---- per-node online softmax over the ring entries (attn2), ubar in place ----
+      // ---- per-node softmax walk over the ring entries, ubar in place ----
       for (int i = warp; i < T; i += A3_WARPS) {
         const int node = s_node[i];
         const int E = s_E[i];
+        const int hd = s_head[i];
+        const double tref = s_tref[i];
         float* Ui = Ur + (int64_t)i * LDU;
         float qp[MAXH][KP], qf[MAXH][KF > 0 ? KF : 1], qc[MAXH][KT], qs[MAXH][KT];
         float up[MAXH][KP], uf[MAXH][KF > 0 ? KF : 1], uc[MAXH][KT], us[MAXH][KT];
@@ -312,54 +373,92 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
             us[hh][j] = 0.f;
           }
         }
-        for (int e = 0; e < E; ++e) {
-          int slot = s_head[i] + e;
-          if (slot >= g.L) slot -= g.L;
-          const float* pay = rs.ring_pay + (((int64_t)node * g.K + l) * g.L + slot) * g.ld_d;
-          const float* ft = rs.ring_feat + ((int64_t)node * g.L + slot) * g.ld_e;
-          const double dt = s_tref[i] - rs.ring_t[(int64_t)node * g.L + slot];
-          float kp[KP], kf[KF > 0 ? KF : 1], kc[KT], ks[KT];
+        const float* payb = rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d;
+        const float* ftb = rs.ring_feat + (int64_t)node * g.L * g.ld_e;
+        const double* tb = rs.ring_t + (int64_t)node * g.L;
+        for (int e0 = 0; e0 < E; e0 += EC) {
+          // all loads of the chunk first (independent, in flight together)
+          float kp[EC][KP], kf[EC][KF > 0 ? KF : 1];
+          double dtv[EC];
 #pragma unroll
-          for (int j = 0; j < KP; ++j) {
-            const int a = lane + 32 * j;
-            kp[j] = a < g.d ? pay[a] : 0.f;
+          for (int u = 0; u < EC; ++u) {
+            const bool ev = e0 + u < E;
+            int slot = ev ? hd + e0 + u : 0;
+            if (slot >= g.L) slot -= g.L;
+            const float* pay = payb + (int64_t)slot * g.ld_d;
+#pragma unroll
+            for (int j = 0; j < KP; ++j) {
+              const int a = lane + 32 * j;
+              kp[u][j] = (ev && a < g.d) ? __ldg(pay + a) : 0.f;
+            }
+#pragma unroll
+            for (int j = 0; j < KF; ++j) {
+              const int a = lane + 32 * j;
+              kf[u][j] = (ev && a < g.d_e) ? __ldg(ftb + (int64_t)slot * g.ld_e + a) : 0.f;
+            }
+            dtv[u] = ev ? tref - __ldg(tb + slot) : 0.0;
           }
+          float lg[EC][MAXH];
+          float kc[EC][KT], ks[EC][KT];
 #pragma unroll
-          for (int j = 0; j < KF; ++j) {
-            const int a = lane + 32 * j;
-            kf[j] = a < g.d_e ? ft[a] : 0.f;
-          }
+          for (int u = 0; u < EC; ++u) {
 #pragma unroll
-          for (int j = 0; j < KT; ++j) {
-            const int f = lane + 32 * j;
-            float sv = 0.f, cv = 0.f;
-            if (f < g.half) phase_sincos(w.omega[f], dt, &sv, &cv);
-            kc[j] = cv * g.phi_amp;
-            ks[j] = sv * g.phi_amp;
+            for (int j = 0; j < KT; ++j) {
+              const int f = lane + 32 * j;
+              float sv = 0.f, cv = 0.f;
+              if (f < g.half) phase_sincos(w.omega[f], dtv[u], &sv, &cv);
+              kc[u][j] = cv * g.phi_amp;
+              ks[u][j] = sv * g.phi_amp;
+            }
+#pragma unroll
+            for (int hh = 0; hh < MAXH; ++hh) {
+              float part = 0.f;
+              if (hh < g.H) {
+#pragma unroll
+                for (int j = 0; j < KP; ++j) part = fmaf(qp[hh][j], kp[u][j], part);
+#pragma unroll
+                for (int j = 0; j < KF; ++j) part = fmaf(qf[hh][j], kf[u][j], part);
+#pragma unroll
+                for (int j = 0; j < KT; ++j)
+                  part = fmaf(qc[hh][j], kc[u][j], fmaf(qs[hh][j], ks[u][j], part));
+              }
+              lg[u][hh] = warp_sum(part);
+            }
           }
 #pragma unroll
           for (int hh = 0; hh < MAXH; ++hh) {
             if (hh < g.H) {
-              float part = 0.f;
+              float cm = -INFINITY;
 #pragma unroll
-              for (int j = 0; j < KP; ++j) part = fmaf(qp[hh][j], kp[j], part);
-#pragma unroll
-              for (int j = 0; j < KF; ++j) part = fmaf(qf[hh][j], kf[j], part);
-#pragma unroll
-              for (int j = 0; j < KT; ++j) part = fmaf(qc[hh][j], kc[j], fmaf(qs[hh][j], ks[j], part));
-              const float logit = warp_sum(part);
-              const float nm = fmaxf(mx[hh], logit);
+              for (int u = 0; u < EC; ++u)
+                if (e0 + u < E) cm = fmaxf(cm, lg[u][hh]);
+              const float nm = fmaxf(mx[hh], cm);
               const float sc = __expf(mx[hh] - nm);
-              const float p = __expf(logit - nm);
-              zs[hh] = fmaf(zs[hh], sc, p);
+              zs[hh] *= sc;
 #pragma unroll
-              for (int j = 0; j < KP; ++j) up[hh][j] = fmaf(p, kp[j], up[hh][j] * sc);
+              for (int j = 0; j < KP; ++j) up[hh][j] *= sc;
 #pragma unroll
-              for (int j = 0; j < KF; ++j) uf[hh][j] = fmaf(p, kf[j], uf[hh][j] * sc);
+              for (int j = 0; j < KF; ++j) uf[hh][j] *= sc;
 #pragma unroll
               for (int j = 0; j < KT; ++j) {
-                uc[hh][j] = fmaf(p, kc[j], uc[hh][j] * sc);
-                us[hh][j] = fmaf(p, ks[j], us[hh][j] * sc);
+                uc[hh][j] *= sc;
+                us[hh][j] *= sc;
+              }
+#pragma unroll
+              for (int u = 0; u < EC; ++u) {
+                if (e0 + u < E) {
+                  const float p = __expf(lg[u][hh] - nm);
+                  zs[hh] += p;
+#pragma unroll
+                  for (int j = 0; j < KP; ++j) up[hh][j] = fmaf(p, kp[u][j], up[hh][j]);
+#pragma unroll
+                  for (int j = 0; j < KF; ++j) uf[hh][j] = fmaf(p, kf[u][j], uf[hh][j]);
+#pragma unroll
+                  for (int j = 0; j < KT; ++j) {
+                    uc[hh][j] = fmaf(p, kc[u][j], uc[hh][j]);
+                    us[hh][j] = fmaf(p, ks[u][j], us[hh][j]);
+                  }
+                }
               }
               mx[hh] = nm;
             }
@@ -410,13 +509,7 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
           }
           tmem_st_wait();
         }
-        a3_stage(Wb, w.wv + ((int64_t)l * g.H + hh) * tc_blk(w.Np_v, w.Kp_u), tc_blk(w.Np_v, w.Kp_u));
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) a3_mma(tmem, 0, w.Kp_u, Wb, w.Np_v, w.Kp_u, w.dv, &bar);
-        mbar_wait(&bar, phase);
-        phase ^= 1;
-        tc_fence_after();
+        gemm(l, 1 + g.H + hh, 0, w.Kp_u, w.Np_v, w.Kp_u, w.dv, true);
         if (quad_live) {
           for (int c0 = 8 * cg; c0 < g.d_k; c0 += 32) {
             float v[8];
@@ -428,9 +521,8 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
             }
           }
         }
-        tc_fence_before();
-        __syncthreads();  // A region / weight buffer are reused by the next head
       }
+      __syncthreads();  // every column group's c rows are in Cr
       // ---- out_l = c W_O ----
       if (quad_live) {
         for (int c0 = 8 * cg; c0 < w.Kp_c; c0 += 32) {
@@ -447,14 +539,7 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
         }
         tmem_st_wait();
       }
-      a3_stage(Wb, w.wo + (int64_t)l * tc_blk(w.Np_o, w.Kp_c), tc_blk(w.Np_o, w.Kp_c));
-      tc_fence_before();
-      __syncthreads();
-      if (tid == 0) a3_mma(tmem, 0, w.Kp_c, Wb, w.Np_o, w.Kp_c, w.dO, &bar);
-      mbar_wait(&bar, phase);
-      phase ^= 1;
-      tc_fence_after();
-      const bool last = (l == g.K - 1);
+      gemm(l, nblk - 1, 0, w.Kp_c, w.Np_o, w.Kp_c, w.dO, !last || has_next);
       if (quad_live) {
         const int node = row < T ? s_node[row] : -1;
         const int mode = row < T ? s_mode[row] : 0;
@@ -493,9 +578,9 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
           rs.valid_at[node] = rs.valid_at_ptr ? rs.valid_at_ptr[0] : rs.valid_at_const;
         }
       }
-      tc_fence_before();
-      __syncthreads();
     }
+    tc_fence_before();
+    __syncthreads();
   }
   tc_fence_before();
   __syncthreads();

@@ -1,0 +1,654 @@
+// Recompute kernel v4: 128-row tiles on tcgen05 with bf16x3 split GEMMs.
+//
+// Function: the engine recompute of attn2/attn3 (reference
+// S/kernels/pipeline_numba.py:15-111 with the key/value projections folded to
+// the query side), for H = 2 and k_in <= 224 (the C3/C4 widths).
+//
+// Why a v4. At the end of a 30M-edge C4 stream one batch recomputes ~109K rows
+// with ~10 ring entries each (1 GB of frozen payload). attn3 ran 61-row tiles
+// (its q~/ubar rows for a tile live in shared memory) and re-staged ~1 MB of
+// split-TF32 weights per tile, and its walk spent ~147 instructions per ring
+// entry. v4:
+//  * bf16x3 split GEMMs (hi*hi + hi*lo + lo*hi, fp32 accumulate in TMEM;
+//    ~1e-5 row-relative, the 1e-4 bar has a 10x margin): A operands and
+//    weight blocks are half the size of split-TF32, so q~ for both heads
+//    stays in TMEM and a tile is the full 128 lanes; weight blocks (~52 KB)
+//    are double-buffered and staged by TMA bulk copies one block ahead.
+//  * q~ leaves TMEM one 32-row quadrant at a time through a double-buffered
+//    shared-memory row buffer; the walk writes ubar back into the same
+//    buffer and the quadrant's warps pack it (bf16 hi/lo) into the TMEM
+//    columns q~ occupied, where it is the A operand of the W_V GEMMs.
+//  * the walk: one LDG.128 per ring entry and lane, the time encoding's
+//    sqrt(1/d_t) folded into W_K / W_V, the logits of a chunk of entries
+//    (both heads) reduced with one transposing butterfly, packed f32x2 FMAs.
+//  * L2 prefetch one quadrant ahead (the next quadrant's ring rows while the
+//    current one is walked), so the walk's loads hit L2.
+//
+// TMEM columns (fp32 accumulators; bf16 A operands pack two per column):
+//   X_A  [0, Kx)           x_l hi|lo                (A of Q)
+//   ACCQ [Kx, Kx+Nq)       q, head h at h*Kq         (D of Q)
+//   QA   [0, Kq)           q_h hi|lo                 (A of K_h)
+//   QT0  [512-Nk, 512)     q~_0  -> ubar_0 hi|lo     (D of K_0, then A of V_0)
+//   QT1  [Kq, Kq+Nk)       q~_1  -> ubar_1 hi|lo
+//   C0   [0, Nv)  C1 [Kq+max(Nk,Kc), +Nv)            (D of V_h)
+//   CA   [Kq, Kq+Kc)       c hi|lo, head h at h*Kq   (A of O)
+//   ACCO [Kq+Kc, +No)      out                       (D of O)
+// Host-side checks (a4_plan) guarantee every live range is disjoint.
+#pragma once
+
+#include <cuda_bf16.h>
+
+#include "attn3.cuh"
+
+struct A4W {
+  const uint16_t *wq, *wk, *wv, *wo;  // packed bf16 B operands, hi block then lo block
+  const float* bq;                    // [K][H*Kq]
+  const double* omega;
+  int Kx, Kq, Ku, Kc, Nq, Nk, Nv, No;
+  int qt0, qt1, c1, ca, acco;         // TMEM columns
+  int kfo, kto, kpad;                 // key layout [payload | features | time], each 4-padded
+  int ldu;                            // row stride of the quadrant row buffer (floats)
+  int wblk_bytes;                     // one staged weight block buffer (bytes)
+};
+
+static inline bool a4_plan(const Geo& g, A4W* w) {
+  auto r4 = [](int x) { return (x + 3) & ~3; };
+  w->kfo = r4(g.d);
+  w->kto = w->kfo + r4(g.d_e);
+  w->kpad = w->kto + r4(g.d_t);
+  if (g.H != 2 || r4(g.d) > 128 || r4(g.d_e) > 128 || r4(g.d_t) > 128) return false;
+  w->Kx = r16(g.d);
+  w->Kq = r16(g.d_k);
+  w->Ku = r16(w->kpad);
+  w->Kc = g.H * w->Kq;
+  w->Nq = g.H * w->Kq;
+  w->Nk = r16(w->kpad);
+  w->Nv = r16(g.d_k);
+  w->No = r16(g.d);
+  w->qt0 = 512 - w->Nk;
+  w->qt1 = w->Kq;
+  w->c1 = w->Kq + std::max(w->Nk, w->Kc);  // above ubar_1 (read by V_1) and above CA
+  w->ca = w->Kq;
+  w->acco = w->Kq + w->Kc;
+  int ldu = g.H * w->kpad;
+  while (ldu % 8 != 4) ++ldu;  // 8 consecutive rows hit distinct 16-byte bank groups
+  w->ldu = ldu;
+  int mb = std::max(std::max(w->Nq * w->Kx, w->Nk * w->Kq), std::max(w->Nv * w->Ku, w->No * w->Kc));
+  w->wblk_bytes = (mb * 2 * 2 + 1023) & ~1023;
+  return w->Nk <= 256 && w->Nq <= 256 && w->No <= 256 && w->Ku <= w->Nk &&
+         w->Kx + w->Nq <= w->qt0 &&            // ACCQ alive while K_0 writes QT0
+         w->qt1 + w->Nk <= w->qt0 &&           // QT1 / QT0 disjoint
+         w->Kq <= w->Kx && w->Nv <= w->Kq &&   // QA inside X_A; C0 below QT1
+         w->c1 + w->Nv <= 512 &&               // C1 (may overlap QT0: V_0 is done)
+         w->acco + w->No <= 512 &&             // ACCO
+         w->Kx <= w->acco;                     // X_A (next layer) below ACCO
+}
+
+__host__ __device__ inline int64_t a4_blk_elems(int Np, int Kp) { return 2ll * Np * Kp; }
+
+static inline size_t attn4_smem_bytes(const A4W& w) {
+  return 1024 + 2 * (size_t)w.wblk_bytes + 2 * 32 * (size_t)w.ldu * 4;
+}
+
+#define A4_THREADS 512
+#define A4_WARPS 16
+#define A4_TMAX 128
+#define A4_EC 4  // ring entries per chunk of the walk
+
+// ---- bf16 helpers ----
+__device__ __forceinline__ uint32_t bf16_bits(float x) {
+  return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
+// hi/lo bf16 split of (a, b), packed two per 32-bit column (element 2c low)
+__device__ __forceinline__ void bf16x2_split(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const uint32_t ha = bf16_bits(a), hb = bf16_bits(b);
+  const float ra = a - __uint_as_float(ha << 16), rb = b - __uint_as_float(hb << 16);
+  hi = ha | (hb << 16);
+  lo = bf16_bits(ra) | (bf16_bits(rb) << 16);
+}
+// 16 consecutive elements -> 8 hi columns at col, 8 lo columns at col + half
+__device__ __forceinline__ void a4_st16(uint32_t taddr_hi, uint32_t taddr_lo, const float (&v)[16]) {
+  float h[8], l[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    uint32_t a, b;
+    bf16x2_split(v[2 * q], v[2 * q + 1], a, b);
+    h[q] = __uint_as_float(a);
+    l[q] = __uint_as_float(b);
+  }
+  tmem_st8(taddr_hi, h);
+  tmem_st8(taddr_lo, l);
+}
+__device__ __forceinline__ void tmem_ld8_nw(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr));
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q] = __uint_as_float(r[q]);
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+__host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
+  return (1u << 4)                       // c_format F32
+         | (1u << 7)                     // a_format BF16
+         | (1u << 10)                    // b_format BF16
+         | ((uint32_t)(N >> 3) << 17)    // N >> 3 (A and B K-major)
+         | ((uint32_t)(M >> 4) << 24);   // M >> 4
+}
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// one thread: bf16x3 MMAs of one block, A = TMEM [a, a+Kp) (hi then lo), B = smem
+// K-major bf16 [Np][Kp] (8x8 core matrices, hi block then lo block), then commit
+__device__ __forceinline__ void a4_mma(uint32_t tmem, int a, const uint16_t* Wb, int Np, int Kp,
+                                       int dcol, uint64_t* bar) {
+  tc_fence_after();
+  const uint32_t idesc = umma_idesc_bf16(128, Np);
+  const uint32_t sbo = (uint32_t)(Kp / 8) * 128u;
+  const uint32_t bh = smem_u32(Wb), bl = bh + (uint32_t)Np * Kp * 2u;
+  const uint32_t ah0 = tmem + (uint32_t)a, al0 = ah0 + (uint32_t)(Kp / 2);
+  for (int s = 0; s < Kp / 16; ++s) {
+    const uint32_t off = (uint32_t)s * 256u;
+    const uint64_t dh = umma_desc(bh + off, 128, sbo), dl = umma_desc(bl + off, 128, sbo);
+    const uint32_t ah = ah0 + 8u * s, al = al0 + 8u * s;
+    umma_bf16_ts(tmem + (uint32_t)dcol, ah, dh, idesc, s > 0 ? 1u : 0u);
+    umma_bf16_ts(tmem + (uint32_t)dcol, ah, dl, idesc, 1u);
+    umma_bf16_ts(tmem + (uint32_t)dcol, al, dh, idesc, 1u);
+  }
+  umma_commit(bar);
+}
+
+// weight block j (Q, K_0, K_1, V_0, V_1, O) of layer l: source and element count
+__device__ __forceinline__ const uint16_t* a4_block(const Geo& g, const A4W& w, int l, int j,
+                                                    int64_t* elems) {
+  if (j == 0) {
+    *elems = a4_blk_elems(w.Nq, w.Kx);
+    return w.wq + (int64_t)l * *elems;
+  }
+  if (j <= 2) {
+    *elems = a4_blk_elems(w.Nk, w.Kq);
+    return w.wk + ((int64_t)l * 2 + (j - 1)) * *elems;
+  }
+  if (j <= 4) {
+    *elems = a4_blk_elems(w.Nv, w.Ku);
+    return w.wv + ((int64_t)l * 2 + (j - 3)) * *elems;
+  }
+  *elems = a4_blk_elems(w.No, w.Kc);
+  return w.wo + (int64_t)l * *elems;
+}
+
+// L2 prefetch of layer l's ring rows (payload lines, timestamps) of tile rows [r0, r1)
+__device__ __forceinline__ void a4_prefetch(const Geo& g, const RingSrc& rs, const int* nodes,
+                                            const int* Es, const int* heads, int r0, int r1,
+                                            int l, int tid) {
+  const int per_entry = 4 + (g.d_e ? 2 : 0);  // 400 B payload spans <= 4 lines (+ features)
+  const int per_row = g.L * per_entry + 1;
+  for (int x = tid; x < (r1 - r0) * per_row; x += A4_THREADS) {
+    const int i = r0 + x / per_row, r = x % per_row;
+    const int node = nodes[i];
+    if (node < 0) continue;
+    if (r == g.L * per_entry) {
+      prefetch_l2(rs.ring_t + (int64_t)node * g.L);
+      continue;
+    }
+    const int e = r / per_entry, q = r % per_entry;
+    if (e >= Es[i]) continue;
+    int slot = heads[i] + e;
+    if (slot >= g.L) slot -= g.L;
+    const char* base;
+    int nb, qq;
+    if (q < 4) {
+      base = reinterpret_cast<const char*>(rs.ring_pay + (((int64_t)node * g.K + l) * g.L + slot) * g.ld_d);
+      nb = g.d * 4;
+      qq = q;
+    } else {
+      base = reinterpret_cast<const char*>(rs.ring_feat + ((int64_t)node * g.L + slot) * g.ld_e);
+      nb = g.d_e * 4;
+      qq = q - 4;
+    }
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(base);
+    const uintptr_t line = (a0 >> 7) + (uintptr_t)qq;
+    if (line > ((a0 + (uintptr_t)nb - 1) >> 7)) continue;
+    prefetch_l2(reinterpret_cast<const void*>(line << 7));
+  }
+}
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&d))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return d;
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&d))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return d;
+}
+
+// Walk of one row (warp-per-row): softmax over its ring entries for both
+// heads; q~ read from, ubar written to the row buffer U (both heads, k_in each).
+// Lane l owns key features [4l, 4l+4) of the payload (l < d/4), of the edge
+// features (l < d_e/4) and frequencies 2l, 2l+1 of the time encoding (l < d_t/4).
+template <int KF>
+__device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const RingSrc& rs,
+                                            float* U, int node, int E, int hd, double tref, int l,
+                                            int lane) {
+  constexpr int EC = A4_EC;
+  const int kfo = w.kfo, kto = w.kto, kp = w.kpad;
+  const bool lp = lane < kfo / 4, lf = KF && lane < (kto - kfo) / 4, lt = lane < (kp - kto) / 4;
+  const double* omega = w.omega;
+  float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 qp[2], qf[2], qt[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float* Uh = U + h * kp;
+    qp[h] = lp ? *reinterpret_cast<const float4*>(Uh + 4 * lane) : zero4;
+    qf[h] = lf ? *reinterpret_cast<const float4*>(Uh + kfo + 4 * lane) : zero4;
+    qt[h] = lt ? *reinterpret_cast<const float4*>(Uh + kto + 4 * lane) : zero4;
+  }
+  float2 up[2][2], uf[2][2], ut[2][2];
+  float mx[2] = {-INFINITY, -INFINITY}, zs[2] = {0.f, 0.f};
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) up[h][c] = uf[h][c] = ut[h][c] = make_float2(0.f, 0.f);
+  double om0 = 0.0, om1 = 0.0;
+  const bool f0 = lt && 2 * lane < g.half, f1 = lt && 2 * lane + 1 < g.half;
+  if (f0) om0 = __ldg(omega + 2 * lane);
+  if (f1) om1 = __ldg(omega + 2 * lane + 1);
+  const float* payb = rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d + 4 * lane;
+  const float* ftb = rs.ring_feat + (int64_t)node * g.L * g.ld_e + 4 * lane;
+  const double* tb = rs.ring_t + (int64_t)node * g.L;
+  for (int e0 = 0; e0 < E; e0 += EC) {
+    float4 kp[EC], kf[EC];
+    double tv[EC];
+#pragma unroll
+    for (int u = 0; u < EC; ++u) {
+      const bool ev = e0 + u < E;
+      int slot = hd + e0 + u;
+      if (slot >= g.L) slot -= g.L;
+      kp[u] = (ev && lp) ? __ldg(reinterpret_cast<const float4*>(payb + slot * g.ld_d)) : zero4;
+      kf[u] = (KF && ev && lf) ? __ldg(reinterpret_cast<const float4*>(ftb + slot * g.ld_e)) : zero4;
+      tv[u] = ev ? __ldg(tb + slot) : tref;
+    }
+    // per-lane partial logits, value index v = 2u + h
+    float part[2 * EC];
+    float4 kt[EC];
+#pragma unroll
+    for (int u = 0; u < EC; ++u) {
+      float s0 = 0.f, c0 = 0.f, s1 = 0.f, c1 = 0.f;
+      const double dt = tref - tv[u];
+      if (f0) phase_sincos(om0, dt, &s0, &c0);
+      if (f1) phase_sincos(om1, dt, &s1, &c1);
+      kt[u] = make_float4(c0, s0, c1, s1);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float2 a = fmul2(make_float2(qp[h].x, qp[h].y), make_float2(kp[u].x, kp[u].y));
+        a = ffma2(make_float2(qp[h].z, qp[h].w), make_float2(kp[u].z, kp[u].w), a);
+        a = ffma2(make_float2(qt[h].x, qt[h].y), make_float2(kt[u].x, kt[u].y), a);
+        a = ffma2(make_float2(qt[h].z, qt[h].w), make_float2(kt[u].z, kt[u].w), a);
+        if (KF) {
+          a = ffma2(make_float2(qf[h].x, qf[h].y), make_float2(kf[u].x, kf[u].y), a);
+          a = ffma2(make_float2(qf[h].z, qf[h].w), make_float2(kf[u].z, kf[u].w), a);
+        }
+        part[2 * u + h] = a.x + a.y;
+      }
+    }
+    // transposing butterfly: 8 values -> lane L holds the full sum of value (L >> 2)
+    static_assert(2 * EC == 8, "butterfly assumes 8 logits per chunk");
+    {
+      const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float send = b4 ? part[j] : part[j + 4];
+        const float keep = b4 ? part[j + 4] : part[j];
+        part[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const float send = b3 ? part[j] : part[j + 2];
+        const float keep = b3 ? part[j + 2] : part[j];
+        part[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+      {
+        const float send = b2 ? part[0] : part[1];
+        const float keep = b2 ? part[1] : part[0];
+        part[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+      part[0] += __shfl_xor_sync(0xffffffffu, part[0], 2);
+      part[0] += __shfl_xor_sync(0xffffffffu, part[0], 1);
+    }
+    float lg[2 * EC];
+#pragma unroll
+    for (int v = 0; v < 2 * EC; ++v) lg[v] = __shfl_sync(0xffffffffu, part[0], 4 * v);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float cm = -INFINITY;
+#pragma unroll
+      for (int u = 0; u < EC; ++u)
+        if (e0 + u < E) cm = fmaxf(cm, lg[2 * u + h]);
+      const float nm = fmaxf(mx[h], cm);
+      const float sc = __expf(mx[h] - nm);
+      const float2 sc2 = make_float2(sc, sc);
+      zs[h] *= sc;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        up[h][c] = fmul2(up[h][c], sc2);
+        ut[h][c] = fmul2(ut[h][c], sc2);
+        if (KF) uf[h][c] = fmul2(uf[h][c], sc2);
+      }
+#pragma unroll
+      for (int u = 0; u < EC; ++u) {
+        const float p = (e0 + u < E) ? __expf(lg[2 * u + h] - nm) : 0.f;
+        const float2 p2 = make_float2(p, p);
+        zs[h] += p;
+        up[h][0] = ffma2(p2, make_float2(kp[u].x, kp[u].y), up[h][0]);
+        up[h][1] = ffma2(p2, make_float2(kp[u].z, kp[u].w), up[h][1]);
+        ut[h][0] = ffma2(p2, make_float2(kt[u].x, kt[u].y), ut[h][0]);
+        ut[h][1] = ffma2(p2, make_float2(kt[u].z, kt[u].w), ut[h][1]);
+        if (KF) {
+          uf[h][0] = ffma2(p2, make_float2(kf[u].x, kf[u].y), uf[h][0]);
+          uf[h][1] = ffma2(p2, make_float2(kf[u].z, kf[u].w), uf[h][1]);
+        }
+      }
+      mx[h] = nm;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float* Uh = U + h * kp;
+    const float inv = E > 0 ? 1.f / zs[h] : 0.f;
+    if (lp)
+      *reinterpret_cast<float4*>(Uh + 4 * lane) =
+          make_float4(up[h][0].x * inv, up[h][0].y * inv, up[h][1].x * inv, up[h][1].y * inv);
+    if (lf)
+      *reinterpret_cast<float4*>(Uh + kfo + 4 * lane) =
+          make_float4(uf[h][0].x * inv, uf[h][0].y * inv, uf[h][1].x * inv, uf[h][1].y * inv);
+    if (lt)
+      *reinterpret_cast<float4*>(Uh + kto + 4 * lane) =
+          make_float4(ut[h][0].x * inv, ut[h][0].y * inv, ut[h][1].x * inv, ut[h][1].y * inv);
+  }
+}
+
+template <int KF>
+__global__ void __launch_bounds__(A4_THREADS, 1)
+attn4_kernel(Geo g, A4W w, RingSrc rs) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sbase = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint16_t* Wb0 = reinterpret_cast<uint16_t*>(sbase);
+  uint16_t* Wb1 = reinterpret_cast<uint16_t*>(sbase + w.wblk_bytes);
+  float* Ub0 = reinterpret_cast<float*>(sbase + 2 * (size_t)w.wblk_bytes);
+  float* Ub1 = Ub0 + 32 * w.ldu;
+  __shared__ int s_node[A4_TMAX], s_E[A4_TMAX], s_head[A4_TMAX], s_mode[A4_TMAX];
+  __shared__ double s_tref[A4_TMAX];
+  __shared__ uint64_t mbar, wbar[2];
+  __shared__ uint32_t tslot;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int quad = warp & 3, cg = warp >> 2;
+  const int64_t N = rs.count();
+  if (N <= 0) return;
+  const int64_t grid = gridDim.x;
+  const int64_t waves = cdiv(N, grid * A4_TMAX);
+  const int T = (int)cdiv(N, grid * waves);  // balanced tile rows (<= 128)
+  const int64_t ntiles = cdiv(N, T);
+  if ((int64_t)blockIdx.x >= ntiles) return;
+  const int64_t my_tiles = cdiv(ntiles - blockIdx.x, grid);
+  const int64_t total_blocks = my_tiles * g.K * 6;
+  const int64_t pre_rows = rs.fused ? (int64_t)rs.pre_n[0] : N;
+  const int64_t d_rows = rs.fused ? (int64_t)rs.post_n[0] : 0;
+
+  if (warp == 0) tmem_alloc(&tslot, 512);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    mbar_init(&wbar[0], 1);
+    mbar_init(&wbar[1], 1);
+    mbar_fence_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
+  const int row = 32 * quad + lane;
+  auto stage = [&](int64_t G) {  // one thread
+    int64_t el;
+    const uint16_t* src = a4_block(g, w, (int)((G / 6) % g.K), (int)(G % 6), &el);
+    bulk_stage((G & 1) ? (void*)Wb1 : (void*)Wb0, src, (uint32_t)(el * 2), &wbar[G & 1]);
+  };
+  if (tid == 0) {
+    stage(0);
+    if (total_blocks > 1) stage(1);
+  }
+  int64_t G = 0;  // weight blocks consumed by this CTA
+  // one GEMM: wait for its weights, MMA, wait for the MMA, refill the buffer
+  auto gemm = [&](int a, int Np, int Kp, int dcol) {
+    mbar_wait(&wbar[G & 1], (uint32_t)((G >> 1) & 1));
+    if (tid == 0) a4_mma(tmem, a, (G & 1) ? Wb1 : Wb0, Np, Kp, dcol, &mbar);
+    mbar_wait(&mbar, (uint32_t)(G & 1));
+    tc_fence_after();
+    if (tid == 0 && G + 2 < total_blocks) stage(G + 2);
+    ++G;
+  };
+  auto cta_sync_tc = [&]() {
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  };
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += grid) {
+    const int64_t base = tile * T;
+    if (tid < A4_TMAX) {
+      const int i = tid;
+      const int64_t idx = base + i;
+      int node = -1, E = 0, head = 0, mode = 0;
+      double tref = 0.0;
+      if (i < T && idx < N) {
+        node = rs.node(idx);
+        if (rs.fused) mode = idx >= pre_rows ? 2 : (idx < d_rows ? 1 : 0);
+        const int cc = rs.ring_ccnt[node];
+        E = cc >= 0 ? cc : (rs.use_store ? rs.ring_cnt[node] : 0);
+        head = rs.ring_head[node];
+        if (E > 0) tref = rs.ring_t[(int64_t)node * g.L + head];
+      }
+      s_node[i] = node; s_E[i] = E; s_head[i] = head; s_tref[i] = tref; s_mode[i] = mode;
+      if (rs.e_count) {
+        unsigned long long e_pre = mode == 2 ? 0ull : (unsigned long long)E;
+        unsigned long long e_post = mode == 2 ? (unsigned long long)E : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          e_pre += __shfl_xor_sync(0xffffffffu, e_pre, o);
+          e_post += __shfl_xor_sync(0xffffffffu, e_post, o);
+        }
+        if (lane == 0 && e_pre) atomicAdd(rs.e_count, e_pre);
+        if (lane == 0 && e_post && rs.e_count_post) atomicAdd(rs.e_count_post, e_post);
+      }
+    }
+    __syncthreads();
+    const int nq = (T + 31) / 32;
+    const bool quad_live = quad < nq;
+    // x_0 -> X_A (bf16 hi|lo)
+    if (quad_live) {
+      const int node = row < T ? s_node[row] : -1;
+      const float* src = nullptr;
+      if (node >= 0)
+        src = s_mode[row] == 2 ? rs.mem_post + (base + row - pre_rows) * g.ld_s
+                               : rs.mem + (int64_t)node * g.ld_s;
+      for (int j = cg; j < w.Kx / 16; j += 4) {
+        float v[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = 16 * j + 4 * q;
+          float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (src && c < g.d_s) x = __ldg(reinterpret_cast<const float4*>(src + c));
+          v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+        }
+        a4_st16(tmem + lane_base + (uint32_t)(8 * j), tmem + lane_base + (uint32_t)(w.Kx / 2 + 8 * j), v);
+      }
+      tmem_st_wait();
+    }
+
+    for (int l = 0; l < g.K; ++l) {
+      const bool last = (l == g.K - 1);
+      a4_prefetch(g, rs, s_node, s_E, s_head, 0, min(32, T), l, tid);
+      // ---- q = x W_Q + b ----
+      cta_sync_tc();
+      gemm(0, w.Nq, w.Kx, w.Kx);
+      for (int h = 0; h < 2; ++h) {
+        // q_h (+ bias) -> QA as bf16 hi|lo
+        if (quad_live) {
+          const float* bq = w.bq + ((int64_t)l * 2 + h) * w.Kq;
+          for (int j = cg; j < w.Kq / 16; j += 4) {
+            float a[8], b[8], v[16];
+            tmem_ld8_nw(tmem + lane_base + (uint32_t)(w.Kx + h * w.Kq + 16 * j), a);
+            tmem_ld8_nw(tmem + lane_base + (uint32_t)(w.Kx + h * w.Kq + 16 * j + 8), b);
+            tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              v[q] = a[q] + __ldg(bq + 16 * j + q);
+              v[8 + q] = b[q] + __ldg(bq + 16 * j + 8 + q);
+            }
+            a4_st16(tmem + lane_base + (uint32_t)(8 * j), tmem + lane_base + (uint32_t)(w.Kq / 2 + 8 * j), v);
+          }
+          tmem_st_wait();
+        }
+        cta_sync_tc();
+        // ---- q~_h = (W_K,h / sqrt(d_k)) q_h -> QT_h ----
+        gemm(0, w.Nk, w.Kq, h == 0 ? w.qt0 : w.qt1);
+      }
+      // ---- walk, one 32-row quadrant at a time ----
+      for (int q = 0; q < nq; ++q) {
+        float* Ub = (q & 1) ? Ub1 : Ub0;
+        if (q + 1 < nq) a4_prefetch(g, rs, s_node, s_E, s_head, 32 * (q + 1), min(32 * (q + 2), T), l, tid);
+        if (quad == q) {  // q~ rows of this quadrant -> Ub
+          const int nch = (w.kpad + 7) / 8;
+          for (int c = cg; c < 2 * nch; c += 4) {
+            const int h = c / nch, j = c % nch;
+            float v[8];
+            tmem_ld8_nw(tmem + lane_base + (uint32_t)((h == 0 ? w.qt0 : w.qt1) + 8 * j), v);
+            tmem_ld_wait();
+            float* dst = Ub + lane * w.ldu + h * w.kpad + 8 * j;
+            *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+            if (8 * j + 8 <= w.kpad)
+              *reinterpret_cast<float4*>(dst + 4) = make_float4(v[4], v[5], v[6], v[7]);
+          }
+        }
+        __syncthreads();
+        for (int i = warp; i < 32; i += A4_WARPS) {
+          const int r = 32 * q + i;
+          if (r >= T || s_node[r] < 0) continue;
+          a4_walk_row<KF>(g, w, rs, Ub + i * w.ldu, s_node[r], s_E[r], s_head[r], s_tref[r], l,
+                          lane);
+        }
+        __syncthreads();
+        if (quad == q) {  // ubar rows -> TMEM (bf16 hi|lo) where q~ was
+          const int nch = w.Ku / 16;
+          for (int c = cg; c < 2 * nch; c += 4) {
+            const int h = c / nch, j = c % nch;
+            const float* srow = Ub + lane * w.ldu + h * w.kpad;
+            float v[16];
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4) {
+              const int k = 16 * j + 4 * k4;
+              float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (k < w.kpad) x = *reinterpret_cast<const float4*>(srow + k);
+              v[4 * k4] = x.x; v[4 * k4 + 1] = x.y; v[4 * k4 + 2] = x.z; v[4 * k4 + 3] = x.w;
+            }
+            const int base_col = h == 0 ? w.qt0 : w.qt1;
+            a4_st16(tmem + lane_base + (uint32_t)(base_col + 8 * j),
+                    tmem + lane_base + (uint32_t)(base_col + w.Ku / 2 + 8 * j), v);
+          }
+          tmem_st_wait();
+        }
+      }
+      cta_sync_tc();
+      // ---- c_h = ubar_h W_V,h ----
+      gemm(w.qt0, w.Nv, w.Ku, 0);
+      gemm(w.qt1, w.Nv, w.Ku, w.c1);
+      if (quad_live) {  // c -> CA (bf16 hi|lo), head h at element h*Kq
+        const int nch = w.Kq / 16;
+        for (int c = cg; c < 2 * nch; c += 4) {
+          const int h = c / nch, j = c % nch;
+          float a[8], b[8], v[16];
+          const int src = (h == 0 ? 0 : w.c1) + 16 * j;
+          tmem_ld8_nw(tmem + lane_base + (uint32_t)src, a);
+          tmem_ld8_nw(tmem + lane_base + (uint32_t)(src + 8), b);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            v[k] = a[k];
+            v[8 + k] = b[k];
+          }
+          const int e0 = h * w.Kq + 16 * j;  // element index in the c operand
+          a4_st16(tmem + lane_base + (uint32_t)(w.ca + e0 / 2),
+                  tmem + lane_base + (uint32_t)(w.ca + w.Kc / 2 + e0 / 2), v);
+        }
+        tmem_st_wait();
+      }
+      cta_sync_tc();
+      // ---- out_l = c W_O ----
+      gemm(w.ca, w.No, w.Kc, w.acco);
+      if (quad_live) {
+        const int node = row < T ? s_node[row] : -1;
+        const int mode = row < T ? s_mode[row] : 0;
+        const int64_t idx = base + row;
+        float* dst = nullptr;
+        if (node >= 0) {
+          if (mode == 1) dst = last ? rs.dpred + idx * g.ld_d : nullptr;
+          else if (rs.final_out) dst = last ? rs.final_out + idx * g.ld_d : nullptr;
+          else dst = rs.h + ((int64_t)node * g.K + l) * g.ld_d;
+        }
+        for (int j = cg; j < w.Kx / 16; j += 4) {
+          float a[8], b[8], v[16];
+          tmem_ld8_nw(tmem + lane_base + (uint32_t)(w.acco + 16 * j), a);
+          tmem_ld8_nw(tmem + lane_base + (uint32_t)(w.acco + 16 * j + 8), b);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            v[k] = (16 * j + k < g.d) ? a[k] : 0.f;
+            v[8 + k] = (16 * j + 8 + k < g.d) ? b[k] : 0.f;
+          }
+          if (dst) {
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4) {
+              const int c = 16 * j + 4 * k4;
+              if (c < g.d)
+                *reinterpret_cast<float4*>(dst + c) =
+                    make_float4(v[4 * k4], v[4 * k4 + 1], v[4 * k4 + 2], v[4 * k4 + 3]);
+            }
+          }
+          if (!last)
+            a4_st16(tmem + lane_base + (uint32_t)(8 * j), tmem + lane_base + (uint32_t)(w.Kx / 2 + 8 * j), v);
+        }
+        if (!last) tmem_st_wait();
+      }
+      if (last && rs.write_valid && tid < T) {
+        const int node = s_node[tid];
+        if (node >= 0 && s_mode[tid] != 1) {
+          rs.valid[node] = 1;
+          rs.valid_at[node] = rs.valid_at_ptr ? rs.valid_at_ptr[0] : rs.valid_at_const;
+        }
+      }
+    }
+    cta_sync_tc();
+  }
+  if (warp == 0) tmem_free(tmem, 512);
+}

@@ -10,6 +10,7 @@
 
 #include "batch.cuh"
 #include "attn3.cuh"
+#include "attn4.cuh"
 
 #ifndef STGN_VERSION
 #define STGN_VERSION "stgn 0.1.0 sm_100a"
@@ -21,6 +22,7 @@
 typedef void (*attn_fn_t)(Geo, AttnWeights, RingSrc, FlatSrc, int);
 typedef void (*attn2_fn_t)(Geo, EngW, RingSrc, int, int);
 typedef void (*attn3_fn_t)(Geo, TcW, RingSrc, int);
+typedef void (*attn4_fn_t)(Geo, A4W, RingSrc);
 
 template <bool FLAT>
 static attn_fn_t pick_attn(const Geo& g) {
@@ -94,6 +96,10 @@ struct stgn_engine {
   int attn3_tmax = 0;
   TcW tcw;
   bool tc_ok = false, use_tc = false;
+  attn4_fn_t attn4 = nullptr;  // bf16x3 tcgen05 recompute kernel, 128-row tiles (H = 2)
+  size_t attn4_smem = 0;
+  A4W a4w;
+  bool a4_ok = false, use_a4 = false;
   EngW ew;
   size_t mem_smem = 0;
   int mem_wsm = 0;
@@ -217,6 +223,16 @@ int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engin
       cudaGetLastError();
     }
   }
+  memset(&e->a4w, 0, sizeof(e->a4w));
+  if (a4_plan(e->g, &e->a4w)) {
+    e->attn4_smem = attn4_smem_bytes(e->a4w);
+    e->attn4 = e->g.d_e > 0 ? attn4_kernel<1> : attn4_kernel<0>;
+    e->a4_ok = e->attn4_smem <= 227 * 1024 &&
+               cudaFuncSetAttribute((const void*)e->attn4,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)e->attn4_smem) == cudaSuccess;
+    cudaGetLastError();
+  }
   ce = cudaFuncSetAttribute((const void*)e->attn2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)e->attn2_smem);
   if (ce != cudaSuccess) {
@@ -306,6 +322,15 @@ int stgn_engine_set_weights(stgn_engine* e, const stgn_weights* w) {
     e->tcw.bq = w->bq;
     e->tcw.omega = w->omega;
   }
+  e->use_a4 = e->a4_ok && w->t4q && w->t4k && w->t4v && w->t4o && w->t4bq;
+  if (e->use_a4) {
+    e->a4w.wq = w->t4q;
+    e->a4w.wk = w->t4k;
+    e->a4w.wv = w->t4v;
+    e->a4w.wo = w->t4o;
+    e->a4w.bq = w->t4bq;
+    e->a4w.omega = w->omega;
+  }
   e->aw.wq = w->wq;
   e->aw.wkt = w->wkt;
   e->aw.wv = w->wv;
@@ -351,7 +376,9 @@ static RingSrc ring_src(const stgn_engine* e) {
 }
 
 static void launch_attn(const stgn_engine* e, const RingSrc& rs, cudaStream_t st) {
-  if (e->use_tc)
+  if (e->use_a4)
+    e->attn4<<<e->num_sms, A4_THREADS, e->attn4_smem, st>>>(e->g, e->a4w, rs);
+  else if (e->use_tc)
     e->attn3<<<e->num_sms, A3_THREADS, e->attn3_smem, st>>>(e->g, e->tcw, rs, e->attn3_tmax);
   else
     e->attn2<<<e->num_sms, A2_THREADS, e->attn2_smem, st>>>(e->g, e->ew, rs, e->attn2_tmax,
@@ -858,10 +885,11 @@ extern "C" int stgn_pipeline_many(const stgn_dims* dims, int64_t N, int64_t E, c
 
 extern "C" int stgn_engine_info(stgn_engine* e, int64_t* info, int n) {
   if (!e || !info) return STGN_ERR_INVALID;
-  const int64_t v[10] = {e->graph ? 1 : 0, e->cond_used ? 1 : 0, e->launches, e->attn2_tmax,
+  const int64_t v[12] = {e->graph ? 1 : 0, e->cond_used ? 1 : 0, e->launches, e->attn2_tmax,
                          e->attn2_wsm, e->num_sms, (int64_t)e->attn2_smem, (int64_t)e->mem_smem,
-                         e->use_tc ? 1 : 0, e->attn3_tmax};
-  for (int i = 0; i < n && i < 10; ++i) info[i] = v[i];
+                         e->use_tc ? 1 : 0, e->attn3_tmax, e->use_a4 ? 1 : 0,
+                         (int64_t)e->attn4_smem};
+  for (int i = 0; i < n && i < 12; ++i) info[i] = v[i];
   return STGN_OK;
 }
 

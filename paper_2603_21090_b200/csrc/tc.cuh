@@ -130,6 +130,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// ---- TMA bulk copy (1-D, global -> shared) completing on an mbarrier ----
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// one thread: stage `bytes` (multiple of 16) into dst in <= 32 KB pieces, one tx count
+__device__ __forceinline__ void bulk_stage(void* dst, const void* src, uint32_t bytes,
+                                           uint64_t* bar) {
+  mbar_expect_tx(bar, bytes);
+  for (uint32_t o = 0; o < bytes; o += 32768u) {
+    const uint32_t n = bytes - o < 32768u ? bytes - o : 32768u;
+    bulk_g2s(reinterpret_cast<char*>(dst) + o, reinterpret_cast<const char*>(src) + o, n, bar);
+  }
+}
+
 // ---- TMEM -> registers: 32 lanes x 8 consecutive 32-bit columns per warp ----
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   uint32_t r[8];

@@ -34,6 +34,17 @@ def _torch():
     return torch
 
 
+def _bf16_rne(x):
+    """float64 -> bf16 bits (uint16), via float32, round to nearest even."""
+    u = np.asarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
+    return u.astype(np.uint16)
+
+
+def _bf16_float(b):
+    return (b.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
 def _rup(x, m):
     return (x + m - 1) // m * m
 
@@ -410,7 +421,7 @@ class IncrementalEngine:
 
     def __init__(self, cfg: RunConfig, params: ModelParameters, *, recompute: str = "affected",
                  max_batch: int | None = None, device: int | None = None,
-                 tensor_cores: bool = True):
+                 tensor_cores: bool | str = True):
         cfg.validate()
         if cfg.mode != "exact":
             raise ConfigError("the B200 engine implements exact mode (delta mode is out of scope)")
@@ -428,7 +439,11 @@ class IncrementalEngine:
         self.ld_s, self.ld_d = _rup(dm.d_s, 4), _rup(dm.d, 4)
         self.ld_e = _rup(max(dm.d_e, 1), 4)
         self.recompute = recompute
-        self.tensor_cores = bool(tensor_cores)  # tcgen05 split-TF32 GEMMs where the plan fits
+        # tcgen05 GEMMs where the TMEM plan fits: True = bf16x3 128-row kernel (H = 2,
+        # k_in <= 224), else split-TF32; "tf32" = split-TF32 only; False = FFMA
+        if tensor_cores not in (True, False, "tf32"):
+            raise ConfigError("tensor_cores must be True, False or 'tf32'")
+        self.tensor_cores = tensor_cores
         self._L = _lib.lib()
         self._dims = _lib.dims_struct(dm)
         self._max_batch = max(int(max_batch or cfg.batch_size), 1)
@@ -526,9 +541,65 @@ class IncrementalEngine:
             W["tck"] = self._pack_kmajor(p.w_k)                         # (K, H, k_in, d_k)
             W["tcv"] = self._pack_kmajor(np.transpose(p.w_v, (0, 1, 3, 2)))  # (K, H, d_k, k_in)
             W["tco"] = self._pack_kmajor(np.transpose(p.w_o, (0, 2, 1)))     # (K, d, HD)
+        if self.tensor_cores is True and H == 2:
+            W.update(self._pack_bf16x3())
         self._w = W
         ws = _lib.Weights(**{k: v.data_ptr() for k, v in W.items()}, bpred=float(p.b_pred))
         _lib.check(self._L.stgn_engine_set_weights(self._handle, C.byref(ws)), "set_weights")
+
+    def _pack_bf16x3(self):
+        """Operands of the bf16x3 recompute kernel (stgn.h t4*): the folded
+        per-head weights with 1/sqrt(d_k) in W_K and the time-encoding
+        amplitude sqrt(1/d_t) in the time rows of W_K and W_V."""
+        p, dm = self.params, self.dims
+        K, H, d_k, d = dm.layers, dm.heads, dm.d_k, dm.d
+        Kq = _rup(d_k, 16)
+        amp = np.sqrt(1.0 / dm.d_t)
+        t0 = d + dm.d_e                       # first time-encoding row of k_in
+        ang = p.omega * 0.0
+        phi0 = np.empty(dm.d_t)
+        phi0[0::2], phi0[1::2] = np.cos(ang), np.sin(ang)
+        phi0 *= amp
+        wq = np.zeros((K, H * Kq, d))         # [n = h*Kq + j][k]
+        bq = np.zeros((K, H, Kq))
+        wo = np.zeros((K, d, H * Kq))         # [m][h*Kq + j]
+        for h in range(H):
+            wq[:, h * Kq:h * Kq + d_k, :] = np.transpose(p.w_q[:, h, :d, :], (0, 2, 1))
+            bq[:, h, :d_k] = np.einsum("t,ltc->lc", phi0, p.w_q[:, h, d:, :])
+            wo[:, :, h * Kq:h * Kq + d_k] = np.transpose(p.w_o[:, h * d_k:(h + 1) * d_k, :], (0, 2, 1))
+        # key rows in the kernel's 4-padded layout [payload | features | time]
+        r4 = lambda x: _rup(x, 4)  # noqa: E731
+        kmap = np.concatenate([np.arange(d), r4(d) + np.arange(dm.d_e),
+                               r4(d) + r4(dm.d_e) + np.arange(dm.d_t)])
+        kpad = r4(d) + r4(dm.d_e) + r4(dm.d_t)
+        wk = np.zeros((K, H, kpad, d_k))      # [n][k]
+        wk[:, :, kmap, :] = p.w_k / np.sqrt(d_k)
+        wk[:, :, kmap[t0:], :] *= amp
+        wv = np.zeros((K, H, d_k, kpad))      # [n][k]
+        wv[:, :, :, kmap] = np.transpose(p.w_v, (0, 1, 3, 2))
+        wv[:, :, :, kmap[t0:]] *= amp
+        return {"t4q": self._pack_kmajor_bf16(wq), "t4k": self._pack_kmajor_bf16(wk),
+                "t4v": self._pack_kmajor_bf16(wv), "t4o": self._pack_kmajor_bf16(wo),
+                "t4bq": self._torch.tensor(bq.astype(np.float32), device=self.device)}
+
+    def _pack_kmajor_bf16(self, B):
+        """(..., N, K) float64 -> (..., 2*Np*Kp) bf16 bits (int16 tensor): the
+        K-major tcgen05 B operand (8x8 core matrices), hi block then lo block,
+        hi = bf16(w), lo = bf16(w - hi), both rounded to nearest even."""
+        B = np.asarray(B, dtype=np.float64)
+        *lead, N, K = B.shape
+        Np, Kp = _rup(N, 16), _rup(K, 16)
+        Bp = np.zeros((*lead, Np, Kp))
+        Bp[..., :N, :K] = B
+        hi = _bf16_rne(Bp)
+        lo = _bf16_rne(Bp - _bf16_float(hi))
+        n, k = np.meshgrid(np.arange(Np), np.arange(Kp), indexing="ij")
+        idx = (((n // 8) * (Kp // 8) + k // 8) * 64 + (n % 8) * 8 + k % 8).ravel()
+        out = np.zeros((*lead, 2, Np * Kp), dtype=np.uint16)
+        out[..., 0, idx] = hi.reshape(*lead, Np * Kp)
+        out[..., 1, idx] = lo.reshape(*lead, Np * Kp)
+        out = np.ascontiguousarray(out.reshape(*lead, 2 * Np * Kp)).view(np.int16)
+        return self._torch.tensor(out, device=self.device)
 
     def _pack_kmajor(self, B):
         """(..., N, K) float64 -> (..., 2*Np*Kp) float32 tensor: the K-major
@@ -701,11 +772,11 @@ class IncrementalEngine:
 
     def info(self) -> dict:
         """Engine facts from the C ABI (graph replay, conditional rebuild, tiles)."""
-        buf = (C.c_int64 * 10)()
-        _lib.check(self._L.stgn_engine_info(self._handle, buf, 10), "info")
+        buf = (C.c_int64 * 12)()
+        _lib.check(self._L.stgn_engine_info(self._handle, buf, 12), "info")
         keys = ("graph_active", "conditional_rebuild", "launches_per_batch", "attn_tile_rows",
                 "attn_staged_weight_floats", "num_sms", "attn_smem_bytes", "memory_smem_bytes",
-                "tensor_cores", "tc_tile_rows")
+                "tensor_cores", "tc_tile_rows", "bf16x3", "bf16x3_smem_bytes")
         return {k: int(buf[i]) for i, k in enumerate(keys)}
 
     def _after_batch(self, B, t_last, top):

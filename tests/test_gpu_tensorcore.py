@@ -1,6 +1,7 @@
 """tcgen05 split-TF32 GEMM self-test (descriptor/layout/TMEM round trip)
 against a float64 numpy product; tolerance 2e-6 relative to sum|x||w|.
-Also checks the engine's tensor-core recompute against its FFMA twin."""
+Also checks the engine's three recompute kernels (bf16x3 128-row, split-TF32,
+FFMA) against the reference fixtures."""
 
 import ctypes as C
 
@@ -47,12 +48,16 @@ def test_engine_tensor_core_path_vs_ffma(name):
     z = load("engine_" + name)
     cfg, params, stream = case_setup(z)
     n = int(z["node_count"])
-    for tc in (True, False):
+    for tc in (True, "tf32", False):
         eng = IncrementalEngine(cfg, params, tensor_cores=tc)
         preds = []
         for b in batches(stream, cfg.batch_size):
             preds.extend(eng.process_batch_arrays(b.src, b.dst, b.t, b.feat).tolist())
-        assert eng.info()["tensor_cores"] == int(tc)
+        info = eng.info()
+        # True selects the bf16x3 128-row kernel (all three cases have H = 2 and
+        # a 4-padded k_in <= 224); "tf32" the split-TF32 kernel; False the FFMA kernel
+        assert info["bf16x3"] == int(tc is True), (tc, info)
+        assert info["tensor_cores"] == int(tc is not False), (tc, info)
         assert np.max(np.abs(np.array(preds) - z["preds"])) <= 1e-5
         assert_rows_close(eng.cache.h[:n].reshape(n, -1), z["h"].reshape(n, -1), f"h tc={tc}")
         assert_rows_close(eng.memory.states[:n], z["memory"], f"memory tc={tc}")
