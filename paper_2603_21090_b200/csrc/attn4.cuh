@@ -387,6 +387,168 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   }
 }
 
+// Walk of two rows per warp, one per half-warp (16 lanes): lane hl of a half
+// owns key features [8hl, 8hl+8) of each segment (payload, edge features,
+// time encoding; the time segment's 8 values are frequencies 4hl..4hl+3), so
+// the per-entry scalar work (timestamps, softmax, masks) and the logit
+// butterfly are shared by two rows. The loop runs to the larger of the two
+// entry counts; the shorter row's surplus entries are masked.
+template <int KF>
+__device__ __forceinline__ void a4_walk_pair(const Geo& g, const A4W& w, const RingSrc& rs,
+                                             const double* s_om, float* U, int node, int E,
+                                             int hd, double tref, int l, int lane) {
+  constexpr int EC = 2;
+  const int hl = lane & 15;
+  const int kfo = w.kfo, kto = w.kto, kp = w.kpad;
+  const bool vp0 = 8 * hl < kfo, vp1 = 8 * hl + 4 < kfo;
+  const bool vf0 = KF && 8 * hl < kto - kfo, vf1 = KF && 8 * hl + 4 < kto - kfo;
+  const bool vt0 = 8 * hl < kp - kto, vt1 = 8 * hl + 4 < kp - kto;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 qp[2][2], qt[2][2], qf[2][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float* Uh = U + h * kp + 8 * hl;
+    qp[h][0] = vp0 ? *reinterpret_cast<const float4*>(Uh) : z4;
+    qp[h][1] = vp1 ? *reinterpret_cast<const float4*>(Uh + 4) : z4;
+    qt[h][0] = vt0 ? *reinterpret_cast<const float4*>(Uh + kto) : z4;
+    qt[h][1] = vt1 ? *reinterpret_cast<const float4*>(Uh + kto + 4) : z4;
+    qf[h][0] = vf0 ? *reinterpret_cast<const float4*>(Uh + kfo) : z4;
+    qf[h][1] = vf1 ? *reinterpret_cast<const float4*>(Uh + kfo + 4) : z4;
+  }
+  float2 up[2][4], ut[2][4], uf[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) up[h][c] = ut[h][c] = uf[h][c] = make_float2(0.f, 0.f);
+  float mx[2] = {-INFINITY, -INFINITY}, zs[2] = {0.f, 0.f};
+  const int Emax = max(E, __shfl_xor_sync(0xffffffffu, E, 16));
+  const float* payb = rs.ring_pay + ((int64_t)max(node, 0) * g.K + l) * g.L * g.ld_d + 8 * hl;
+  const float* ftb = rs.ring_feat + (int64_t)max(node, 0) * g.L * g.ld_e + 8 * hl;
+  const double* tb = rs.ring_t + (int64_t)max(node, 0) * g.L;
+  for (int e0 = 0; e0 < Emax; e0 += EC) {
+    float4 kpv[EC][2], kfv[EC][2];
+    double tv[EC];
+#pragma unroll
+    for (int u = 0; u < EC; ++u) {
+      const bool ev = e0 + u < E;
+      int slot = hd + e0 + u;
+      if (slot >= g.L) slot -= g.L;
+      const float* pp = payb + slot * g.ld_d;
+      kpv[u][0] = (ev && vp0) ? __ldg(reinterpret_cast<const float4*>(pp)) : z4;
+      kpv[u][1] = (ev && vp1) ? __ldg(reinterpret_cast<const float4*>(pp + 4)) : z4;
+      if (KF) {
+        const float* fp = ftb + slot * g.ld_e;
+        kfv[u][0] = (ev && vf0) ? __ldg(reinterpret_cast<const float4*>(fp)) : z4;
+        kfv[u][1] = (ev && vf1) ? __ldg(reinterpret_cast<const float4*>(fp + 4)) : z4;
+      }
+      tv[u] = ev ? __ldg(tb + slot) : tref;
+    }
+    float4 ktv[EC][2];
+    float part[2 * EC];
+#pragma unroll
+    for (int u = 0; u < EC; ++u) {
+      const double dt = tref - tv[u];
+      float sc[4], cc[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int f = 4 * hl + k;
+        sc[k] = 0.f;
+        cc[k] = 0.f;
+        if (f < g.half) phase_sincos(s_om[f], dt, &sc[k], &cc[k]);
+      }
+      ktv[u][0] = make_float4(cc[0], sc[0], cc[1], sc[1]);
+      ktv[u][1] = make_float4(cc[2], sc[2], cc[3], sc[3]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float2 a = fmul2(make_float2(qp[h][0].x, qp[h][0].y), make_float2(kpv[u][0].x, kpv[u][0].y));
+        a = ffma2(make_float2(qp[h][0].z, qp[h][0].w), make_float2(kpv[u][0].z, kpv[u][0].w), a);
+        a = ffma2(make_float2(qp[h][1].x, qp[h][1].y), make_float2(kpv[u][1].x, kpv[u][1].y), a);
+        a = ffma2(make_float2(qp[h][1].z, qp[h][1].w), make_float2(kpv[u][1].z, kpv[u][1].w), a);
+        a = ffma2(make_float2(qt[h][0].x, qt[h][0].y), make_float2(ktv[u][0].x, ktv[u][0].y), a);
+        a = ffma2(make_float2(qt[h][0].z, qt[h][0].w), make_float2(ktv[u][0].z, ktv[u][0].w), a);
+        a = ffma2(make_float2(qt[h][1].x, qt[h][1].y), make_float2(ktv[u][1].x, ktv[u][1].y), a);
+        a = ffma2(make_float2(qt[h][1].z, qt[h][1].w), make_float2(ktv[u][1].z, ktv[u][1].w), a);
+        if (KF) {
+          a = ffma2(make_float2(qf[h][0].x, qf[h][0].y), make_float2(kfv[u][0].x, kfv[u][0].y), a);
+          a = ffma2(make_float2(qf[h][0].z, qf[h][0].w), make_float2(kfv[u][0].z, kfv[u][0].w), a);
+          a = ffma2(make_float2(qf[h][1].x, qf[h][1].y), make_float2(kfv[u][1].x, kfv[u][1].y), a);
+          a = ffma2(make_float2(qf[h][1].z, qf[h][1].w), make_float2(kfv[u][1].z, kfv[u][1].w), a);
+        }
+        part[2 * u + h] = a.x + a.y;
+      }
+    }
+    // 16-lane transposing butterfly: value v = 2u + h ends on lanes with ((hl >> 2) & 3) == v
+    {
+      const bool b3 = hl & 8, b2 = hl & 4;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const float send = b3 ? part[j] : part[j + 2];
+        const float keep = b3 ? part[j + 2] : part[j];
+        part[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+      const float send = b2 ? part[0] : part[1];
+      const float keep = b2 ? part[1] : part[0];
+      part[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      part[0] += __shfl_xor_sync(0xffffffffu, part[0], 2);
+      part[0] += __shfl_xor_sync(0xffffffffu, part[0], 1);
+    }
+    float lg[2 * EC];
+#pragma unroll
+    for (int v = 0; v < 2 * EC; ++v) lg[v] = __shfl_sync(0xffffffffu, part[0], (lane & 16) | (4 * v));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float cm = -INFINITY;
+#pragma unroll
+      for (int u = 0; u < EC; ++u)
+        if (e0 + u < E) cm = fmaxf(cm, lg[2 * u + h]);
+      const float nm = fmaxf(mx[h], cm);
+      const float scl = nm == -INFINITY ? 1.f : __expf(mx[h] - nm);
+      const float2 sc2 = make_float2(scl, scl);
+      zs[h] *= scl;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        up[h][c] = fmul2(up[h][c], sc2);
+        ut[h][c] = fmul2(ut[h][c], sc2);
+        if (KF) uf[h][c] = fmul2(uf[h][c], sc2);
+      }
+#pragma unroll
+      for (int u = 0; u < EC; ++u) {
+        const float p = (e0 + u < E) ? __expf(lg[2 * u + h] - nm) : 0.f;
+        const float2 p2 = make_float2(p, p);
+        zs[h] += p;
+        up[h][0] = ffma2(p2, make_float2(kpv[u][0].x, kpv[u][0].y), up[h][0]);
+        up[h][1] = ffma2(p2, make_float2(kpv[u][0].z, kpv[u][0].w), up[h][1]);
+        up[h][2] = ffma2(p2, make_float2(kpv[u][1].x, kpv[u][1].y), up[h][2]);
+        up[h][3] = ffma2(p2, make_float2(kpv[u][1].z, kpv[u][1].w), up[h][3]);
+        ut[h][0] = ffma2(p2, make_float2(ktv[u][0].x, ktv[u][0].y), ut[h][0]);
+        ut[h][1] = ffma2(p2, make_float2(ktv[u][0].z, ktv[u][0].w), ut[h][1]);
+        ut[h][2] = ffma2(p2, make_float2(ktv[u][1].x, ktv[u][1].y), ut[h][2]);
+        ut[h][3] = ffma2(p2, make_float2(ktv[u][1].z, ktv[u][1].w), ut[h][3]);
+        if (KF) {
+          uf[h][0] = ffma2(p2, make_float2(kfv[u][0].x, kfv[u][0].y), uf[h][0]);
+          uf[h][1] = ffma2(p2, make_float2(kfv[u][0].z, kfv[u][0].w), uf[h][1]);
+          uf[h][2] = ffma2(p2, make_float2(kfv[u][1].x, kfv[u][1].y), uf[h][2]);
+          uf[h][3] = ffma2(p2, make_float2(kfv[u][1].z, kfv[u][1].w), uf[h][3]);
+        }
+      }
+      mx[h] = nm;
+    }
+  }
+  __syncwarp();
+  if (node < 0) return;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float* Uh = U + h * kp + 8 * hl;
+    const float inv = E > 0 ? 1.f / zs[h] : 0.f;
+    if (vp0) *reinterpret_cast<float4*>(Uh) = make_float4(up[h][0].x * inv, up[h][0].y * inv, up[h][1].x * inv, up[h][1].y * inv);
+    if (vp1) *reinterpret_cast<float4*>(Uh + 4) = make_float4(up[h][2].x * inv, up[h][2].y * inv, up[h][3].x * inv, up[h][3].y * inv);
+    if (vt0) *reinterpret_cast<float4*>(Uh + kto) = make_float4(ut[h][0].x * inv, ut[h][0].y * inv, ut[h][1].x * inv, ut[h][1].y * inv);
+    if (vt1) *reinterpret_cast<float4*>(Uh + kto + 4) = make_float4(ut[h][2].x * inv, ut[h][2].y * inv, ut[h][3].x * inv, ut[h][3].y * inv);
+    if (vf0) *reinterpret_cast<float4*>(Uh + kfo) = make_float4(uf[h][0].x * inv, uf[h][0].y * inv, uf[h][1].x * inv, uf[h][1].y * inv);
+    if (vf1) *reinterpret_cast<float4*>(Uh + kfo + 4) = make_float4(uf[h][2].x * inv, uf[h][2].y * inv, uf[h][3].x * inv, uf[h][3].y * inv);
+  }
+}
+
 template <int KF>
 __global__ void __launch_bounds__(A4_THREADS, 1)
 attn4_kernel(Geo g, A4W w, RingSrc rs) {
@@ -400,6 +562,9 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
   __shared__ int s_node[A4_TMAX], s_E[A4_TMAX], s_head[A4_TMAX], s_mode[A4_TMAX];
   __shared__ double s_tref[A4_TMAX];
   __shared__ uint64_t mbar, wbar[2];
+  __shared__ uint64_t qbar_full[2], qbar_done[2], qbar_packed[2];
+  __shared__ int qctr[2];
+  __shared__ double s_om[64];
   __shared__ uint32_t tslot;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -417,10 +582,16 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
   const int64_t d_rows = rs.fused ? (int64_t)rs.post_n[0] : 0;
 
   if (warp == 0) tmem_alloc(&tslot, 512);
+  if (tid < 64) s_om[tid] = tid < g.half ? w.omega[tid] : 0.0;
   if (tid == 0) {
     mbar_init(&mbar, 1);
     mbar_init(&wbar[0], 1);
     mbar_init(&wbar[1], 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&qbar_full[b], 128);
+      mbar_init(&qbar_done[b], A4_THREADS);
+      mbar_init(&qbar_packed[b], 128);
+    }
     mbar_fence_init();
   }
   tc_fence_before();
@@ -439,10 +610,15 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
     if (total_blocks > 1) stage(1);
   }
   int64_t G = 0;  // weight blocks consumed by this CTA
-  // one GEMM: wait for its weights, MMA, wait for the MMA, refill the buffer
+  int ub_use[2] = {0, 0};  // uses of each quadrant row buffer so far (mbarrier phases)
+  // one GEMM: wait for its weights, MMA, wait for the MMA, refill the buffer.
+  // Callers put a CTA barrier before every gemm: mbarrier waits are by phase
+  // parity, so no thread may fall two commit phases behind.
   auto gemm = [&](int a, int Np, int Kp, int dcol) {
-    mbar_wait(&wbar[G & 1], (uint32_t)((G >> 1) & 1));
-    if (tid == 0) a4_mma(tmem, a, (G & 1) ? Wb1 : Wb0, Np, Kp, dcol, &mbar);
+    if (tid == 0) {  // only the issuing thread waits for the weights
+      mbar_wait(&wbar[G & 1], (uint32_t)((G >> 1) & 1));
+      a4_mma(tmem, a, (G & 1) ? Wb1 : Wb0, Np, Kp, dcol, &mbar);
+    }
     mbar_wait(&mbar, (uint32_t)(G & 1));
     tc_fence_after();
     if (tid == 0 && G + 2 < total_blocks) stage(G + 2);
@@ -508,7 +684,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
 
     for (int l = 0; l < g.K; ++l) {
       const bool last = (l == g.K - 1);
-      a4_prefetch(g, rs, s_node, s_E, s_head, 0, min(32, T), l, tid);
+      a4_prefetch(g, rs, s_node, s_E, s_head, 0, T, l, tid);  // this layer's ring rows
       // ---- q = x W_Q + b ----
       cta_sync_tc();
       gemm(0, w.Nq, w.Kx, w.Kx);
@@ -535,10 +711,18 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
         gemm(0, w.Nk, w.Kq, h == 0 ? w.qt0 : w.qt1);
       }
       // ---- walk, one 32-row quadrant at a time ----
+      // Quadrant pipeline over two row buffers, ordered by mbarriers instead of
+      // CTA barriers: the quadrant's own warps copy q~ out of TMEM (full), every
+      // warp takes rows of the buffer from a shared counter and walks them
+      // (done), the quadrant's warps pack ubar back into TMEM (packed), which
+      // frees the buffer for quadrant q + 2. A warp that finishes early moves
+      // on to the next quadrant's rows.
       for (int q = 0; q < nq; ++q) {
-        float* Ub = (q & 1) ? Ub1 : Ub0;
-        if (q + 1 < nq) a4_prefetch(g, rs, s_node, s_E, s_head, 32 * (q + 1), min(32 * (q + 2), T), l, tid);
+        const int b = q & 1;
+        float* Ub = b ? Ub1 : Ub0;
+        const int nrows = min(32, T - 32 * q);
         if (quad == q) {  // q~ rows of this quadrant -> Ub
+          if (ub_use[b] > 0) mbar_wait(&qbar_packed[b], (uint32_t)((ub_use[b] - 1) & 1));
           const int nch = (w.kpad + 7) / 8;
           for (int c = cg; c < 2 * nch; c += 4) {
             const int h = c / nch, j = c % nch;
@@ -550,16 +734,25 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
             if (8 * j + 8 <= w.kpad)
               *reinterpret_cast<float4*>(dst + 4) = make_float4(v[4], v[5], v[6], v[7]);
           }
+          if (tid == 32 * q) qctr[b] = 0;  // warp (quad q, cg 0), lane 0
+          mbar_arrive(&qbar_full[b]);
         }
-        __syncthreads();
-        for (int i = warp; i < 32; i += A4_WARPS) {
-          const int r = 32 * q + i;
-          if (r >= T || s_node[r] < 0) continue;
-          a4_walk_row<KF>(g, w, rs, Ub + i * w.ldu, s_node[r], s_E[r], s_head[r], s_tref[r], l,
-                          lane);
+        mbar_wait(&qbar_full[b], (uint32_t)(ub_use[b] & 1));
+        for (;;) {  // two rows per warp (one per half-warp)
+          int i = 0;
+          if (lane == 0) i = atomicAdd(&qctr[b], 2);
+          i = __shfl_sync(0xffffffffu, i, 0);
+          if (i >= nrows) break;
+          const int ii = i + (lane >> 4);
+          const int r = 32 * q + ii;
+          const bool live = ii < nrows && s_node[r] >= 0;
+          a4_walk_pair<KF>(g, w, rs, s_om, Ub + (live ? ii : i) * w.ldu, live ? s_node[r] : -1,
+                           live ? s_E[r] : 0, live ? s_head[r] : 0, live ? s_tref[r] : 0.0, l,
+                           lane);
         }
-        __syncthreads();
+        mbar_arrive(&qbar_done[b]);
         if (quad == q) {  // ubar rows -> TMEM (bf16 hi|lo) where q~ was
+          mbar_wait(&qbar_done[b], (uint32_t)(ub_use[b] & 1));
           const int nch = w.Ku / 16;
           for (int c = cg; c < 2 * nch; c += 4) {
             const int h = c / nch, j = c % nch;
@@ -577,11 +770,16 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
                     tmem + lane_base + (uint32_t)(base_col + w.Ku / 2 + 8 * j), v);
           }
           tmem_st_wait();
+          mbar_arrive(&qbar_packed[b]);
         }
+        ++ub_use[b];
       }
       cta_sync_tc();
       // ---- c_h = ubar_h W_V,h ----
       gemm(w.qt0, w.Nv, w.Ku, 0);
+      // every thread must observe the V_0 commit phase before V_1 can complete the
+      // next one (a parity wait cannot tell phase G from phase G + 2)
+      cta_sync_tc();
       gemm(w.qt1, w.Nv, w.Ku, w.c1);
       if (quad_live) {  // c -> CA (bf16 hi|lo), head h at element h*Kq
         const int nch = w.Kq / 16;
