@@ -387,168 +387,6 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   }
 }
 
-// Walk of two rows per warp, one per half-warp (16 lanes): lane hl of a half
-// owns key features [8hl, 8hl+8) of each segment (payload, edge features,
-// time encoding; the time segment's 8 values are frequencies 4hl..4hl+3), so
-// the per-entry scalar work (timestamps, softmax, masks) and the logit
-// butterfly are shared by two rows. The loop runs to the larger of the two
-// entry counts; the shorter row's surplus entries are masked.
-template <int KF>
-__device__ __forceinline__ void a4_walk_pair(const Geo& g, const A4W& w, const RingSrc& rs,
-                                             const double* s_om, float* U, int node, int E,
-                                             int hd, double tref, int l, int lane) {
-  constexpr int EC = 2;
-  const int hl = lane & 15;
-  const int kfo = w.kfo, kto = w.kto, kp = w.kpad;
-  const bool vp0 = 8 * hl < kfo, vp1 = 8 * hl + 4 < kfo;
-  const bool vf0 = KF && 8 * hl < kto - kfo, vf1 = KF && 8 * hl + 4 < kto - kfo;
-  const bool vt0 = 8 * hl < kp - kto, vt1 = 8 * hl + 4 < kp - kto;
-  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  float4 qp[2][2], qt[2][2], qf[2][2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const float* Uh = U + h * kp + 8 * hl;
-    qp[h][0] = vp0 ? *reinterpret_cast<const float4*>(Uh) : z4;
-    qp[h][1] = vp1 ? *reinterpret_cast<const float4*>(Uh + 4) : z4;
-    qt[h][0] = vt0 ? *reinterpret_cast<const float4*>(Uh + kto) : z4;
-    qt[h][1] = vt1 ? *reinterpret_cast<const float4*>(Uh + kto + 4) : z4;
-    qf[h][0] = vf0 ? *reinterpret_cast<const float4*>(Uh + kfo) : z4;
-    qf[h][1] = vf1 ? *reinterpret_cast<const float4*>(Uh + kfo + 4) : z4;
-  }
-  float2 up[2][4], ut[2][4], uf[2][4];
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) up[h][c] = ut[h][c] = uf[h][c] = make_float2(0.f, 0.f);
-  float mx[2] = {-INFINITY, -INFINITY}, zs[2] = {0.f, 0.f};
-  const int Emax = max(E, __shfl_xor_sync(0xffffffffu, E, 16));
-  const float* payb = rs.ring_pay + ((int64_t)max(node, 0) * g.K + l) * g.L * g.ld_d + 8 * hl;
-  const float* ftb = rs.ring_feat + (int64_t)max(node, 0) * g.L * g.ld_e + 8 * hl;
-  const double* tb = rs.ring_t + (int64_t)max(node, 0) * g.L;
-  for (int e0 = 0; e0 < Emax; e0 += EC) {
-    float4 kpv[EC][2], kfv[EC][2];
-    double tv[EC];
-#pragma unroll
-    for (int u = 0; u < EC; ++u) {
-      const bool ev = e0 + u < E;
-      int slot = hd + e0 + u;
-      if (slot >= g.L) slot -= g.L;
-      const float* pp = payb + slot * g.ld_d;
-      kpv[u][0] = (ev && vp0) ? __ldg(reinterpret_cast<const float4*>(pp)) : z4;
-      kpv[u][1] = (ev && vp1) ? __ldg(reinterpret_cast<const float4*>(pp + 4)) : z4;
-      if (KF) {
-        const float* fp = ftb + slot * g.ld_e;
-        kfv[u][0] = (ev && vf0) ? __ldg(reinterpret_cast<const float4*>(fp)) : z4;
-        kfv[u][1] = (ev && vf1) ? __ldg(reinterpret_cast<const float4*>(fp + 4)) : z4;
-      }
-      tv[u] = ev ? __ldg(tb + slot) : tref;
-    }
-    float4 ktv[EC][2];
-    float part[2 * EC];
-#pragma unroll
-    for (int u = 0; u < EC; ++u) {
-      const double dt = tref - tv[u];
-      float sc[4], cc[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int f = 4 * hl + k;
-        sc[k] = 0.f;
-        cc[k] = 0.f;
-        if (f < g.half) phase_sincos(s_om[f], dt, &sc[k], &cc[k]);
-      }
-      ktv[u][0] = make_float4(cc[0], sc[0], cc[1], sc[1]);
-      ktv[u][1] = make_float4(cc[2], sc[2], cc[3], sc[3]);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float2 a = fmul2(make_float2(qp[h][0].x, qp[h][0].y), make_float2(kpv[u][0].x, kpv[u][0].y));
-        a = ffma2(make_float2(qp[h][0].z, qp[h][0].w), make_float2(kpv[u][0].z, kpv[u][0].w), a);
-        a = ffma2(make_float2(qp[h][1].x, qp[h][1].y), make_float2(kpv[u][1].x, kpv[u][1].y), a);
-        a = ffma2(make_float2(qp[h][1].z, qp[h][1].w), make_float2(kpv[u][1].z, kpv[u][1].w), a);
-        a = ffma2(make_float2(qt[h][0].x, qt[h][0].y), make_float2(ktv[u][0].x, ktv[u][0].y), a);
-        a = ffma2(make_float2(qt[h][0].z, qt[h][0].w), make_float2(ktv[u][0].z, ktv[u][0].w), a);
-        a = ffma2(make_float2(qt[h][1].x, qt[h][1].y), make_float2(ktv[u][1].x, ktv[u][1].y), a);
-        a = ffma2(make_float2(qt[h][1].z, qt[h][1].w), make_float2(ktv[u][1].z, ktv[u][1].w), a);
-        if (KF) {
-          a = ffma2(make_float2(qf[h][0].x, qf[h][0].y), make_float2(kfv[u][0].x, kfv[u][0].y), a);
-          a = ffma2(make_float2(qf[h][0].z, qf[h][0].w), make_float2(kfv[u][0].z, kfv[u][0].w), a);
-          a = ffma2(make_float2(qf[h][1].x, qf[h][1].y), make_float2(kfv[u][1].x, kfv[u][1].y), a);
-          a = ffma2(make_float2(qf[h][1].z, qf[h][1].w), make_float2(kfv[u][1].z, kfv[u][1].w), a);
-        }
-        part[2 * u + h] = a.x + a.y;
-      }
-    }
-    // 16-lane transposing butterfly: value v = 2u + h ends on lanes with ((hl >> 2) & 3) == v
-    {
-      const bool b3 = hl & 8, b2 = hl & 4;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const float send = b3 ? part[j] : part[j + 2];
-        const float keep = b3 ? part[j + 2] : part[j];
-        part[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-      }
-      const float send = b2 ? part[0] : part[1];
-      const float keep = b2 ? part[1] : part[0];
-      part[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-      part[0] += __shfl_xor_sync(0xffffffffu, part[0], 2);
-      part[0] += __shfl_xor_sync(0xffffffffu, part[0], 1);
-    }
-    float lg[2 * EC];
-#pragma unroll
-    for (int v = 0; v < 2 * EC; ++v) lg[v] = __shfl_sync(0xffffffffu, part[0], (lane & 16) | (4 * v));
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float cm = -INFINITY;
-#pragma unroll
-      for (int u = 0; u < EC; ++u)
-        if (e0 + u < E) cm = fmaxf(cm, lg[2 * u + h]);
-      const float nm = fmaxf(mx[h], cm);
-      const float scl = nm == -INFINITY ? 1.f : __expf(mx[h] - nm);
-      const float2 sc2 = make_float2(scl, scl);
-      zs[h] *= scl;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        up[h][c] = fmul2(up[h][c], sc2);
-        ut[h][c] = fmul2(ut[h][c], sc2);
-        if (KF) uf[h][c] = fmul2(uf[h][c], sc2);
-      }
-#pragma unroll
-      for (int u = 0; u < EC; ++u) {
-        const float p = (e0 + u < E) ? __expf(lg[2 * u + h] - nm) : 0.f;
-        const float2 p2 = make_float2(p, p);
-        zs[h] += p;
-        up[h][0] = ffma2(p2, make_float2(kpv[u][0].x, kpv[u][0].y), up[h][0]);
-        up[h][1] = ffma2(p2, make_float2(kpv[u][0].z, kpv[u][0].w), up[h][1]);
-        up[h][2] = ffma2(p2, make_float2(kpv[u][1].x, kpv[u][1].y), up[h][2]);
-        up[h][3] = ffma2(p2, make_float2(kpv[u][1].z, kpv[u][1].w), up[h][3]);
-        ut[h][0] = ffma2(p2, make_float2(ktv[u][0].x, ktv[u][0].y), ut[h][0]);
-        ut[h][1] = ffma2(p2, make_float2(ktv[u][0].z, ktv[u][0].w), ut[h][1]);
-        ut[h][2] = ffma2(p2, make_float2(ktv[u][1].x, ktv[u][1].y), ut[h][2]);
-        ut[h][3] = ffma2(p2, make_float2(ktv[u][1].z, ktv[u][1].w), ut[h][3]);
-        if (KF) {
-          uf[h][0] = ffma2(p2, make_float2(kfv[u][0].x, kfv[u][0].y), uf[h][0]);
-          uf[h][1] = ffma2(p2, make_float2(kfv[u][0].z, kfv[u][0].w), uf[h][1]);
-          uf[h][2] = ffma2(p2, make_float2(kfv[u][1].x, kfv[u][1].y), uf[h][2]);
-          uf[h][3] = ffma2(p2, make_float2(kfv[u][1].z, kfv[u][1].w), uf[h][3]);
-        }
-      }
-      mx[h] = nm;
-    }
-  }
-  __syncwarp();
-  if (node < 0) return;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    float* Uh = U + h * kp + 8 * hl;
-    const float inv = E > 0 ? 1.f / zs[h] : 0.f;
-    if (vp0) *reinterpret_cast<float4*>(Uh) = make_float4(up[h][0].x * inv, up[h][0].y * inv, up[h][1].x * inv, up[h][1].y * inv);
-    if (vp1) *reinterpret_cast<float4*>(Uh + 4) = make_float4(up[h][2].x * inv, up[h][2].y * inv, up[h][3].x * inv, up[h][3].y * inv);
-    if (vt0) *reinterpret_cast<float4*>(Uh + kto) = make_float4(ut[h][0].x * inv, ut[h][0].y * inv, ut[h][1].x * inv, ut[h][1].y * inv);
-    if (vt1) *reinterpret_cast<float4*>(Uh + kto + 4) = make_float4(ut[h][2].x * inv, ut[h][2].y * inv, ut[h][3].x * inv, ut[h][3].y * inv);
-    if (vf0) *reinterpret_cast<float4*>(Uh + kfo) = make_float4(uf[h][0].x * inv, uf[h][0].y * inv, uf[h][1].x * inv, uf[h][1].y * inv);
-    if (vf1) *reinterpret_cast<float4*>(Uh + kfo + 4) = make_float4(uf[h][2].x * inv, uf[h][2].y * inv, uf[h][3].x * inv, uf[h][3].y * inv);
-  }
-}
-
 template <int KF>
 __global__ void __launch_bounds__(A4_THREADS, 1)
 attn4_kernel(Geo g, A4W w, RingSrc rs) {
@@ -564,7 +402,6 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
   __shared__ uint64_t mbar, wbar[2];
   __shared__ uint64_t qbar_full[2], qbar_done[2], qbar_packed[2];
   __shared__ int qctr[2];
-  __shared__ double s_om[64];
   __shared__ uint32_t tslot;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -582,7 +419,6 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
   const int64_t d_rows = rs.fused ? (int64_t)rs.post_n[0] : 0;
 
   if (warp == 0) tmem_alloc(&tslot, 512);
-  if (tid < 64) s_om[tid] = tid < g.half ? w.omega[tid] : 0.0;
   if (tid == 0) {
     mbar_init(&mbar, 1);
     mbar_init(&wbar[0], 1);
@@ -738,17 +574,15 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
           mbar_arrive(&qbar_full[b]);
         }
         mbar_wait(&qbar_full[b], (uint32_t)(ub_use[b] & 1));
-        for (;;) {  // two rows per warp (one per half-warp)
+        for (;;) {
           int i = 0;
-          if (lane == 0) i = atomicAdd(&qctr[b], 2);
+          if (lane == 0) i = atomicAdd(&qctr[b], 1);
           i = __shfl_sync(0xffffffffu, i, 0);
           if (i >= nrows) break;
-          const int ii = i + (lane >> 4);
-          const int r = 32 * q + ii;
-          const bool live = ii < nrows && s_node[r] >= 0;
-          a4_walk_pair<KF>(g, w, rs, s_om, Ub + (live ? ii : i) * w.ldu, live ? s_node[r] : -1,
-                           live ? s_E[r] : 0, live ? s_head[r] : 0, live ? s_tref[r] : 0.0, l,
-                           lane);
+          const int r = 32 * q + i;
+          if (s_node[r] < 0) continue;
+          a4_walk_row<KF>(g, w, rs, Ub + i * w.ldu, s_node[r], s_E[r], s_head[r], s_tref[r], l,
+                          lane);
         }
         mbar_arrive(&qbar_done[b]);
         if (quad == q) {  // ubar rows -> TMEM (bf16 hi|lo) where q~ was
