@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--window-steps", type=int, default=100)
     ap.add_argument("--sweep", default="100,300,1000,3000,10000")
     ap.add_argument("--sweep-steps", type=int, default=30)
+    ap.add_argument("--no-rebuild-leg", action="store_true")
     ap.add_argument("--seed", type=int, default=2)
     ap.add_argument("--rebuild", default="adaptive")
     ap.add_argument("--recompute", default="affected", choices=["affected", "direct"])
@@ -341,6 +342,30 @@ def run_ours(args, world, rank, local_rank):
         "fallback (B200_PROFILING.md)"
     info = eng.info()
 
+    # 3b) full rebuild (C4's O(|V|) path: rebuild_nodes(None)), node-id range per rank
+    rb = None
+    if not args.no_rebuild_leg:
+        from paper_2603_21090_b200.dist import shard_range
+        n_all = eng.node_count
+        lo, hi = shard_range(n_all, world, rank)
+        ents = int(eng._tab.ring_cnt[lo:hi].to(torch.int64).sum().item())
+        r_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        r_ev[0].record(stream)
+        eng.rebuild_nodes(None if world == 1 else range(lo, hi))
+        r_ev[1].record(stream)
+        torch.cuda.synchronize()
+        r_ms = _max_over_ranks(torch, dist, world, dev, float(r_ev[0].elapsed_time(r_ev[1])))
+        by = recompute_bytes(g, hi - lo, ents)
+        rb = {"nodes": n_all, "nodes_per_rank": hi - lo, "ms": r_ms,
+              "nodes_per_s": n_all / (r_ms / 1e3), "entries_rank0": ents,
+              "algorithmic_bytes_rank0": by,
+              "achieved_gbs_rank0": by / (r_ms / 1e3) / 1e9,
+              "frac_hbm": by / (r_ms / 1e3) / 1e9 / hbm_peak,
+              "sharding": f"node-id ranges over {world} rank(s), no data-path collective"}
+
     # 4) batch-size sweep (C4: 100..10K edges/batch) at the end-of-stream state
     sweep_out = []
     for b in sweep:
@@ -390,6 +415,7 @@ def run_ours(args, world, rank, local_rank):
             "engine": info,
             "window": win,
             "sweep": sweep_out,
+            "full_rebuild": rb,
             "setup_s": {"generate": t_gen, "fast_forward": t_ff},
         }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -281,6 +281,10 @@ int stgn_generate_stream(const uint64_t* rng_state, int64_t n, int64_t m, int32_
                          double burstiness, int64_t* src, int64_t* dst, double* t,
                          uint64_t* rng_state_out);
 
+/* Debug: phase timestamps of CTA 0 of the bf16x3 recompute kernel, returns the
+ * count copied (0 unless the library was built with -DA4_PROF); resets. */
+int stgn_debug_a4_prof(uint64_t* out, int cap);
+
 /* Library version string and the sm architecture it was built for. */
 const char* stgn_version(void);
 

@@ -90,10 +90,33 @@ static inline size_t attn4_smem_bytes(const A4W& w) {
   return 1024 + 2 * (size_t)w.wblk_bytes + 2 * 32 * (size_t)w.ldu * 4;
 }
 
-#define A4_THREADS 512
+#ifndef A4_WARPS
 #define A4_WARPS 16
+#endif
+#define A4_THREADS (A4_WARPS * 32)
+// Phase timestamps of CTA 0 (debug builds with -DA4_PROF; read by stgn_debug_a4_prof).
+#ifdef A4_PROF
+__device__ unsigned long long g_a4_prof[8192];
+__device__ int g_a4_prof_n;
+#define A4_MARK(tag)                                                              \
+  do {                                                                           \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && g_a4_prof_n < 8190) {             \
+      unsigned long long t_;                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                      \
+      g_a4_prof[g_a4_prof_n++] = (t_ << 4) | (unsigned long long)(tag);           \
+    }                                                                            \
+  } while (0)
+#else
+#define A4_MARK(tag) do {} while (0)
+#endif
+#define A4_NCG (A4_WARPS / 4)  // warps per TMEM lane quadrant (column groups)
 #define A4_TMAX 128
-#define A4_EC 4  // ring entries per chunk of the walk
+#ifndef A4_PREFETCH
+#define A4_PREFETCH 0  // L2 prefetch of ring rows: 0 none, 1 one quadrant ahead, 2 whole tile per layer
+#endif
+#ifndef A4_EC
+#define A4_EC 4  // ring entries per chunk of the walk (2 or 4)
+#endif
 
 // ---- bf16 helpers ----
 __device__ __forceinline__ uint32_t bf16_bits(float x) {
@@ -101,10 +124,12 @@ __device__ __forceinline__ uint32_t bf16_bits(float x) {
 }
 // hi/lo bf16 split of (a, b), packed two per 32-bit column (element 2c low)
 __device__ __forceinline__ void bf16x2_split(float a, float b, uint32_t& hi, uint32_t& lo) {
-  const uint32_t ha = bf16_bits(a), hb = bf16_bits(b);
-  const float ra = a - __uint_as_float(ha << 16), rb = b - __uint_as_float(hb << 16);
-  hi = ha | (hb << 16);
-  lo = bf16_bits(ra) | (bf16_bits(rb) << 16);
+  // one packed conversion per pair for each of hi and lo (cvt.rn.bf16x2.f32)
+  __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+  hi = *reinterpret_cast<uint32_t*>(&h2);
+  const float ra = a - __uint_as_float(hi << 16), rb = b - __uint_as_float(hi & 0xFFFF0000u);
+  __nv_bfloat162 l2 = __floats2bfloat162_rn(ra, rb);
+  lo = *reinterpret_cast<uint32_t*>(&l2);
 }
 // 16 consecutive elements -> 8 hi columns at col, 8 lo columns at col + half
 __device__ __forceinline__ void a4_st16(uint32_t taddr_hi, uint32_t taddr_lo, const float (&v)[16]) {
@@ -275,6 +300,14 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   const float* payb = rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d + 4 * lane;
   const float* ftb = rs.ring_feat + (int64_t)node * g.L * g.ld_e + 4 * lane;
   const double* tb = rs.ring_t + (int64_t)node * g.L;
+  // ring timestamps are loaded one chunk ahead (the time encoding needs them first)
+  double tn[EC];
+#pragma unroll
+  for (int u = 0; u < EC; ++u) {
+    int slot = hd + u;
+    if (slot >= g.L) slot -= g.L;
+    tn[u] = u < E ? __ldg(tb + slot) : tref;
+  }
   for (int e0 = 0; e0 < E; e0 += EC) {
     float4 kp[EC], kf[EC];
     double tv[EC];
@@ -285,7 +318,12 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
       if (slot >= g.L) slot -= g.L;
       kp[u] = (ev && lp) ? __ldg(reinterpret_cast<const float4*>(payb + slot * g.ld_d)) : zero4;
       kf[u] = (KF && ev && lf) ? __ldg(reinterpret_cast<const float4*>(ftb + slot * g.ld_e)) : zero4;
-      tv[u] = ev ? __ldg(tb + slot) : tref;
+      tv[u] = tn[u];
+      const int en = e0 + EC + u;
+      int sn = hd + en;
+      if (sn >= g.L) sn -= g.L;
+      if (sn >= g.L) sn -= g.L;
+      tn[u] = en < E ? __ldg(tb + sn) : tref;
     }
     // per-lane partial logits, value index v = 2u + h
     float part[2 * EC];
@@ -310,33 +348,37 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
         part[2 * u + h] = a.x + a.y;
       }
     }
-    // transposing butterfly: 8 values -> lane L holds the full sum of value (L >> 2)
-    static_assert(2 * EC == 8, "butterfly assumes 8 logits per chunk");
+    // transposing butterfly: 2*EC values; value v ends on lanes v*(32/(2*EC)) ..
+    float lg[2 * EC];
     {
       const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float send = b4 ? part[j] : part[j + 4];
-        const float keep = b4 ? part[j + 4] : part[j];
+      for (int j = 0; j < EC; ++j) {
+        const float send = b4 ? part[j] : part[j + EC];
+        const float keep = b4 ? part[j + EC] : part[j];
         part[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
       }
+      if constexpr (EC >= 2) {
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const float send = b3 ? part[j] : part[j + 2];
-        const float keep = b3 ? part[j + 2] : part[j];
-        part[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        for (int j = 0; j < EC / 2; ++j) {
+          const float send = b3 ? part[j] : part[j + EC / 2];
+          const float keep = b3 ? part[j + EC / 2] : part[j];
+          part[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
       }
-      {
+      if constexpr (EC >= 4) {
         const float send = b2 ? part[0] : part[1];
         const float keep = b2 ? part[1] : part[0];
         part[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      } else {
+        part[0] += __shfl_xor_sync(0xffffffffu, part[0], 4);
       }
       part[0] += __shfl_xor_sync(0xffffffffu, part[0], 2);
       part[0] += __shfl_xor_sync(0xffffffffu, part[0], 1);
-    }
-    float lg[2 * EC];
+      constexpr int stride = 32 / (2 * EC);
 #pragma unroll
-    for (int v = 0; v < 2 * EC; ++v) lg[v] = __shfl_sync(0xffffffffu, part[0], 4 * v);
+      for (int v = 0; v < 2 * EC; ++v) lg[v] = __shfl_sync(0xffffffffu, part[0], stride * v);
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       float cm = -INFINITY;
@@ -424,9 +466,9 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
     mbar_init(&wbar[0], 1);
     mbar_init(&wbar[1], 1);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&qbar_full[b], 128);
+      mbar_init(&qbar_full[b], 32 * A4_NCG);
       mbar_init(&qbar_done[b], A4_THREADS);
-      mbar_init(&qbar_packed[b], 128);
+      mbar_init(&qbar_packed[b], 32 * A4_NCG);
     }
     mbar_fence_init();
   }
@@ -504,7 +546,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
       if (node >= 0)
         src = s_mode[row] == 2 ? rs.mem_post + (base + row - pre_rows) * g.ld_s
                                : rs.mem + (int64_t)node * g.ld_s;
-      for (int j = cg; j < w.Kx / 16; j += 4) {
+      for (int j = cg; j < w.Kx / 16; j += A4_NCG) {
         float v[16];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -520,15 +562,20 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
 
     for (int l = 0; l < g.K; ++l) {
       const bool last = (l == g.K - 1);
+#if A4_PREFETCH == 2
       a4_prefetch(g, rs, s_node, s_E, s_head, 0, T, l, tid);  // this layer's ring rows
+#elif A4_PREFETCH == 1
+      a4_prefetch(g, rs, s_node, s_E, s_head, 0, min(32, T), l, tid);  // first quadrant
+#endif
       // ---- q = x W_Q + b ----
+      A4_MARK(0);
       cta_sync_tc();
       gemm(0, w.Nq, w.Kx, w.Kx);
       for (int h = 0; h < 2; ++h) {
         // q_h (+ bias) -> QA as bf16 hi|lo
         if (quad_live) {
           const float* bq = w.bq + ((int64_t)l * 2 + h) * w.Kq;
-          for (int j = cg; j < w.Kq / 16; j += 4) {
+          for (int j = cg; j < w.Kq / 16; j += A4_NCG) {
             float a[8], b[8], v[16];
             tmem_ld8_nw(tmem + lane_base + (uint32_t)(w.Kx + h * w.Kq + 16 * j), a);
             tmem_ld8_nw(tmem + lane_base + (uint32_t)(w.Kx + h * w.Kq + 16 * j + 8), b);
@@ -542,11 +589,13 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
           }
           tmem_st_wait();
         }
+        A4_MARK(1);
         cta_sync_tc();
         // ---- q~_h = (W_K,h / sqrt(d_k)) q_h -> QT_h ----
         gemm(0, w.Nk, w.Kq, h == 0 ? w.qt0 : w.qt1);
       }
       // ---- walk, one 32-row quadrant at a time ----
+      A4_MARK(2);
       // Quadrant pipeline over two row buffers, ordered by mbarriers instead of
       // CTA barriers: the quadrant's own warps copy q~ out of TMEM (full), every
       // warp takes rows of the buffer from a shared counter and walks them
@@ -557,10 +606,13 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
         const int b = q & 1;
         float* Ub = b ? Ub1 : Ub0;
         const int nrows = min(32, T - 32 * q);
+#if A4_PREFETCH == 1
+        if (q + 1 < nq) a4_prefetch(g, rs, s_node, s_E, s_head, 32 * (q + 1), min(32 * (q + 2), T), l, tid);
+#endif
         if (quad == q) {  // q~ rows of this quadrant -> Ub
           if (ub_use[b] > 0) mbar_wait(&qbar_packed[b], (uint32_t)((ub_use[b] - 1) & 1));
           const int nch = (w.kpad + 7) / 8;
-          for (int c = cg; c < 2 * nch; c += 4) {
+          for (int c = cg; c < 2 * nch; c += A4_NCG) {
             const int h = c / nch, j = c % nch;
             float v[8];
             tmem_ld8_nw(tmem + lane_base + (uint32_t)((h == 0 ? w.qt0 : w.qt1) + 8 * j), v);
@@ -588,7 +640,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
         if (quad == q) {  // ubar rows -> TMEM (bf16 hi|lo) where q~ was
           mbar_wait(&qbar_done[b], (uint32_t)(ub_use[b] & 1));
           const int nch = w.Ku / 16;
-          for (int c = cg; c < 2 * nch; c += 4) {
+          for (int c = cg; c < 2 * nch; c += A4_NCG) {
             const int h = c / nch, j = c % nch;
             const float* srow = Ub + lane * w.ldu + h * w.kpad;
             float v[16];
@@ -608,6 +660,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
         }
         ++ub_use[b];
       }
+      A4_MARK(3);
       cta_sync_tc();
       // ---- c_h = ubar_h W_V,h ----
       gemm(w.qt0, w.Nv, w.Ku, 0);
@@ -617,7 +670,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
       gemm(w.qt1, w.Nv, w.Ku, w.c1);
       if (quad_live) {  // c -> CA (bf16 hi|lo), head h at element h*Kq
         const int nch = w.Kq / 16;
-        for (int c = cg; c < 2 * nch; c += 4) {
+        for (int c = cg; c < 2 * nch; c += A4_NCG) {
           const int h = c / nch, j = c % nch;
           float a[8], b[8], v[16];
           const int src = (h == 0 ? 0 : w.c1) + 16 * j;
@@ -635,6 +688,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
         }
         tmem_st_wait();
       }
+      A4_MARK(4);
       cta_sync_tc();
       // ---- out_l = c W_O ----
       gemm(w.ca, w.No, w.Kc, w.acco);
@@ -648,7 +702,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
           else if (rs.final_out) dst = last ? rs.final_out + idx * g.ld_d : nullptr;
           else dst = rs.h + ((int64_t)node * g.K + l) * g.ld_d;
         }
-        for (int j = cg; j < w.Kx / 16; j += 4) {
+        for (int j = cg; j < w.Kx / 16; j += A4_NCG) {
           float a[8], b[8], v[16];
           tmem_ld8_nw(tmem + lane_base + (uint32_t)(w.acco + 16 * j), a);
           tmem_ld8_nw(tmem + lane_base + (uint32_t)(w.acco + 16 * j + 8), b);
@@ -672,6 +726,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
         }
         if (!last) tmem_st_wait();
       }
+      A4_MARK(5);
       if (last && rs.write_valid && tid < T) {
         const int node = s_node[tid];
         if (node >= 0 && s_mode[tid] != 1) {

@@ -893,6 +893,24 @@ extern "C" int stgn_engine_info(stgn_engine* e, int64_t* info, int n) {
   return STGN_OK;
 }
 
+// Phase timestamps of CTA 0 of the 128-row recompute kernel (builds with
+// -DA4_PROF only; otherwise 0 entries). Each entry: globaltimer_ns << 4 | tag.
+extern "C" int stgn_debug_a4_prof(uint64_t* out, int cap) {
+#ifdef A4_PROF
+  int n = 0;
+  if (cudaMemcpyFromSymbol(&n, g_a4_prof_n, sizeof(int)) != cudaSuccess) return -1;
+  n = n < cap ? n : cap;
+  if (n > 0 && cudaMemcpyFromSymbol(out, g_a4_prof, sizeof(uint64_t) * n) != cudaSuccess) return -1;
+  const int zero = 0;
+  cudaMemcpyToSymbol(g_a4_prof_n, &zero, sizeof(int));
+  return n;
+#else
+  (void)out;
+  (void)cap;
+  return 0;
+#endif
+}
+
 extern "C" int stgn_debug_tc_gemm(int F, int N, int K, const float* W, const float* X, float* D,
                                   int mode, void* stream) {
   if (F < 1 || F > 128 || N < 1 || N > 256 || K < 1) return STGN_ERR_INVALID;

@@ -12,6 +12,6 @@ fi
 timeout 1200 python bench.py > $O/$TAG.bench.json 2> $O/$TAG.bench.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off -c 400 --csv \
    --log-file $O/$TAG.launches.csv python tools/prof_run.py --batches 10 > $O/$TAG.launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:$KRE -s 2 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:$KRE -s 3 -c 1 \
    -o $O/$TAG.prof -f python tools/prof_run.py --batches 10 > $O/$TAG.prof.log 2>&1
 tail -3 $O/$TAG.pytest.log; tail -1 $O/$TAG.smoke.log; cat $O/$TAG.bench.json; tail -3 $O/$TAG.bench.err
