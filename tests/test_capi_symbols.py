@@ -19,7 +19,7 @@ def _header():
 
 
 def test_header_declares_exactly_the_bound_symbols():
-    declared = set(re.findall(r"\b(stgn_[a-z_]+)\s*\(", _header()))
+    declared = set(re.findall(r"\b(stgn_[a-z0-9_]+)\s*\(", _header()))
     assert declared == set(_lib.EXPORTS)
 
 
