@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--sweep", default="100,300,1000,3000,10000")
     ap.add_argument("--sweep-steps", type=int, default=30)
     ap.add_argument("--no-rebuild-leg", action="store_true")
+    ap.add_argument("--no-direct-leg", action="store_true")
     ap.add_argument("--seed", type=int, default=2)
     ap.add_argument("--rebuild", default="adaptive")
     ap.add_argument("--recompute", default="affected", choices=["affected", "direct"])
@@ -241,7 +242,7 @@ def run_ours(args, world, rank, local_rank):
     SW = args.sweep_steps
     tail = (W + K + KE + P) * B
     total = max(args.edges, tail + B)
-    n_sweep = sum((3 + SW) * b for b in sweep)
+    n_sweep = sum((3 + SW) * b for b in sweep) + (3 + min(K, 100)) * B  # + the direct-scope leg
     t_gen = time.perf_counter()
     st = make_stream(args, total + n_sweep, rank)
     t_gen = time.perf_counter() - t_gen
@@ -341,6 +342,11 @@ def run_ours(args, world, rank, local_rank):
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else \
         "fallback (B200_PROFILING.md)"
     info = eng.info()
+    traffic = None  # DRAM bytes per launch of the same kernel from the committed ncu capture
+    tr_path = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    if os.path.exists(tr_path) and info.get("bf16x3"):
+        with open(tr_path) as fh:
+            traffic = json.load(fh).get("traffic_bytes_per_launch")
 
     # 3b) full rebuild (C4's O(|V|) path: rebuild_nodes(None)), node-id range per rank
     rb = None
@@ -365,6 +371,24 @@ def run_ours(args, world, rank, local_rank):
               "achieved_gbs_rank0": by / (r_ms / 1e3) / 1e9,
               "frac_hbm": by / (r_ms / 1e3) / 1e9 / hbm_peak,
               "sharding": f"node-id ranges over {world} rank(s), no data-path collective"}
+
+    # 3c) the value-identical V_direct-only recompute on the same state ("measure
+    # and report both"); the headline above is the literal recompute over A
+    direct = None
+    if args.recompute == "affected" and not args.no_direct_leg:
+        eng.set_recompute("direct")
+        KD = min(K, 100)
+        df = DeviceStream(eng, st, B, pos, pos + (3 + KD) * B)
+        df.run(0, 3, report_last=True)
+        d_ms, d_per = _timed_batches(torch, stream, df, 3, KD)
+        d_ms = _max_over_ranks(torch, dist, world, dev, d_ms)
+        direct = {"value": world * KD * B / (d_ms / 1e3), "unit": UNIT, "steps": KD,
+                  "p50_ms": float(np.percentile(d_per, 50)), "p99_ms": float(np.percentile(d_per, 99)),
+                  "note": "recompute over V_direct only; A is still computed exactly and its "
+                          "embeddings are bit-identical (payloads frozen at insertion)"}
+        pos += (3 + KD) * B
+        del df
+        eng.set_recompute("affected")
 
     # 4) batch-size sweep (C4: 100..10K edges/batch) at the end-of-stream state
     sweep_out = []
@@ -400,7 +424,8 @@ def run_ours(args, world, rank, local_rank):
                     "p99_ms": float(np.percentile(e2e_lat, 99) * 1e3),
                     "wall_s": t_wall},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": achieved_gbs / hbm_peak, "traffic": None,
+                         "unit": "GB/s", "frac": achieved_gbs / hbm_peak, "traffic": traffic,
+                         "traffic_source": "profiles/r01_ncu_traffic.json (ncu --set full)",
                          "kernel": kname + ": recompute of A (pre-batch memory) + V_direct "
                                            "(post-batch memory), one launch",
                          "avg_launch_ms": a_ms, "algorithmic_bytes": float(np.mean(attn_bytes)),
@@ -416,6 +441,7 @@ def run_ours(args, world, rank, local_rank):
             "window": win,
             "sweep": sweep_out,
             "full_rebuild": rb,
+            "direct_scope": direct,
             "setup_s": {"generate": t_gen, "fast_forward": t_ff},
         }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -249,6 +249,10 @@ int stgn_pipeline_many(const stgn_dims* dims, int64_t N, int64_t E, const float*
                        float* out, float* scores, float* values, float* maxlog, float* zsum,
                        float* qvecs, void* stream);
 
+/* Recompute scope for the following batches (STGN_SCOPE_*); DIRECT needs an
+ * infinite window (else STGN_ERR_INVALID). */
+int stgn_engine_set_scope(stgn_engine* eng, int scope);
+
 /* Per-stage device timing (CUDA events; disables graph replay while on).
  * stage_times writes up to cap stage durations (ms) of the last batch and
  * returns how many; *launches = kernel launches per batch. */

@@ -694,13 +694,25 @@ __global__ void k_drift_decide(StateView st, Scratch s, int rebuild, int64_t int
     // fixed per-block partition -> deterministic sum
     const int64_t per = cdiv(n, gridDim.x);
     const int64_t lo = blockIdx.x * per, hi = lo + per < n ? lo + per : n;
-    for (int64_t q = lo + threadIdx.x; q < hi; q += blockDim.x) {
-      const double acc = st.drift_acc[q];
-      const double dec = acc == 0.0 ? 0.0 : acc * st.gpow[tau - st.drift_touched[q]];
-      part += dec;
-      if (dec > delta_max) {
-        const int pos = atomicAdd(&s.res->n_drifted, 1);
-        s.drifted[pos] = st.cum_list[q];
+    const int64_t bd = blockDim.x;
+    // four independent positions per step (memory-level parallelism), fixed order
+    for (int64_t q0 = lo + threadIdx.x; q0 < hi; q0 += 4 * bd) {
+      double acc[4];
+      int64_t tch[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t q = q0 + u * bd;
+        acc[u] = q < hi ? st.drift_acc[q] : 0.0;
+        tch[u] = q < hi ? st.drift_touched[q] : tau;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double dec = acc[u] == 0.0 ? 0.0 : acc[u] * st.gpow[tau - tch[u]];
+        part += dec;
+        if (dec > delta_max) {
+          const int pos = atomicAdd(&s.res->n_drifted, 1);
+          s.drifted[pos] = st.cum_list[q0 + u * bd];
+        }
       }
     }
   }
@@ -716,13 +728,21 @@ __global__ void k_drift_decide(StateView st, Scratch s, int rebuild, int64_t int
     is_last = (t == gridDim.x - 1);
   }
   __syncthreads();
-  if (is_last && threadIdx.x == 0) {
-    __threadfence();
+  if (!is_last) return;
+  __threadfence();
+  {  // the last block sums the block partials in a fixed order (deterministic)
+    double t = 0.0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) t += s.partials[b];
+    t = warp_sum_d(t);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
     int kind = 0;
     double gdrift = 0.0;
     if (rebuild == STGN_REBUILD_ADAPTIVE) {
       double tot = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) tot += s.partials[b];
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
       gdrift = n > 0 ? tot / (double)n : 0.0;
       if (gdrift > delta_max) {
         const double nn = (double)s.hdr->node_count;

@@ -461,7 +461,7 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   mark();
   // drift + rebuild policy
   k_drift_record<<<g_wide, T, 0, st>>>(v, s);
-  k_drift_decide<<<e->num_sms, T, 0, st>>>(v, s, e->cfg.rebuild, e->cfg.rebuild_interval,
+  k_drift_decide<<<4 * e->num_sms, T, 0, st>>>(v, s, e->cfg.rebuild, e->cfg.rebuild_interval,
                                            e->cfg.delta_max, e->cfg.alpha, cond);
   n += 2;
   mark();
@@ -890,6 +890,15 @@ extern "C" int stgn_engine_info(stgn_engine* e, int64_t* info, int n) {
                          e->use_tc ? 1 : 0, e->attn3_tmax, e->use_a4 ? 1 : 0,
                          (int64_t)e->attn4_smem};
   for (int i = 0; i < n && i < 12; ++i) info[i] = v[i];
+  return STGN_OK;
+}
+
+// Switch the recompute scope between batches (drops the captured graph).
+extern "C" int stgn_engine_set_scope(stgn_engine* e, int scope) {
+  if (!e || (scope != STGN_SCOPE_AFFECTED && scope != STGN_SCOPE_DIRECT)) return STGN_ERR_INVALID;
+  if (scope == STGN_SCOPE_DIRECT && std::isfinite(e->cfg.window)) return STGN_ERR_INVALID;
+  e->cfg.scope = scope;
+  drop_graph(e);
   return STGN_OK;
 }
 

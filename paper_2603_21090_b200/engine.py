@@ -757,6 +757,14 @@ class IncrementalEngine:
             self.last_report = None
         return preds
 
+    def set_recompute(self, recompute: str):
+        """Switch between "affected" (the reference's literal exact mode) and
+        "direct" (value-identical with an infinite window) for later batches."""
+        if recompute not in _lib.SCOPE:
+            raise ConfigError(f"recompute must be one of {tuple(_lib.SCOPE)}")
+        _lib.check(self._L.stgn_engine_set_scope(self._handle, _lib.SCOPE[recompute]), "set_scope")
+        self.recompute = recompute
+
     # -- profiling ----------------------------------------------------------------
     def set_profiling(self, on: bool):
         _lib.check(self._L.stgn_engine_set_profiling(self._handle, int(bool(on))), "profiling")
