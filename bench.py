@@ -310,6 +310,7 @@ def run_ours(args, world, rank, local_rank):
     pos += KE * B
 
     # 3) per-stage device times (events, no graph) for the roofline
+    info0 = eng.info()
     eng.set_profiling(True)
     stage_acc, attn_bytes, attn_flops, attn_ms, nA_list, eA_list = {}, [], [], [], [], []
     g = dims
@@ -323,7 +324,7 @@ def run_ours(args, world, rank, local_rank):
         # one launch recomputes A (pre-batch memory) and V_direct (post-batch memory)
         nA = int(r.affected) + (int(r.direct) if args.recompute == "affected" else 0)
         EA = int(r.entries_affected) + int(r.entries_direct)
-        attn_bytes.append(recompute_bytes(g, nA, EA))
+        attn_bytes.append(recompute_bytes(g, nA, EA, time_basis=bool(info0.get("bf16x3"))))
         attn_flops.append(recompute_flops(g, nA, EA))
         attn_ms.append(times["recompute"])
         nA_list.append(nA)
@@ -364,7 +365,7 @@ def run_ours(args, world, rank, local_rank):
         r_ev[1].record(stream)
         torch.cuda.synchronize()
         r_ms = _max_over_ranks(torch, dist, world, dev, float(r_ev[0].elapsed_time(r_ev[1])))
-        by = recompute_bytes(g, hi - lo, ents)
+        by = recompute_bytes(g, hi - lo, ents, time_basis=bool(info0.get("bf16x3")))
         rb = {"nodes": n_all, "nodes_per_rank": hi - lo, "ms": r_ms,
               "nodes_per_s": n_all / (r_ms / 1e3), "entries_rank0": ents,
               "algorithmic_bytes_rank0": by,
@@ -453,12 +454,15 @@ def run_ours(args, world, rank, local_rank):
         print(json.dumps(line), flush=True)
 
 
-def recompute_bytes(g, rows, entries):
+def recompute_bytes(g, rows, entries, time_basis=False):
     """Algorithmic HBM bytes of one recompute launch: per row
     the memory row, ring meta and the K*d output; per ring entry the K*d
-    frozen payload, d_e features and the 8 B timestamp."""
+    frozen payload, d_e features and the 8 B timestamp -- or, for the bf16x3
+    kernel, the slot's stored time basis (4 * round_up(d_t, 4) bytes) that
+    replaces the timestamp and the per-entry trigonometry."""
+    t_bytes = 4 * ((g.d_t + 3) // 4 * 4) if time_basis else 8
     return rows * (4 * g.d_s + 4 * g.layers * g.d + 16) + \
-        entries * (4 * g.layers * g.d + 4 * g.d_e + 8)
+        entries * (4 * g.layers * g.d + 4 * g.d_e + t_bytes)
 
 
 def recompute_flops(g, rows, entries):

@@ -146,6 +146,8 @@ typedef struct {
   double   *ring_t;     /* [cap_nodes][L] */
   float    *ring_pay;   /* [cap_nodes][K][L][ld_d] */
   float    *ring_feat;  /* [cap_nodes][L][ld_e] */
+  float    *ring_tb;    /* [cap_nodes][L][ld_t] time basis [cos w_f t, sin w_f t] of the slot's
+                           timestamp (ld_t = round_up(d_t,4)), written at insertion */
   uint32_t *amark, *dmark;                      /* [cap_nodes] batch stamps */
   int32_t  *nodecnt, *nodeadj, *nodefill, *nodeoff;  /* [cap_nodes] scratch */
   double   *drift_acc;  /* [cap_nodes] estimator, indexed by cumulative-set position */

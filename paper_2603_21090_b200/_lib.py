@@ -58,7 +58,7 @@ class Ctl(C.Structure):
 
 STATE_PTRS = (
     "mem", "last", "version", "h", "valid", "valid_at", "ring_cnt", "ring_head", "ring_ccnt",
-    "ring_nbr", "ring_eid", "ring_t", "ring_pay", "ring_feat", "amark", "dmark", "nodecnt",
+    "ring_nbr", "ring_eid", "ring_t", "ring_pay", "ring_feat", "ring_tb", "amark", "dmark", "nodecnt",
     "nodeadj", "nodefill", "nodeoff", "drift_acc", "drift_touched", "cum_mark", "cum_list",
     "cum_pos",
     "e_src", "e_dst", "e_t", "e_feat", "e_prev", "adj_head", "adj_deg", "gpow", "ctl", "scratch",

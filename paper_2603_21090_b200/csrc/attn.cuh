@@ -42,6 +42,7 @@ struct RingSrc {
   const int32_t *ring_cnt, *ring_head, *ring_ccnt;
   const double* ring_t;
   const float *ring_pay, *ring_feat;
+  const float* ring_tb;           // [node][L][ld_t] time basis of the slot timestamps
   // outputs / side effects
   const double* valid_at_ptr;   // device value (hdr->t_batch) or nullptr
   double valid_at_const;

@@ -267,9 +267,17 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
 }
 
 // Walk of one row (warp-per-row): softmax over its ring entries for both
-// heads; q~ read from, ubar written to the row buffer U (both heads, k_in each).
+// heads; q~ read from, ubar written to the row buffer U (both heads, kpad each).
 // Lane l owns key features [4l, 4l+4) of the payload (l < d/4), of the edge
-// features (l < d_e/4) and frequencies 2l, 2l+1 of the time encoding (l < d_t/4).
+// features and of the time encoding (frequencies 2l, 2l+1).
+//
+// Time encoding without per-entry trigonometry: phi(tref - t_e) is the
+// rotation by w tref of the slot's stored basis b_e = [cos w t_e, sin w t_e]
+// (ring_tb, written at insertion), so
+//   q~_phi . phi(tref - t_e) = [P | Q] . b_e,  P = qc cos a + qs sin a,
+//                                              Q = qc sin a - qs cos a  (a = w tref)
+// and sum_e alpha_e phi(tref - t_e) = R(a) sum_e alpha_e b_e: the row pays two
+// sincos per lane, each entry one LDG.128 of basis and plain FMAs.
 template <int KF>
 __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const RingSrc& rs,
                                             float* U, int node, int E, int hd, double tref, int l,
@@ -277,15 +285,20 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   constexpr int EC = A4_EC;
   const int kfo = w.kfo, kto = w.kto, kp = w.kpad;
   const bool lp = lane < kfo / 4, lf = KF && lane < (kto - kfo) / 4, lt = lane < (kp - kto) / 4;
-  const double* omega = w.omega;
   float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  // rotation of this row's reference time, frequencies 2l and 2l+1
+  float ca0 = 1.f, sa0 = 0.f, ca1 = 1.f, sa1 = 0.f;
+  if (lt && 2 * lane < g.half) phase_sincos(__ldg(w.omega + 2 * lane), tref, &sa0, &ca0);
+  if (lt && 2 * lane + 1 < g.half) phase_sincos(__ldg(w.omega + 2 * lane + 1), tref, &sa1, &ca1);
   float4 qp[2], qf[2], qt[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const float* Uh = U + h * kp;
     qp[h] = lp ? *reinterpret_cast<const float4*>(Uh + 4 * lane) : zero4;
     qf[h] = lf ? *reinterpret_cast<const float4*>(Uh + kfo + 4 * lane) : zero4;
-    qt[h] = lt ? *reinterpret_cast<const float4*>(Uh + kto + 4 * lane) : zero4;
+    float4 q = lt ? *reinterpret_cast<const float4*>(Uh + kto + 4 * lane) : zero4;
+    qt[h] = make_float4(q.x * ca0 + q.y * sa0, q.x * sa0 - q.y * ca0,
+                        q.z * ca1 + q.w * sa1, q.z * sa1 - q.w * ca1);
   }
   float2 up[2][2], uf[2][2], ut[2][2];
   float mx[2] = {-INFINITY, -INFINITY}, zs[2] = {0.f, 0.f};
@@ -293,48 +306,24 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   for (int h = 0; h < 2; ++h)
 #pragma unroll
     for (int c = 0; c < 2; ++c) up[h][c] = uf[h][c] = ut[h][c] = make_float2(0.f, 0.f);
-  double om0 = 0.0, om1 = 0.0;
-  const bool f0 = lt && 2 * lane < g.half, f1 = lt && 2 * lane + 1 < g.half;
-  if (f0) om0 = __ldg(omega + 2 * lane);
-  if (f1) om1 = __ldg(omega + 2 * lane + 1);
   const float* payb = rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d + 4 * lane;
   const float* ftb = rs.ring_feat + (int64_t)node * g.L * g.ld_e + 4 * lane;
-  const double* tb = rs.ring_t + (int64_t)node * g.L;
-  // ring timestamps are loaded one chunk ahead (the time encoding needs them first)
-  double tn[EC];
-#pragma unroll
-  for (int u = 0; u < EC; ++u) {
-    int slot = hd + u;
-    if (slot >= g.L) slot -= g.L;
-    tn[u] = u < E ? __ldg(tb + slot) : tref;
-  }
+  const float* tbb = rs.ring_tb + (int64_t)node * g.L * g.ld_t + 4 * lane;
   for (int e0 = 0; e0 < E; e0 += EC) {
-    float4 kp[EC], kf[EC];
-    double tv[EC];
+    float4 kp[EC], kf[EC], kt[EC];
 #pragma unroll
     for (int u = 0; u < EC; ++u) {
       const bool ev = e0 + u < E;
       int slot = hd + e0 + u;
       if (slot >= g.L) slot -= g.L;
       kp[u] = (ev && lp) ? __ldg(reinterpret_cast<const float4*>(payb + slot * g.ld_d)) : zero4;
+      kt[u] = (ev && lt) ? __ldg(reinterpret_cast<const float4*>(tbb + slot * g.ld_t)) : zero4;
       kf[u] = (KF && ev && lf) ? __ldg(reinterpret_cast<const float4*>(ftb + slot * g.ld_e)) : zero4;
-      tv[u] = tn[u];
-      const int en = e0 + EC + u;
-      int sn = hd + en;
-      if (sn >= g.L) sn -= g.L;
-      if (sn >= g.L) sn -= g.L;
-      tn[u] = en < E ? __ldg(tb + sn) : tref;
     }
     // per-lane partial logits, value index v = 2u + h
     float part[2 * EC];
-    float4 kt[EC];
 #pragma unroll
     for (int u = 0; u < EC; ++u) {
-      float s0 = 0.f, c0 = 0.f, s1 = 0.f, c1 = 0.f;
-      const double dt = tref - tv[u];
-      if (f0) phase_sincos(om0, dt, &s0, &c0);
-      if (f1) phase_sincos(om1, dt, &s1, &c1);
-      kt[u] = make_float4(c0, s0, c1, s1);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float2 a = fmul2(make_float2(qp[h].x, qp[h].y), make_float2(kp[u].x, kp[u].y));
@@ -423,9 +412,13 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
     if (lf)
       *reinterpret_cast<float4*>(Uh + kfo + 4 * lane) =
           make_float4(uf[h][0].x * inv, uf[h][0].y * inv, uf[h][1].x * inv, uf[h][1].y * inv);
-    if (lt)
+    if (lt) {  // rotate the accumulated basis back by w tref
+      const float uc0 = ut[h][0].x * inv, us0 = ut[h][0].y * inv;
+      const float uc1 = ut[h][1].x * inv, us1 = ut[h][1].y * inv;
       *reinterpret_cast<float4*>(Uh + kto + 4 * lane) =
-          make_float4(ut[h][0].x * inv, ut[h][0].y * inv, ut[h][1].x * inv, ut[h][1].y * inv);
+          make_float4(ca0 * uc0 + sa0 * us0, sa0 * uc0 - ca0 * us0, ca1 * uc1 + sa1 * us1,
+                      sa1 * uc1 - ca1 * us1);
+    }
   }
 }
 

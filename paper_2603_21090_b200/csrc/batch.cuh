@@ -27,7 +27,7 @@ struct StateView {
   int32_t *ring_cnt, *ring_head, *ring_ccnt, *ring_nbr;
   int64_t* ring_eid;
   double* ring_t;
-  float *ring_pay, *ring_feat;
+  float *ring_pay, *ring_feat, *ring_tb;
   uint32_t *amark, *dmark;
   int32_t *nodecnt, *nodeadj, *nodefill, *nodeoff;
   double* drift_acc;
@@ -209,7 +209,7 @@ __device__ __forceinline__ int64_t entry_index(int64_t m0, int r) {
 // freezing the opposite endpoint's pre-batch stack [s || 0, h_0..h_{K-2}]
 // as the payload; link the append-only store's per-node chains. One warp
 // per record.
-__global__ void k_ring(Geo g, StateView st, Scratch s) {
+__global__ void k_ring(Geo g, StateView st, Scratch s, const double* __restrict__ omega) {
   const BatchHdr* hd = s.hdr;
   const int64_t R = 2 * hd->B;
   const int lane = threadIdx.x & 31;
@@ -237,6 +237,14 @@ __global__ void k_ring(Geo g, StateView st, Scratch s) {
       st.ring_t[rs] = s.in_t[i];
     }
     for (int j = lane; j < g.d_e; j += 32) st.ring_feat[rs * g.ld_e + j] = s.in_feat[i * g.ld_e + j];
+    // time basis of the entry's timestamp: phi(tref - t) = rotation of [cos w t, sin w t] by
+    // w tref, so the recompute needs no per-entry trigonometry (attn4.cuh)
+    for (int f = lane; f < g.half; f += 32) {
+      float sv, cv;
+      phase_sincos(omega[f], s.in_t[i], &sv, &cv);
+      st.ring_tb[rs * g.ld_t + 2 * f] = cv;
+      st.ring_tb[rs * g.ld_t + 2 * f + 1] = sv;
+    }
     for (int l = 0; l < g.K; ++l) {
       float* dstp = st.ring_pay + (((int64_t)v * g.K + l) * g.L + slot) * g.ld_d;
       if (l == 0) {

@@ -350,6 +350,7 @@ int stgn_engine_bind(stgn_engine* e, const stgn_state* s) {
   v.valid_at = s->valid_at; v.ring_cnt = s->ring_cnt; v.ring_head = s->ring_head;
   v.ring_ccnt = s->ring_ccnt; v.ring_nbr = s->ring_nbr; v.ring_eid = s->ring_eid;
   v.ring_t = s->ring_t; v.ring_pay = s->ring_pay; v.ring_feat = s->ring_feat;
+  v.ring_tb = s->ring_tb;
   v.amark = s->amark; v.dmark = s->dmark; v.nodecnt = s->nodecnt; v.nodeadj = s->nodeadj;
   v.nodefill = s->nodefill; v.nodeoff = s->nodeoff; v.drift_acc = s->drift_acc;
   v.drift_touched = s->drift_touched; v.cum_mark = s->cum_mark; v.cum_list = s->cum_list;
@@ -372,6 +373,7 @@ static RingSrc ring_src(const stgn_engine* e) {
   r.mem = v.mem; r.h = v.h; r.valid = v.valid; r.valid_at = v.valid_at;
   r.ring_cnt = v.ring_cnt; r.ring_head = v.ring_head; r.ring_ccnt = v.ring_ccnt;
   r.ring_t = v.ring_t; r.ring_pay = v.ring_pay; r.ring_feat = v.ring_feat;
+  r.ring_tb = v.ring_tb;
   return r;
 }
 
@@ -414,7 +416,7 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   k_scan<<<1, 1024, 0, st>>>(g, v, s);
   k_place<<<g_rec, T, 0, st>>>(v, s);
   k_rank<<<g_rec, T, 0, st>>>(v, s);
-  k_ring<<<g_warp, T, 0, st>>>(g, v, s);
+  k_ring<<<g_warp, T, 0, st>>>(g, v, s, e->w.omega);
   k_dupdate<<<g_rec, T, 0, st>>>(g, v, s);
   n += 7;
   mark();

@@ -17,7 +17,7 @@ static inline __host__ __device__ int64_t cdiv(int64_t x, int64_t m) { return (x
 struct Geo {
   int d_s, d_e, d_t, d_x, d_m, d_k, H, K, L;
   int d, q_in, k_in, msg_in, HD;
-  int ld_s, ld_d, ld_e, ld_m;
+  int ld_s, ld_d, ld_e, ld_m, ld_t;
   int half;             // d_t / 2
   float inv_sqrt_dk;
   float phi_amp;        // sqrt(1/d_t)
@@ -36,6 +36,7 @@ static inline Geo make_geo(const stgn_dims& dm, int L) {
   g.ld_d = (int)round_up(g.d, 4);
   g.ld_e = (int)round_up(dm.d_e > 0 ? dm.d_e : 1, 4);
   g.ld_m = (int)round_up(dm.d_m, 4);
+  g.ld_t = (int)round_up(dm.d_t, 4);
   g.half = dm.d_t / 2;
   g.inv_sqrt_dk = (float)(1.0 / sqrt((double)dm.d_k));
   g.phi_amp = (float)sqrt(1.0 / (double)dm.d_t);

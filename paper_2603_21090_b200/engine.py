@@ -146,6 +146,7 @@ class _Tables:
         self.ring_t = z(N, g.L, dt=torch.float64)
         self.ring_pay = z(N, g.K, g.L, g.ld_d)
         self.ring_feat = z(N, g.L, g.ld_e)
+        self.ring_tb = z(N, g.L, g.ld_t)
         self.drift_acc = z(N, dt=torch.float64)
         self.drift_touched = z(N, dt=torch.int64)
         self.adj_head = z(N, dt=torch.int64, fill=-1)
@@ -156,7 +157,7 @@ class _Tables:
 
     def _node_names(self):
         return ("mem", "last", "version", "h", "valid", "valid_at", *self.NODE_I32, "ring_nbr",
-                "ring_eid", "ring_t", "ring_pay", "ring_feat", "drift_acc", "drift_touched",
+                "ring_eid", "ring_t", "ring_pay", "ring_feat", "ring_tb", "drift_acc", "drift_touched",
                 "adj_head", "adj_deg")
 
     def _alloc_edges(self, E):
@@ -438,6 +439,7 @@ class IncrementalEngine:
         self.K, self.L = dm.layers, cfg.fanout
         self.ld_s, self.ld_d = _rup(dm.d_s, 4), _rup(dm.d, 4)
         self.ld_e = _rup(max(dm.d_e, 1), 4)
+        self.ld_t = _rup(dm.d_t, 4)
         self.recompute = recompute
         # tcgen05 GEMMs where the TMEM plan fits: True = bf16x3 128-row kernel (H = 2,
         # k_in <= 224), else split-TF32; "tf32" = split-TF32 only; False = FFMA
