@@ -114,8 +114,11 @@ __device__ int g_a4_prof_n;
 #ifndef A4_PREFETCH
 #define A4_PREFETCH 0  // L2 prefetch of ring rows: 0 none, 1 one quadrant ahead, 2 whole tile per layer
 #endif
+#ifndef A4_HINTS
+#define A4_HINTS 0  // L2 eviction hints on the walk's loads
+#endif
 #ifndef A4_EC
-#define A4_EC 4  // ring entries per chunk of the walk (2 or 4)
+#define A4_EC 2  // ring entries per chunk of the walk (2 or 4)
 #endif
 
 // ---- bf16 helpers ----
@@ -212,40 +215,51 @@ __device__ __forceinline__ const uint16_t* a4_block(const Geo& g, const A4W& w, 
   return w.wo + (int64_t)l * *elems;
 }
 
-// L2 prefetch of layer l's ring rows (payload lines, timestamps) of tile rows [r0, r1)
+// L2 prefetch of layer l's ring rows of tile rows [r0, r1): the valid slots
+// of the payload block and of the time-basis block (each a contiguous run of
+// slots, split in two when the ring wraps). One warp per row, lanes over lines.
 __device__ __forceinline__ void a4_prefetch(const Geo& g, const RingSrc& rs, const int* nodes,
                                             const int* Es, const int* heads, int r0, int r1,
                                             int l, int tid) {
-  const int per_entry = 4 + (g.d_e ? 2 : 0);  // 400 B payload spans <= 4 lines (+ features)
-  const int per_row = g.L * per_entry + 1;
-  for (int x = tid; x < (r1 - r0) * per_row; x += A4_THREADS) {
-    const int i = r0 + x / per_row, r = x % per_row;
-    const int node = nodes[i];
-    if (node < 0) continue;
-    if (r == g.L * per_entry) {
-      prefetch_l2(rs.ring_t + (int64_t)node * g.L);
-      continue;
+  const int lane = tid & 31;
+  for (int i = r0 + (tid >> 5); i < r1; i += A4_WARPS) {
+    const int node = nodes[i], E = Es[i], hd = heads[i];
+    if (node < 0 || E <= 0) continue;
+    const int n1 = min(E, g.L - hd), n2 = E - n1;  // slots [hd, hd+n1) and [0, n2)
+    const char* pay = reinterpret_cast<const char*>(rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d);
+    const char* tb = reinterpret_cast<const char*>(rs.ring_tb + (int64_t)node * g.L * g.ld_t);
+    const int pb = g.ld_d * 4, tbb = g.ld_t * 4;
+#pragma unroll
+    for (int part = 0; part < 4; ++part) {
+      const char* base = (part < 2 ? pay : tb);
+      const int stride = part < 2 ? pb : tbb;
+      const int s0 = (part & 1) ? 0 : hd, ns = (part & 1) ? n2 : n1;
+      if (ns <= 0) continue;
+      const uintptr_t a0 = reinterpret_cast<uintptr_t>(base + (int64_t)s0 * stride);
+      const uintptr_t a1 = a0 + (uintptr_t)ns * stride - 1;
+      for (uintptr_t line = (a0 >> 7) + lane; line <= (a1 >> 7); line += 32)
+        prefetch_l2(reinterpret_cast<const void*>(line << 7));
     }
-    const int e = r / per_entry, q = r % per_entry;
-    if (e >= Es[i]) continue;
-    int slot = heads[i] + e;
-    if (slot >= g.L) slot -= g.L;
-    const char* base;
-    int nb, qq;
-    if (q < 4) {
-      base = reinterpret_cast<const char*>(rs.ring_pay + (((int64_t)node * g.K + l) * g.L + slot) * g.ld_d);
-      nb = g.d * 4;
-      qq = q;
-    } else {
-      base = reinterpret_cast<const char*>(rs.ring_feat + ((int64_t)node * g.L + slot) * g.ld_e);
-      nb = g.d_e * 4;
-      qq = q - 4;
-    }
-    const uintptr_t a0 = reinterpret_cast<uintptr_t>(base);
-    const uintptr_t line = (a0 >> 7) + (uintptr_t)qq;
-    if (line > ((a0 + (uintptr_t)nb - 1) >> 7)) continue;
-    prefetch_l2(reinterpret_cast<const void*>(line << 7));
   }
+}
+
+// 128-bit read-only load with an L2 eviction-policy hint (createpolicy)
+__device__ __forceinline__ float4 ldg_pol(const float* p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint64_t pol_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
@@ -309,6 +323,11 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   const float* payb = rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d + 4 * lane;
   const float* ftb = rs.ring_feat + (int64_t)node * g.L * g.ld_e + 4 * lane;
   const float* tbb = rs.ring_tb + (int64_t)node * g.L * g.ld_t + 4 * lane;
+#if A4_HINTS
+  // payload rows are read once per layer; the time basis again by the next layer
+  const uint64_t pol_pay = pol_evict_first();
+  const uint64_t pol_tb = l + 1 < g.K ? pol_evict_last() : pol_evict_first();
+#endif
   for (int e0 = 0; e0 < E; e0 += EC) {
     float4 kp[EC], kf[EC], kt[EC];
 #pragma unroll
@@ -316,8 +335,13 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
       const bool ev = e0 + u < E;
       int slot = hd + e0 + u;
       if (slot >= g.L) slot -= g.L;
+#if A4_HINTS
+      kp[u] = (ev && lp) ? ldg_pol(payb + slot * g.ld_d, pol_pay) : zero4;
+      kt[u] = (ev && lt) ? ldg_pol(tbb + slot * g.ld_t, pol_tb) : zero4;
+#else
       kp[u] = (ev && lp) ? __ldg(reinterpret_cast<const float4*>(payb + slot * g.ld_d)) : zero4;
       kt[u] = (ev && lt) ? __ldg(reinterpret_cast<const float4*>(tbb + slot * g.ld_t)) : zero4;
+#endif
       kf[u] = (KF && ev && lf) ? __ldg(reinterpret_cast<const float4*>(ftb + slot * g.ld_e)) : zero4;
     }
     // per-lane partial logits, value index v = 2u + h
