@@ -112,6 +112,7 @@ struct stgn_engine {
   cudaGraphExec_t graph = nullptr;
   bool graph_ok = true;   // capture allowed
   bool profiling = false;
+  bool fork_always = true;    // graph branches also when no conditional node is captured
   cudaEvent_t ev[16] = {};
   int64_t launches = 0;
   cudaStream_t aux = nullptr;   // captures the conditional rebuild body
@@ -119,6 +120,10 @@ struct stgn_engine {
   bool cond_used = false;       // rebuild block is a device-side conditional graph node
   cudaStream_t work = nullptr;  // the batch sequence / graph runs here
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  // graph branches: the memory update runs beside the BFS/records, the drift
+  // policy beside the recompute (captured fork/join, graph mode only)
+  cudaStream_t side[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork[2] = {nullptr, nullptr}, ev_join[2] = {nullptr, nullptr};
 };
 
 static void drop_graph(stgn_engine* e) {
@@ -275,6 +280,11 @@ int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engin
   if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&e->work, cudaStreamNonBlocking);
   if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming);
   if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e->ev_out, cudaEventDisableTiming);
+  for (int i = 0; i < 2 && ce == cudaSuccess; ++i) {
+    ce = cudaStreamCreateWithFlags(&e->side[i], cudaStreamNonBlocking);
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e->ev_fork[i], cudaEventDisableTiming);
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e->ev_join[i], cudaEventDisableTiming);
+  }
   if (ce != cudaSuccess) {
     stgn_set_error(__FILE__, __LINE__, ce);
     stgn_engine_destroy(e);
@@ -291,6 +301,11 @@ int stgn_engine_destroy(stgn_engine* e) {
   if (e->work) cudaStreamDestroy(e->work);
   if (e->ev_in) cudaEventDestroy(e->ev_in);
   if (e->ev_out) cudaEventDestroy(e->ev_out);
+  for (int i = 0; i < 2; ++i) {
+    if (e->side[i]) cudaStreamDestroy(e->side[i]);
+    if (e->ev_fork[i]) cudaEventDestroy(e->ev_fork[i]);
+    if (e->ev_join[i]) cudaEventDestroy(e->ev_join[i]);
+  }
   for (auto& ev : e->ev)
     if (ev) cudaEventDestroy(ev);
   if (e->h_in) cudaFreeHost(e->h_in);
@@ -392,6 +407,21 @@ static const char* kStageNames[] = {"group+ring", "affected_bfs", "change_record
                                     "rebuild", "cleanup"};
 #define NSTAGES 9
 
+static void launch_memory(const stgn_engine* e, cudaStream_t st) {
+  const Geo& g = e->g;
+  const int64_t R = 2 * (int64_t)e->cfg.max_batch;
+  k_memory<<<(int)std::min<int64_t>(cdiv(R, GRU_T), e->num_sms), MG_THREADS, e->mem_smem, st>>>(
+      g, e->sv, e->sc, e->w.wmsg, e->w.bmsg, e->w.omega, e->w.wgru, e->w.ugru, e->w.bgru,
+      e->cfg.aggregator, (int)round_up(g.d_m, 4), (int)round_up(g.d_s, 4), e->mem_wsm);
+}
+
+static void launch_drift(const stgn_engine* e, cudaStream_t st, cudaGraphConditionalHandle cond) {
+  k_drift_record<<<4 * e->num_sms, 256, 0, st>>>(e->sv, e->sc);
+  k_drift_decide<<<4 * e->num_sms, 256, 0, st>>>(e->sv, e->sc, e->cfg.rebuild,
+                                                 e->cfg.rebuild_interval, e->cfg.delta_max,
+                                                 e->cfg.alpha, cond);
+}
+
 // The whole per-batch sequence; every size is read on the device. With
 // profiling on, an event is recorded after every stage (no graph).
 static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalHandle cond) {
@@ -420,6 +450,18 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   k_dupdate<<<g_rec, T, 0, st>>>(g, v, s);
   n += 7;
   mark();
+  // Branch 0 (graph mode): the memory update needs only the ingest records and
+  // pre-batch memory; it writes scratch only, so it overlaps the BFS/records.
+  const bool fork = cond != 0 || e->fork_always;
+  cudaStream_t mst = st;
+  if (fork && !e->profiling) {
+    cudaEventRecord(e->ev_fork[0], st);
+    cudaStreamWaitEvent(e->side[0], e->ev_fork[0], 0);
+    mst = e->side[0];
+    launch_memory(e, mst);
+    n += 1;
+    cudaEventRecord(e->ev_join[0], mst);
+  }
   for (int hop = 1; hop <= g.K; ++hop) {
     k_hop<<<g_wide, T, 0, st>>>(g, v, s, hop);
     k_hop_fin<<<1, 32, 0, st>>>(s, hop);
@@ -433,13 +475,27 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   n += 1;
   mark();
   // stage 5 (memory update of V_direct) into mem_new; commits after the recompute
-  k_memory<<<(int)std::min<int64_t>(cdiv(R, GRU_T), e->num_sms), MG_THREADS, e->mem_smem, st>>>(
-      g, v, s, e->w.wmsg, e->w.bmsg, e->w.omega, e->w.wgru, e->w.ugru, e->w.bgru,
-      e->cfg.aggregator, (int)round_up(g.d_m, 4), (int)round_up(g.d_s, 4), e->mem_wsm);
-  n += 1;
+  if (mst == st) {
+    launch_memory(e, st);
+    n += 1;
+  } else {
+    cudaStreamWaitEvent(st, e->ev_join[0], 0);
+  }
   mark();
   // stages 2-4 and the post-commit refresh in one launch: rows = A (or V_direct)
   // with pre-batch memory, then V_direct with post-batch memory
+  // Branch 1 (graph mode): the drift estimators and the rebuild decision read
+  // the change records only, so they overlap the recompute; joined before the
+  // (conditional) rebuild block.
+  cudaStream_t dst_ = st;
+  if (fork && !e->profiling) {
+    cudaEventRecord(e->ev_fork[1], st);
+    cudaStreamWaitEvent(e->side[1], e->ev_fork[1], 0);
+    dst_ = e->side[1];
+    launch_drift(e, dst_, cond);
+    n += 2;
+    cudaEventRecord(e->ev_join[1], dst_);
+  }
   RingSrc rs = ring_src(e);
   rs.list = s.alist;
   rs.fused = 1;
@@ -462,10 +518,12 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   n += 1;
   mark();
   // drift + rebuild policy
-  k_drift_record<<<g_wide, T, 0, st>>>(v, s);
-  k_drift_decide<<<4 * e->num_sms, T, 0, st>>>(v, s, e->cfg.rebuild, e->cfg.rebuild_interval,
-                                           e->cfg.delta_max, e->cfg.alpha, cond);
-  n += 2;
+  if (dst_ == st) {
+    launch_drift(e, st, cond);
+    n += 2;
+  } else {
+    cudaStreamWaitEvent(st, e->ev_join[1], 0);
+  }
   mark();
   if (e->cfg.rebuild != STGN_REBUILD_NEVER) {
     // Inside a captured graph the rebuild block is the body of a conditional
