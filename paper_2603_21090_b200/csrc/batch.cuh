@@ -407,48 +407,61 @@ __global__ void k_records(Geo g, StateView st, Scratch s, int finite_window) {
 // (L <= 32): the window prefix is a ballot, the distinct direct
 // neighbours a __match_any_sync, so a node costs a few parallel loads.
 __global__ void k_records_warp(Geo g, StateView st, Scratch s, int finite_window) {
+  // floor(32 / L) affected nodes per warp, one L-lane segment each
   const int nA = s.res->nA, nD = s.res->nD;
   const uint32_t stamp = s.hdr->stamp;
   const double cutoff = s.hdr->cutoff;
   const int lane = threadIdx.x & 31;
+  const int S = 32 / g.L;
+  const int seg = lane / g.L, sl = lane - seg * g.L;  // segment, lane within it
+  const bool seg_live = seg < S;
+  const unsigned seg_mask = seg_live ? (((1u << g.L) - 1u) << (seg * g.L)) : 0u;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   unsigned long long hit = 0, miss = 0, changed = 0;
-  for (int64_t a64 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a64 < nA;
-       a64 += warps) {
-    const int a = (int)a64;
-    const int v = s.alist[a];
-    int added = 0, expired = 0, len, was_cached;
-    if (a < nD) {
-      const int kadj = st.nodeadj[v];
-      was_cached = s.d_wascached[a];
-      const int merged = kadj + s.d_baselen[a];
-      len = merged < g.L ? merged : g.L;
-      expired = was_cached ? (merged > g.L ? merged - g.L : 0) : 0;
-      added = kadj;
-    } else {
-      const int cc = st.ring_ccnt[v];
-      was_cached = cc >= 0;
-      len = was_cached ? cc : st.ring_cnt[v];
+  for (int64_t a0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * S; a0 < nA;
+       a0 += warps * S) {
+    const int a = (int)a0 + seg;
+    const bool live = seg_live && a < nA;
+    int v = 0, added = 0, expired = 0, len = 0, was_cached = 0;
+    if (live) {
+      v = s.alist[a];
+      if (a < nD) {
+        const int kadj = st.nodeadj[v];
+        was_cached = s.d_wascached[a];
+        const int merged = kadj + s.d_baselen[a];
+        len = merged < g.L ? merged : g.L;
+        expired = was_cached ? (merged > g.L ? merged - g.L : 0) : 0;
+        added = kadj;
+      } else {
+        const int cc = st.ring_ccnt[v];
+        was_cached = cc >= 0;
+        len = was_cached ? cc : st.ring_cnt[v];
+      }
     }
     int n_new = added < len ? added : len;
-    int slot = st.ring_head[v] + lane;
+    int slot = live ? st.ring_head[v] + sl : 0;
     if (slot >= g.L) slot -= g.L;
     const int64_t rs = (int64_t)v * g.L + slot;
-    const bool in_list = lane < len;
+    const bool in_list = live && sl < len;
     if (finite_window) {
-      const unsigned old = __ballot_sync(0xffffffffu, in_list && st.ring_t[rs] < cutoff);
+      const unsigned old = (__ballot_sync(0xffffffffu, in_list && st.ring_t[rs] < cutoff) & seg_mask) >>
+                           (seg_live ? seg * g.L : 0);
       const int keep = old ? __ffs(old) - 1 : len;
       expired += len - keep;
       len = keep;
       if (n_new > len) n_new = len;
     }
-    const bool cand = lane >= n_new && lane < len;
-    const int u = cand ? st.ring_nbr[rs] : -1 - lane;  // distinct dummies off-range
+    const bool cand = live && sl >= n_new && sl < len;
+    const int u = cand ? st.ring_nbr[rs] : -1;
     const bool dir = cand && st.dmark[u] == stamp;
-    const unsigned peers = __match_any_sync(0xffffffffu, u);
+    // ids are compared within the segment only: key = (node id, segment); lanes
+    // that hold no candidate get a key no other lane has
+    const unsigned long long key = cand ? (((unsigned long long)(unsigned)u << 8) | (unsigned)seg)
+                                        : (0xFFFFFFFF00000000ull | (unsigned)lane);
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
     const bool first = (__ffs(peers) - 1) == lane;  // lowest position holding this id
-    const int upd = __popc(__ballot_sync(0xffffffffu, dir && first));
-    if (lane == 0) {
+    const int upd = __popc(__ballot_sync(0xffffffffu, dir && first) & seg_mask);
+    if (live && sl == 0) {
       const int size = added + expired + upd;
       s.a_size[a] = size;
       s.a_len[a] = len;
