@@ -531,7 +531,9 @@ __global__ void k_predict_commit(Geo g, StateView st, Scratch s, const double* w
 // node's last message (its own side) enters. The new memory goes to
 // mem_new (committed after the recompute, which still reads pre-batch memory).
 #define MG_THREADS 512
+#ifndef GRU_T
 #define GRU_T 16
+#endif
 #define MEM_SREC 256  // records staged per pass
 __global__ void __launch_bounds__(MG_THREADS)
 k_memory(Geo g, StateView st, Scratch s, const float* wmsg2, const float* bmsg,

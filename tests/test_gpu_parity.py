@@ -199,3 +199,57 @@ def test_rebuild_nodes_api_matches_oracle(cuda):
     for v in range(n):
         assert [(e.nbr, e.edge_id) for e in eng.store.recent_upto(v, 100)] == \
                [(x[0], x[2]) for x in orc.store.recent(v, 100)]
+
+
+def _ap(pos, neg):
+    """Average precision of positives vs negatives (sklearn's definition)."""
+    from sklearn.metrics import average_precision_score
+    y = np.concatenate([np.ones(len(pos)), np.zeros(len(neg))])
+    return float(average_precision_score(y, np.concatenate([pos, neg])))
+
+
+@pytest.mark.parametrize("layers,d_e,seed", [(2, 0, 2), (1, 172, 0)], ids=["c4-widths", "c1-widths"])
+def test_link_prediction_ap_matches_reference(cuda, layers, d_e, seed):
+    """North-star AP bar: identical to the reference to 3 decimals. The
+    reference has no negative sampler, so the harness defines one
+    and applies it identically to both sides: for every positive edge
+    (src, dst) a seeded uniform negative destination `neg` is scored as
+    sigma(w_p [h_src ‖ h_neg] + b_p) with the prediction-time embedding of src
+    (S/engine.py:425-426) and the final-layer cache row of neg after the batch
+    (its prediction-time row when neg is itself a direct node)."""
+    from oracle.stgn_oracle import Oracle
+    from paper_2603_21090_b200.config import Dims, RunConfig
+    from paper_2603_21090_b200.engine import IncrementalEngine
+    from paper_2603_21090_b200.params import init_params
+    from paper_2603_21090_b200.streamio import generate_stream
+    n_nodes, B, m = 2000, 200, 8000
+    dims = Dims(d_s=100, d_e=d_e, d_t=100, d_m=100, d_k=50, heads=2, layers=layers)
+    cfg = RunConfig(dims=dims, batch_size=B, fanout=10, nodes=n_nodes)
+    params = init_params(0, dims)
+    stream = generate_stream(seed, n_nodes, m, attachment="preferential", d_e=d_e)
+    eng = IncrementalEngine(cfg, params)
+    orc = Oracle(cfg, params)
+    rng = np.random.default_rng(1234)
+    wp, bp = params.w_pred, params.b_pred
+    sig = lambda z: 1.0 / (1.0 + np.exp(-z))  # noqa: E731
+    pos_g, pos_o, neg_g, neg_o = [], [], [], []
+    for k, b in enumerate(batches(stream, B)):
+        p = eng.process_batch_arrays(b.src, b.dst, b.t, b.feat)
+        q = np.array(orc.process_batch(b.src, b.dst, b.t, b.feat))
+        if k < 5:  # warm-up batches (cold memory) are not scored
+            continue
+        neg = rng.integers(0, n_nodes, size=len(b.src))
+        pe_g, pe_o = eng.last_pred_embeddings, orc.last_pred_h
+        hK_g = eng.cache.h[:, -1]
+        for i, (s, v) in enumerate(zip(b.src, neg)):
+            hs_g, hs_o = pe_g[int(s)], pe_o[int(s)]
+            hv_g = pe_g[int(v)] if int(v) in pe_g else hK_g[int(v)]
+            hv_o = pe_o[int(v)] if int(v) in pe_o else orc.h[int(v), -1]
+            neg_g.append(sig(wp @ np.concatenate([hs_g, hv_g]) + bp))
+            neg_o.append(sig(wp @ np.concatenate([hs_o, hv_o]) + bp))
+        pos_g.extend(p.tolist())
+        pos_o.extend(q.tolist())
+    ap_g, ap_o = _ap(np.array(pos_g), np.array(neg_g)), _ap(np.array(pos_o), np.array(neg_o))
+    assert round(ap_g, 3) == round(ap_o, 3), (ap_g, ap_o)
+    assert abs(ap_g - ap_o) < 5e-4
+    assert max(abs(a - b) for a, b in zip(neg_g, neg_o)) <= PRED_ATOL
