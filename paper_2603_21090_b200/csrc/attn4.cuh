@@ -40,6 +40,41 @@
 
 #include "attn3.cuh"
 
+#ifndef A4_WARPS
+#define A4_WARPS 16
+#endif
+#define A4_THREADS (A4_WARPS * 32)
+// Phase timestamps of CTA 0 (debug builds with -DA4_PROF; read by stgn_debug_a4_prof).
+#ifdef A4_PROF
+__device__ unsigned long long g_a4_prof[8192];
+__device__ int g_a4_prof_n;
+#define A4_MARK(tag)                                                              \
+  do {                                                                           \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && g_a4_prof_n < 8190) {             \
+      unsigned long long t_;                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                      \
+      g_a4_prof[g_a4_prof_n++] = (t_ << 4) | (unsigned long long)(tag);           \
+    }                                                                            \
+  } while (0)
+#else
+#define A4_MARK(tag) do {} while (0)
+#endif
+#define A4_NCG (A4_WARPS / 4)  // warps per TMEM lane quadrant (column groups)
+#define A4_TMAX 128
+#ifndef A4_PREFETCH
+#define A4_PREFETCH 0  // L2 prefetch of ring rows: 0 none, 1 one quadrant ahead, 2 whole tile per layer
+#endif
+#ifndef A4_NST
+#define A4_NST 3  // cp.async stages (chunks in flight) per warp in the walk
+#endif
+#ifndef A4_HINTS
+#define A4_HINTS 0  // L2 eviction hints on the walk's loads
+#endif
+#ifndef A4_EC
+#define A4_EC 2  // ring entries per chunk of the walk (2 or 4)
+#endif
+
+
 struct A4W {
   const uint16_t *wq, *wk, *wv, *wo;  // packed bf16 B operands, hi block then lo block
   const float* bq;                    // [K][H*Kq]
@@ -49,6 +84,7 @@ struct A4W {
   int kfo, kto, kpad;                 // key layout [payload | features | time], each 4-padded
   int ldu;                            // row stride of the quadrant row buffer (floats)
   int wblk_bytes;                     // one staged weight block buffer (bytes)
+  int region_bytes;                   // weight buffers / walk stage area (shared)
 };
 
 static inline bool a4_plan(const Geo& g, A4W* w) {
@@ -75,6 +111,8 @@ static inline bool a4_plan(const Geo& g, A4W* w) {
   w->ldu = ldu;
   int mb = std::max(std::max(w->Nq * w->Kx, w->Nk * w->Kq), std::max(w->Nv * w->Ku, w->No * w->Kc));
   w->wblk_bytes = (mb * 2 * 2 + 1023) & ~1023;
+  const int stage_bytes = A4_WARPS * A4_NST * A4_EC * (g.d_e > 0 ? 3 : 2) * 32 * 16;
+  w->region_bytes = std::max(2 * w->wblk_bytes, (stage_bytes + 1023) & ~1023);
   return w->Nk <= 256 && w->Nq <= 256 && w->No <= 256 && w->Ku <= w->Nk &&
          w->Kx + w->Nq <= w->qt0 &&            // ACCQ alive while K_0 writes QT0
          w->qt1 + w->Nk <= w->qt0 &&           // QT1 / QT0 disjoint
@@ -87,39 +125,8 @@ static inline bool a4_plan(const Geo& g, A4W* w) {
 __host__ __device__ inline int64_t a4_blk_elems(int Np, int Kp) { return 2ll * Np * Kp; }
 
 static inline size_t attn4_smem_bytes(const A4W& w) {
-  return 1024 + 2 * (size_t)w.wblk_bytes + 2 * 32 * (size_t)w.ldu * 4;
+  return 1024 + (size_t)w.region_bytes + 2 * 32 * (size_t)w.ldu * 4;
 }
-
-#ifndef A4_WARPS
-#define A4_WARPS 16
-#endif
-#define A4_THREADS (A4_WARPS * 32)
-// Phase timestamps of CTA 0 (debug builds with -DA4_PROF; read by stgn_debug_a4_prof).
-#ifdef A4_PROF
-__device__ unsigned long long g_a4_prof[8192];
-__device__ int g_a4_prof_n;
-#define A4_MARK(tag)                                                              \
-  do {                                                                           \
-    if (blockIdx.x == 0 && threadIdx.x == 0 && g_a4_prof_n < 8190) {             \
-      unsigned long long t_;                                                      \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                      \
-      g_a4_prof[g_a4_prof_n++] = (t_ << 4) | (unsigned long long)(tag);           \
-    }                                                                            \
-  } while (0)
-#else
-#define A4_MARK(tag) do {} while (0)
-#endif
-#define A4_NCG (A4_WARPS / 4)  // warps per TMEM lane quadrant (column groups)
-#define A4_TMAX 128
-#ifndef A4_PREFETCH
-#define A4_PREFETCH 0  // L2 prefetch of ring rows: 0 none, 1 one quadrant ahead, 2 whole tile per layer
-#endif
-#ifndef A4_HINTS
-#define A4_HINTS 0  // L2 eviction hints on the walk's loads
-#endif
-#ifndef A4_EC
-#define A4_EC 2  // ring entries per chunk of the walk (2 or 4)
-#endif
 
 // ---- bf16 helpers ----
 __device__ __forceinline__ uint32_t bf16_bits(float x) {
@@ -243,6 +250,20 @@ __device__ __forceinline__ void a4_prefetch(const Geo& g, const RingSrc& rs, con
   }
 }
 
+// 16-byte global -> shared async copy (L1 bypass); src_bytes = 0 zero-fills
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 // 128-bit read-only load with an L2 eviction-policy hint (createpolicy)
 __device__ __forceinline__ float4 ldg_pol(const float* p, uint64_t pol) {
   float4 v;
@@ -295,7 +316,7 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
 template <int KF>
 __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const RingSrc& rs,
                                             float* U, int node, int E, int hd, double tref, int l,
-                                            int lane) {
+                                            int lane, float4* stg) {
   constexpr int EC = A4_EC;
   const int kfo = w.kfo, kto = w.kto, kp = w.kpad;
   const bool lp = lane < kfo / 4, lf = KF && lane < (kto - kfo) / 4, lt = lane < (kp - kto) / 4;
@@ -323,26 +344,44 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   const float* payb = rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d + 4 * lane;
   const float* ftb = rs.ring_feat + (int64_t)node * g.L * g.ld_e + 4 * lane;
   const float* tbb = rs.ring_tb + (int64_t)node * g.L * g.ld_t + 4 * lane;
-#if A4_HINTS
-  // payload rows are read once per layer; the time basis again by the next layer
-  const uint64_t pol_pay = pol_evict_first();
-  const uint64_t pol_tb = l + 1 < g.K ? pol_evict_last() : pol_evict_first();
-#endif
-  for (int e0 = 0; e0 < E; e0 += EC) {
-    float4 kp[EC], kf[EC], kt[EC];
+  // ring rows move through a per-warp cp.async pipeline of A4_NST chunks in
+  // shared memory (the weight buffers, idle during the walk): the loads of the
+  // next A4_NST - 1 chunks are in flight while one chunk is reduced
+  constexpr int NSEG = KF ? 3 : 2;
+  constexpr int NST = A4_NST;
+  const int nch = (E + EC - 1) / EC;
+  auto issue = [&](int c) {
+    if (c < nch) {
+      float4* sb = stg + (c % NST) * (EC * NSEG * 32) + lane;
 #pragma unroll
-    for (int u = 0; u < EC; ++u) {
-      const bool ev = e0 + u < E;
-      int slot = hd + e0 + u;
-      if (slot >= g.L) slot -= g.L;
-#if A4_HINTS
-      kp[u] = (ev && lp) ? ldg_pol(payb + slot * g.ld_d, pol_pay) : zero4;
-      kt[u] = (ev && lt) ? ldg_pol(tbb + slot * g.ld_t, pol_tb) : zero4;
-#else
-      kp[u] = (ev && lp) ? __ldg(reinterpret_cast<const float4*>(payb + slot * g.ld_d)) : zero4;
-      kt[u] = (ev && lt) ? __ldg(reinterpret_cast<const float4*>(tbb + slot * g.ld_t)) : zero4;
-#endif
-      kf[u] = (KF && ev && lf) ? __ldg(reinterpret_cast<const float4*>(ftb + slot * g.ld_e)) : zero4;
+      for (int u = 0; u < EC; ++u) {
+        const int e = c * EC + u;
+        const bool ev = e < E;
+        int slot = hd + e;
+        if (slot >= g.L) slot -= g.L;
+        if (!ev) slot = 0;
+        cp_async16(sb + (u * NSEG) * 32, payb + slot * g.ld_d, (ev && lp) ? 16 : 0);
+        cp_async16(sb + (u * NSEG + 1) * 32, tbb + slot * g.ld_t, (ev && lt) ? 16 : 0);
+        if (KF) cp_async16(sb + (u * NSEG + 2) * 32, ftb + slot * g.ld_e, (ev && lf) ? 16 : 0);
+      }
+    }
+    cp_async_commit();  // (possibly empty) group per chunk index keeps the counting uniform
+  };
+#pragma unroll
+  for (int c = 0; c < NST - 1; ++c) issue(c);
+  for (int c = 0; c < nch; ++c) {
+    const int e0 = c * EC;
+    issue(c + NST - 1);
+    cp_async_wait<NST - 1>();  // chunk c has landed (this lane's own copies)
+    float4 kp[EC], kf[EC], kt[EC];
+    {
+      const float4* sb = stg + (c % NST) * (EC * NSEG * 32) + lane;
+#pragma unroll
+      for (int u = 0; u < EC; ++u) {
+        kp[u] = sb[(u * NSEG) * 32];
+        kt[u] = sb[(u * NSEG + 1) * 32];
+        kf[u] = KF ? sb[(u * NSEG + 2) * 32] : zero4;
+      }
     }
     // per-lane partial logits, value index v = 2u + h
     float part[2 * EC];
@@ -454,7 +493,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint16_t* Wb0 = reinterpret_cast<uint16_t*>(sbase);
   uint16_t* Wb1 = reinterpret_cast<uint16_t*>(sbase + w.wblk_bytes);
-  float* Ub0 = reinterpret_cast<float*>(sbase + 2 * (size_t)w.wblk_bytes);
+  float* Ub0 = reinterpret_cast<float*>(sbase + (size_t)w.region_bytes);
   float* Ub1 = Ub0 + 32 * w.ldu;
   __shared__ int s_node[A4_TMAX], s_E[A4_TMAX], s_head[A4_TMAX], s_mode[A4_TMAX];
   __shared__ double s_tref[A4_TMAX];
@@ -504,6 +543,10 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
     stage(0);
     if (total_blocks > 1) stage(1);
   }
+  // the walk's per-warp cp.async stages live in the two weight buffers: V_0 and
+  // V_1 (blocks 3, 4 of a layer) are staged after the walk instead of during it
+  float4* stg_warp = reinterpret_cast<float4*>(sbase) + (size_t)warp * A4_NST * A4_EC * (KF ? 3 : 2) * 32;
+  auto deferred = [&](int64_t Gb) { const int j = (int)(Gb % 6); return j == 3 || j == 4; };
   int64_t G = 0;  // weight blocks consumed by this CTA
   int ub_use[2] = {0, 0};  // uses of each quadrant row buffer so far (mbarrier phases)
   // one GEMM: wait for its weights, MMA, wait for the MMA, refill the buffer.
@@ -516,7 +559,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
     }
     mbar_wait(&mbar, (uint32_t)(G & 1));
     tc_fence_after();
-    if (tid == 0 && G + 2 < total_blocks) stage(G + 2);
+    if (tid == 0 && G + 2 < total_blocks && !deferred(G + 2)) stage(G + 2);
     ++G;
   };
   auto cta_sync_tc = [&]() {
@@ -613,6 +656,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
       }
       // ---- walk, one 32-row quadrant at a time ----
       A4_MARK(2);
+      fence_async_smem();
       // Quadrant pipeline over two row buffers, ordered by mbarriers instead of
       // CTA barriers: the quadrant's own warps copy q~ out of TMEM (full), every
       // warp takes rows of the buffer from a shared counter and walks them
@@ -651,7 +695,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
           const int r = 32 * q + i;
           if (s_node[r] < 0) continue;
           a4_walk_row<KF>(g, w, rs, Ub + i * w.ldu, s_node[r], s_E[r], s_head[r], s_tref[r], l,
-                          lane);
+                          lane, stg_warp);
         }
         mbar_arrive(&qbar_done[b]);
         if (quad == q) {  // ubar rows -> TMEM (bf16 hi|lo) where q~ was
@@ -679,6 +723,11 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
       }
       A4_MARK(3);
       cta_sync_tc();
+      if (tid == 0) {  // the walk is done with the weight buffers: stage V_0, V_1
+        fence_async_smem();
+        stage(G);
+        stage(G + 1);
+      }
       // ---- c_h = ubar_h W_V,h ----
       gemm(w.qt0, w.Nv, w.Ku, 0);
       // every thread must observe the V_0 commit phase before V_1 can complete the
