@@ -64,6 +64,9 @@ __device__ int g_a4_prof_n;
 #ifndef A4_PREFETCH
 #define A4_PREFETCH 0  // L2 prefetch of ring rows: 0 none, 1 one quadrant ahead, 2 whole tile per layer
 #endif
+#ifndef A4_NUB
+#define A4_NUB 2  // quadrant row buffers (2: the next quadrant's q~ copy overlaps the walk)
+#endif
 #ifndef A4_NST
 #define A4_NST 3  // cp.async stages (chunks in flight) per warp in the walk
 #endif
@@ -125,7 +128,7 @@ static inline bool a4_plan(const Geo& g, A4W* w) {
 __host__ __device__ inline int64_t a4_blk_elems(int Np, int Kp) { return 2ll * Np * Kp; }
 
 static inline size_t attn4_smem_bytes(const A4W& w) {
-  return 1024 + (size_t)w.region_bytes + 2 * 32 * (size_t)w.ldu * 4;
+  return 1024 + (size_t)w.region_bytes + A4_NUB * 32 * (size_t)w.ldu * 4;
 }
 
 // ---- bf16 helpers ----
@@ -494,7 +497,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
   uint16_t* Wb0 = reinterpret_cast<uint16_t*>(sbase);
   uint16_t* Wb1 = reinterpret_cast<uint16_t*>(sbase + w.wblk_bytes);
   float* Ub0 = reinterpret_cast<float*>(sbase + (size_t)w.region_bytes);
-  float* Ub1 = Ub0 + 32 * w.ldu;
+  float* Ub1 = A4_NUB > 1 ? Ub0 + 32 * w.ldu : Ub0;
   __shared__ int s_node[A4_TMAX], s_E[A4_TMAX], s_head[A4_TMAX], s_mode[A4_TMAX];
   __shared__ double s_tref[A4_TMAX];
   __shared__ uint64_t mbar, wbar[2];
@@ -664,7 +667,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
       // frees the buffer for quadrant q + 2. A warp that finishes early moves
       // on to the next quadrant's rows.
       for (int q = 0; q < nq; ++q) {
-        const int b = q & 1;
+        const int b = A4_NUB > 1 ? (q & 1) : 0;
         float* Ub = b ? Ub1 : Ub0;
         const int nrows = min(32, T - 32 * q);
 #if A4_PREFETCH == 1
