@@ -455,14 +455,16 @@ def run_ours(args, world, rank, local_rank):
 
 
 def recompute_bytes(g, rows, entries, time_basis=False):
-    """Algorithmic HBM bytes of one recompute launch: per row
-    the memory row, ring meta and the K*d output; per ring entry the K*d
-    frozen payload, d_e features and the 8 B timestamp -- or, for the bf16x3
-    kernel, the slot's stored time basis (4 * round_up(d_t, 4) bytes) that
-    replaces the timestamp and the per-entry trigonometry."""
-    t_bytes = 4 * ((g.d_t + 3) // 4 * 4) if time_basis else 8
+    """Algorithmic HBM bytes of one recompute launch, SURVEY.md §8d's per-unit
+    figure: per row the query row (4 d_s), the K*d output and 16 B of ring
+    meta; per ring entry the K*d frozen payload, d_e features and 16 B
+    (timestamp + ids). `time_basis` is accepted for the record but does not
+    change the count: the bf16x3 kernel's stored time basis (4*d_t bytes per
+    entry and layer) is an implementation choice that trades bytes for
+    instructions, and shows up in `roofline.traffic` (ncu DRAM bytes), not here."""
+    del time_basis
     return rows * (4 * g.d_s + 4 * g.layers * g.d + 16) + \
-        entries * (4 * g.layers * g.d + 4 * g.d_e + t_bytes)
+        entries * (4 * g.layers * g.d + 4 * g.d_e + 16)
 
 
 def recompute_flops(g, rows, entries):

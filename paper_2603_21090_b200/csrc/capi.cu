@@ -446,12 +446,9 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   k_scan<<<1, 1024, 0, st>>>(g, v, s);
   k_place<<<g_rec, T, 0, st>>>(v, s);
   k_rank<<<g_rec, T, 0, st>>>(v, s);
-  k_ring<<<g_warp, T, 0, st>>>(g, v, s, e->w.omega);
-  k_dupdate<<<g_rec, T, 0, st>>>(g, v, s);
-  n += 7;
-  mark();
-  // Branch 0 (graph mode): the memory update needs only the ingest records and
-  // pre-batch memory; it writes scratch only, so it overlaps the BFS/records.
+  // Branch 0 (graph mode): the memory update needs only the grouped records
+  // (rec_s, doff) and pre-batch memory and writes scratch only, so it runs
+  // beside the ring insertion, the BFS and the change records.
   const bool fork = cond != 0 || e->fork_always;
   cudaStream_t mst = st;
   if (fork && !e->profiling) {
@@ -462,6 +459,10 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
     n += 1;
     cudaEventRecord(e->ev_join[0], mst);
   }
+  k_ring<<<g_warp, T, 0, st>>>(g, v, s, e->w.omega);
+  k_dupdate<<<g_rec, T, 0, st>>>(g, v, s);
+  n += 7;
+  mark();
   for (int hop = 1; hop <= g.K; ++hop) {
     k_hop<<<g_wide, T, 0, st>>>(g, v, s, hop);
     k_hop_fin<<<1, 32, 0, st>>>(s, hop);
