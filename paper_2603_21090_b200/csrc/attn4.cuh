@@ -259,6 +259,13 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_b
                "r"(src_bytes)
                : "memory");
 }
+__device__ __forceinline__ void cp_async16_pol(void* dst, const void* src, int src_bytes,
+                                               uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(src_bytes), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
@@ -352,6 +359,11 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   // next A4_NST - 1 chunks are in flight while one chunk is reduced
   constexpr int NSEG = KF ? 3 : 2;
   constexpr int NST = A4_NST;
+#if A4_HINTS
+  // a layer's payload rows are read once; the time basis again by the next layer
+  const uint64_t pol_pay = pol_evict_first();
+  const uint64_t pol_tb = l + 1 < g.K ? pol_evict_last() : pol_evict_first();
+#endif
   const int nch = (E + EC - 1) / EC;
   auto issue = [&](int c) {
     if (c < nch) {
@@ -363,8 +375,13 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
         int slot = hd + e;
         if (slot >= g.L) slot -= g.L;
         if (!ev) slot = 0;
+#if A4_HINTS
+        cp_async16_pol(sb + (u * NSEG) * 32, payb + slot * g.ld_d, (ev && lp) ? 16 : 0, pol_pay);
+        cp_async16_pol(sb + (u * NSEG + 1) * 32, tbb + slot * g.ld_t, (ev && lt) ? 16 : 0, pol_tb);
+#else
         cp_async16(sb + (u * NSEG) * 32, payb + slot * g.ld_d, (ev && lp) ? 16 : 0);
         cp_async16(sb + (u * NSEG + 1) * 32, tbb + slot * g.ld_t, (ev && lt) ? 16 : 0);
+#endif
         if (KF) cp_async16(sb + (u * NSEG + 2) * 32, ftb + slot * g.ld_e, (ev && lf) ? 16 : 0);
       }
     }

@@ -253,3 +253,26 @@ def test_link_prediction_ap_matches_reference(cuda, layers, d_e, seed):
     assert round(ap_g, 3) == round(ap_o, 3), (ap_g, ap_o)
     assert abs(ap_g - ap_o) < 5e-4
     assert max(abs(a - b) for a, b in zip(neg_g, neg_o)) <= PRED_ATOL
+
+
+@pytest.mark.parametrize("name", ["k2_last_adaptive", "k1_fixed_de0"])
+def test_full_recompute_engine_matches_reference_oracle(cuda, name):
+    """GPU OracleEngine (full recompute every batch) against the reference's
+    OracleEngine.apply_batch_full run on the same stream
+    (tests/golden/make_oracle_engine.py)."""
+    from paper_2603_21090_b200.full_engine import OracleEngine
+    z = load("engine_" + name)
+    zo = load("oracle_engine_" + name)
+    cfg, params, stream = case_setup(z)
+    eng = OracleEngine(cfg, params)
+    preds, snap = [], None
+    for b in batches(stream, cfg.batch_size):
+        p, snap = eng.apply_batch_arrays(b.src, b.dst, b.t, b.feat)
+        preds.extend(p.tolist())
+    assert np.max(np.abs(np.array(preds) - zo["preds"])) <= PRED_ATOL
+    n = zo["layers"].shape[0]
+    assert snap.layers.shape[0] >= n
+    assert_rows_close(snap.layers[:n].reshape(n, -1), zo["layers"].reshape(n, -1), "layers")
+    assert_rows_close(snap.memory[:n], zo["memory"], "memory")
+    np.testing.assert_array_equal(snap.last_interaction[:n], zo["last"])
+    assert snap.timestamp == float(zo["timestamp"][0])
