@@ -276,3 +276,35 @@ def test_full_recompute_engine_matches_reference_oracle(cuda, name):
     assert_rows_close(snap.memory[:n], zo["memory"], "memory")
     np.testing.assert_array_equal(snap.last_interaction[:n], zo["last"])
     assert snap.timestamp == float(zo["timestamp"][0])
+
+
+def test_streaming_engine_matches_synchronous(cuda):
+    """The pipelined StreamingEngine (uploads and score read-backs on their own
+    streams) yields exactly the scores and state of batch-by-batch
+    process_batch_arrays on the same stream."""
+    from paper_2603_21090_b200.engine import IncrementalEngine
+    from paper_2603_21090_b200.streaming import EdgeRing, StreamingEngine, form_batch
+    z = load("engine_k2_last_adaptive")
+    cfg, params, stream = case_setup(z)
+    sync = IncrementalEngine(cfg, params)
+    ref = []
+    for b in batches(stream, cfg.batch_size):
+        ref.append(sync.process_batch_arrays(b.src, b.dst, b.t, b.feat))
+    eng = IncrementalEngine(cfg, params)
+    se = StreamingEngine(eng, depth=3)
+    ring = EdgeRing(4 * cfg.batch_size, cfg.dims.d_e)
+    got, pos = [], 0
+    while pos < len(stream) or len(ring):
+        pos += ring.enqueue_arrays(stream.src[pos:], stream.dst[pos:], stream.t[pos:],
+                                   stream.feat[pos:])
+        b = form_batch(ring, cfg.batch_size)
+        if b is not None:
+            se.submit(b.src, b.dst, b.t, b.feat)
+        got.extend(se.results())
+    got.extend(se.drain())
+    assert [n for n, _ in got] == list(range(len(ref)))
+    for (_, p), q in zip(got, ref):
+        np.testing.assert_array_equal(p, q)
+    n = int(z["node_count"])
+    np.testing.assert_array_equal(eng.memory.states[:n], sync.memory.states[:n])
+    np.testing.assert_array_equal(eng.cache.h[:n], sync.cache.h[:n])
