@@ -508,6 +508,9 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
 template <int KF>
 __global__ void __launch_bounds__(A4_THREADS, 1)
 attn4_kernel(Geo g, A4W w, RingSrc rs) {
+#ifdef STGN_SKIP_RECOMPUTE  // timing experiments only: results are wrong
+  return;
+#endif
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sbase = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
