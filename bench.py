@@ -152,7 +152,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def cpu_reference(args, B_count, stream_edges=None):
+def cpu_reference(args, B_count, stream_edges=None, warmup=0):
     """Time the oracle port (the reference algorithm restated in float64,
     numba kernel like the reference's) on the same stream window: fast-
     forward the prefix exactly (topology, caches, memory, drift), then time
@@ -160,7 +160,7 @@ def cpu_reference(args, B_count, stream_edges=None):
     from oracle.stgn_oracle import Oracle, pipeline_many
     dims, cfg, params = workload(args)
     B = args.batch
-    st = stream_edges or make_stream(args, args.prefix + B_count * B, 0)
+    st = stream_edges or make_stream(args, args.prefix + (warmup + B_count) * B, 0)
     orc = Oracle(cfg, params)
     # compile the numba kernel outside the timed batches
     pipeline_many(np.zeros((1, 100)), np.array([0, 1]), np.zeros((1, 2, 100)), np.zeros((1, 0)),
@@ -169,17 +169,22 @@ def cpu_reference(args, B_count, stream_edges=None):
     for lo in range(0, args.prefix, B):
         orc.process_batch(st.src[lo:lo + B], st.dst[lo:lo + B], st.t[lo:lo + B],
                           st.feat[lo:lo + B], compute=False)
+    for k in range(warmup):  # untimed full batches (caches, numba) before the timed ones
+        lo = args.prefix + k * B
+        orc.process_batch(st.src[lo:lo + B], st.dst[lo:lo + B], st.t[lo:lo + B],
+                          st.feat[lo:lo + B])
     times = []
-    for k in range(B_count):
+    for k in range(warmup, warmup + B_count):
         lo = args.prefix + k * B
         t0 = time.perf_counter()
         orc.process_batch(st.src[lo:lo + B], st.dst[lo:lo + B], st.t[lo:lo + B],
                           st.feat[lo:lo + B])
         times.append(time.perf_counter() - t0)
     times = np.array(times)
-    sample = (f"oracle port (float64 numpy+numba, 1 thread) on batches {args.prefix // B}.."
-              f"{args.prefix // B + B_count - 1} of the same stream ({B_count} x {B} edges) "
-              f"after an exact fast-forward through the first {args.prefix} edges")
+    k0 = args.prefix // B + warmup
+    sample = (f"oracle port (float64 numpy+numba, 1 thread) on batches {k0}..{k0 + B_count - 1} "
+              f"of the same stream ({B_count} x {B} edges) after an exact fast-forward through "
+              f"the first {args.prefix} edges and {warmup} untimed batches")
     return B_count * B / float(times.sum()), times, sample
 
 
@@ -187,12 +192,15 @@ def run_reference(args, world, rank):
     if rank != 0:
         return
     dims, cfg, params = workload(args)
-    steps = max(1, args.cpu_batches)
-    value, times, sample = cpu_reference(args, steps)
+    # one step = one 600-edge batch of the reference algorithm on the host (~0.3-2 s each);
+    # capped so the whole run stays within a few minutes
+    steps = max(1, min(args.steps, 30))
+    warm = max(0, min(args.warmup, 3))
+    value, times, sample = cpu_reference(args, steps, warmup=warm)
     ms = float(times.mean() * 1e3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
-        "warmup": 0, "ms_per_step": ms, "p50_ms": float(np.percentile(times, 50) * 1e3),
+        "warmup": warm, "ms_per_step": ms, "p50_ms": float(np.percentile(times, 50) * 1e3),
         "p99_ms": float(np.percentile(times, 99) * 1e3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_json(args, 1), "impl": "reference",
