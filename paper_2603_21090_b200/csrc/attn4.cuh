@@ -70,6 +70,12 @@ __device__ int g_a4_prof_n;
 #ifndef A4_NST
 #define A4_NST 3  // cp.async stages (chunks in flight) per warp in the walk
 #endif
+#ifndef A4_STATIC
+#define A4_STATIC 0  // static row assignment with one cp.async stream across rows and quadrants
+#endif
+#if A4_STATIC && A4_WARPS != 16
+#error "A4_STATIC assigns two rows of every 32-row quadrant to each of 16 warps"
+#endif
 #ifndef A4_HINTS
 #define A4_HINTS 0  // L2 eviction hints on the walk's loads
 #endif
@@ -303,6 +309,56 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
   return d;
 }
 
+// Per-warp cp.async issue stream over the ring chunks of the warp's rows of a
+// tile-layer (static assignment: rows 32q + warp and 32q + warp + 16 of every
+// quadrant q, in order). The stream runs A4_NST - 1 chunks ahead of the walk,
+// across row and quadrant boundaries (ring rows do not depend on the quadrant
+// row buffers), so a row's first chunks are in flight before it starts.
+struct A4Iss {
+  int k;     // position in the warp's row sequence
+  int c;     // next chunk of that row
+  int kiss;  // groups committed
+  int nseq;  // rows in the sequence (2 per quadrant)
+};
+template <int KF>
+__device__ __forceinline__ void a4_issue_next(const Geo& g, const A4W& w, const RingSrc& rs,
+                                              A4Iss& is, const int* s_node, const int* s_E,
+                                              const int* s_head, int T, int warp, int l, int lane,
+                                              float4* stg) {
+  constexpr int EC = A4_EC, NSEG = KF ? 3 : 2, NST = A4_NST;
+  int r = -1, nch = 0;
+  while (is.k < is.nseq) {
+    r = 32 * (is.k >> 1) + warp + 16 * (is.k & 1);
+    nch = (r < T && s_node[r] >= 0) ? (s_E[r] + EC - 1) / EC : 0;
+    if (is.c < nch) break;
+    ++is.k;
+    is.c = 0;
+  }
+  if (is.k < is.nseq) {
+    const int node = s_node[r], E = s_E[r], hd = s_head[r];
+    const bool lp = lane < w.kfo / 4, lf = KF && lane < (w.kto - w.kfo) / 4,
+               lt = lane < (w.kpad - w.kto) / 4;
+    const float* payb = rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d + 4 * lane;
+    const float* ftb = rs.ring_feat + (int64_t)node * g.L * g.ld_e + 4 * lane;
+    const float* tbb = rs.ring_tb + (int64_t)node * g.L * g.ld_t + 4 * lane;
+    float4* sb = stg + (is.kiss % NST) * (EC * NSEG * 32) + lane;
+#pragma unroll
+    for (int u = 0; u < EC; ++u) {
+      const int e = is.c * EC + u;
+      const bool ev = e < E;
+      int slot = hd + e;
+      if (slot >= g.L) slot -= g.L;
+      if (!ev) slot = 0;
+      cp_async16(sb + (u * NSEG) * 32, payb + slot * g.ld_d, (ev && lp) ? 16 : 0);
+      cp_async16(sb + (u * NSEG + 1) * 32, tbb + slot * g.ld_t, (ev && lt) ? 16 : 0);
+      if (KF) cp_async16(sb + (u * NSEG + 2) * 32, ftb + slot * g.ld_e, (ev && lf) ? 16 : 0);
+    }
+    ++is.c;
+  }
+  cp_async_commit();
+  ++is.kiss;
+}
+
 // Walk of one row (warp-per-row): softmax over its ring entries for both
 // heads; q~ read from, ubar written to the row buffer U (both heads, kpad each).
 // Lane l owns key features [4l, 4l+4) of the payload (l < d/4), of the edge
@@ -315,10 +371,11 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
 //                                              Q = qc sin a - qs cos a  (a = w tref)
 // and sum_e alpha_e phi(tref - t_e) = R(a) sum_e alpha_e b_e: the row pays two
 // sincos per lane, each entry one LDG.128 of basis and plain FMAs.
-template <int KF>
+template <int KF, typename IssueFn>
 __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const RingSrc& rs,
                                             float* U, int node, int E, int hd, double tref, int l,
-                                            int lane, float4* stg) {
+                                            int lane, float4* stg, IssueFn&& ext_issue,
+                                            int* kcons) {
   constexpr int EC = A4_EC;
   const int kfo = w.kfo, kto = w.kto, kp = w.kpad;
   const bool lp = lane < kfo / 4, lf = KF && lane < (kto - kfo) / 4, lt = lane < (kp - kto) / 4;
@@ -379,15 +436,23 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
     }
     cp_async_commit();  // (possibly empty) group per chunk index keeps the counting uniform
   };
+  if (!kcons) {
 #pragma unroll
-  for (int c = 0; c < NST - 1; ++c) issue(c);
+    for (int c = 0; c < NST - 1; ++c) issue(c);
+  }
   for (int c = 0; c < nch; ++c) {
     const int e0 = c * EC;
-    issue(c + NST - 1);
+    int slot_c = c % NST;
+    if (kcons) {  // the warp-wide stream issues (and runs ahead of) this row's chunks
+      ext_issue();
+      slot_c = (*kcons)++ % NST;
+    } else {
+      issue(c + NST - 1);
+    }
     cp_async_wait<NST - 1>();  // chunk c has landed (this lane's own copies)
     float4 kp[EC], kf[EC], kt[EC];
     {
-      const float4* sb = stg + (c % NST) * (EC * NSEG * 32) + lane;
+      const float4* sb = stg + slot_c * (EC * NSEG * 32) + lane;
 #pragma unroll
       for (int u = 0; u < EC; ++u) {
         kp[u] = sb[(u * NSEG) * 32];
@@ -672,6 +737,15 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
       // ---- walk, one 32-row quadrant at a time ----
       A4_MARK(2);
       fence_async_smem();
+#if A4_STATIC
+      A4Iss iss{0, 0, 0, 2 * nq};
+      int kcons = 0;
+      auto issue_next = [&]() {
+        a4_issue_next<KF>(g, w, rs, iss, s_node, s_E, s_head, T, warp, l, lane, stg_warp);
+      };
+#pragma unroll
+      for (int p0 = 0; p0 < A4_NST - 1; ++p0) issue_next();
+#endif
       // Quadrant pipeline over two row buffers, ordered by mbarriers instead of
       // CTA barriers: the quadrant's own warps copy q~ out of TMEM (full), every
       // warp takes rows of the buffer from a shared counter and walks them
@@ -702,6 +776,15 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
           mbar_arrive(&qbar_full[b]);
         }
         mbar_wait(&qbar_full[b], (uint32_t)(ub_use[b] & 1));
+#if A4_STATIC
+        for (int hh = 0; hh < 2; ++hh) {  // this warp's rows of the quadrant
+          const int i = warp + 16 * hh;
+          const int r = 32 * q + i;
+          if (i >= nrows || s_node[r] < 0) continue;
+          a4_walk_row<KF>(g, w, rs, Ub + i * w.ldu, s_node[r], s_E[r], s_head[r], s_tref[r], l,
+                          lane, stg_warp, issue_next, &kcons);
+        }
+#else
         for (;;) {
           int i = 0;
           if (lane == 0) i = atomicAdd(&qctr[b], 1);
@@ -710,8 +793,9 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
           const int r = 32 * q + i;
           if (s_node[r] < 0) continue;
           a4_walk_row<KF>(g, w, rs, Ub + i * w.ldu, s_node[r], s_E[r], s_head[r], s_tref[r], l,
-                          lane, stg_warp);
+                          lane, stg_warp, [] {}, nullptr);
         }
+#endif
         mbar_arrive(&qbar_done[b]);
         if (quad == q) {  // ubar rows -> TMEM (bf16 hi|lo) where q~ was
           mbar_wait(&qbar_done[b], (uint32_t)(ub_use[b] & 1));
