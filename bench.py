@@ -465,6 +465,12 @@ def run_ours(args, world, rank, local_rank):
             "window": win,
             "sweep": sweep_out,
             "full_rebuild": rb,
+            # the paper's "index refresh" comparison: one full recompute of
+            # every node (the TGL-style / OracleEngine baseline) vs one incremental batch
+            "refresh_vs_full_recompute": None if rb is None else {
+                "full_recompute_ms": rb["ms"], "incremental_ms": total_ms / K,
+                "speedup": rb["ms"] / (total_ms / K),
+                "direct_scope_speedup": (rb["ms"] / direct["p50_ms"]) if direct else None},
             "direct_scope": direct,
             "setup_s": {"generate": t_gen, "fast_forward": t_ff},
         }
