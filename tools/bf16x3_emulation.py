@@ -5,7 +5,12 @@ the float64 pipeline (row-relative embedding error, prediction error).
 
     python tools/bf16x3_emulation.py
 """
-import os; sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle.stgn_oracle import Oracle, pipeline_many
 import oracle.stgn_oracle as so
 from paper_2603_21090_b200.config import Dims, RunConfig
