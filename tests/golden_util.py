@@ -46,3 +46,16 @@ def case_setup(z):
 def batches(stream: EdgeArrays, B: int):
     for lo in range(0, len(stream), B):
         yield stream.slice(lo, min(lo + B, len(stream)))
+
+
+def random_params(seed, dims):
+    """init_params with random biases, as the reference's tests/conftest.py:18-26
+    and tests/golden/make_golden.py:random_params (same draw order)."""
+    from paper_2603_21090_b200.params import init_params
+    p = init_params(seed, dims)
+    rng = np.random.default_rng(seed + 1)
+    for name, t in p.tensors().items():
+        if name.startswith("b_") and name != "b_pred":
+            t[...] = rng.standard_normal(t.shape)
+    p.b_pred = float(rng.standard_normal())
+    return p

@@ -308,3 +308,29 @@ def test_streaming_engine_matches_synchronous(cuda):
     n = int(z["node_count"])
     np.testing.assert_array_equal(eng.memory.states[:n], sync.memory.states[:n])
     np.testing.assert_array_equal(eng.cache.h[:n], sync.cache.h[:n])
+
+
+@pytest.mark.parametrize("name,layers,seed", [("k1", 1, 3), ("k2", 2, 5)])
+def test_staleness_harness_matches_reference(cuda, name, layers, seed):
+    """B=1 sequential replay (full-recompute engine) and the incremental engine
+    at batch sizes 1/4/16/50, against the reference harness's own outputs
+    (tests/golden/make_staleness.py): per-edge predictions within the
+    prediction tolerance, the staleness reports within twice that."""
+    from paper_2603_21090_b200.batcher import compare_sequential_vs_batched, replay_sequential
+    from paper_2603_21090_b200.config import Dims, RunConfig
+    from paper_2603_21090_b200.params import ModelParameters  # noqa: F401
+    from paper_2603_21090_b200.streamio import generate_stream
+    from golden_util import random_params
+    z = load("staleness_" + name)
+    dims = Dims(d_s=6, d_e=3, d_t=6, d_m=5, d_k=4, heads=2, layers=layers)
+    cfg = RunConfig(dims=dims, batch_size=8, fanout=4, nodes=30)
+    params = random_params(seed, dims)
+    stream = generate_stream(seed, 30, 200, attachment="preferential", d_e=3)
+    seq, _ = replay_sequential(stream, cfg, params)
+    assert np.max(np.abs(np.array(seq) - z["seq"])) <= PRED_ATOL
+    reports, slope = compare_sequential_vs_batched(stream, list(z["batch_sizes"]), cfg, params,
+                                                   seq_preds=seq)
+    for r, mx, mn in zip(reports, z["max_dev"], z["mean_dev"]):
+        assert abs(r.max_dev - mx) <= 2 * PRED_ATOL and abs(r.mean_dev - mn) <= 2 * PRED_ATOL
+    assert reports[0].max_dev <= PRED_ATOL  # B = 1 is the sequential replay
+    assert abs(slope - float(z["slope"][0])) <= 1e-6
