@@ -244,7 +244,7 @@ def run_ours(args, world, rank, local_rank):
     dev = torch.device("cuda", local_rank)
     dims, cfg, params = workload(args)
     B, W, K = args.batch, args.warmup, args.steps
-    KE = args.e2e_steps if args.e2e_steps is not None else min(K, 100)
+    KE = args.e2e_steps if args.e2e_steps is not None else K
     P = args.profile_batches
     sweep = [int(x) for x in args.sweep.split(",") if x] if args.sweep else []
     SW = args.sweep_steps

@@ -107,7 +107,7 @@ typedef struct {
    * ((n/8)*(Kp/8) + k/8)*64 + (n%8)*8 + k%8), hi block then lo block
    * (lo = bf16(w - hi)); Kp = round_up(K,16), Np = round_up(N,16), Kq = round_up(d_k,16):
    *   t4q [K]    N = H*Kq (head h at rows h*Kq), K = d            (w_q rows 0..d-1)
-   *   t4k [K][H] N = k_in, K = d_k   w_k / sqrt(d_k), time-encoding rows * sqrt(1/d_t)
+   *   t4k [K][H] N = k_in, K = d_k   w_k * log2(e) / sqrt(d_k), time-encoding rows * sqrt(1/d_t)
    *   t4v [K][H] N = d_k,  K = k_in  w_v^T, time-encoding columns * sqrt(1/d_t)
    *   t4o [K]    N = d,    K = H*Kq (head h at h*Kq)               w_o^T
    *   t4bq [K][H][Kq] float   phi(0) . w_q[l, h, d:, :] (zero padded) */

@@ -291,6 +291,12 @@ __device__ __forceinline__ uint64_t pol_evict_last() {
   return p;
 }
 
+__device__ __forceinline__ float ex2f(float x) {  // 2^x on the SFU (ex2(-inf) = 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   float2 d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;"
@@ -414,9 +420,10 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   const uint64_t pol_tb = l + 1 < g.K ? pol_evict_last() : pol_evict_first();
 #endif
   const int nch = (E + EC - 1) / EC;
+  int iss_slot = 0, con_slot = 0;  // stage slots of the next issue / the next consumed chunk
   auto issue = [&](int c) {
     if (c < nch) {
-      float4* sb = stg + (c % NST) * (EC * NSEG * 32) + lane;
+      float4* sb = stg + iss_slot * (EC * NSEG * 32) + lane;
 #pragma unroll
       for (int u = 0; u < EC; ++u) {
         const int e = c * EC + u;
@@ -435,6 +442,7 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
       }
     }
     cp_async_commit();  // (possibly empty) group per chunk index keeps the counting uniform
+    if (++iss_slot == NST) iss_slot = 0;
   };
   if (!kcons) {
 #pragma unroll
@@ -442,7 +450,8 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   }
   for (int c = 0; c < nch; ++c) {
     const int e0 = c * EC;
-    int slot_c = c % NST;
+    int slot_c = con_slot;
+    if (++con_slot == NST) con_slot = 0;
     if (kcons) {  // the warp-wide stream issues (and runs ahead of) this row's chunks
       ext_issue();
       slot_c = (*kcons)++ % NST;
@@ -515,7 +524,7 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
       for (int u = 0; u < EC; ++u)
         if (e0 + u < E) cm = fmaxf(cm, lg[2 * u + h]);
       const float nm = fmaxf(mx[h], cm);
-      const float sc = __expf(mx[h] - nm);
+      const float sc = ex2f(mx[h] - nm);  // logits are in log2 units (W_K carries log2 e)
       const float2 sc2 = make_float2(sc, sc);
       zs[h] *= sc;
 #pragma unroll
@@ -526,7 +535,7 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
       }
 #pragma unroll
       for (int u = 0; u < EC; ++u) {
-        const float p = (e0 + u < E) ? __expf(lg[2 * u + h] - nm) : 0.f;
+        const float p = (e0 + u < E) ? ex2f(lg[2 * u + h] - nm) : 0.f;
         const float2 p2 = make_float2(p, p);
         zs[h] += p;
         up[h][0] = ffma2(p2, make_float2(kp[u].x, kp[u].y), up[h][0]);

@@ -551,8 +551,9 @@ class IncrementalEngine:
 
     def _pack_bf16x3(self):
         """Operands of the bf16x3 recompute kernel (stgn.h t4*): the folded
-        per-head weights with 1/sqrt(d_k) in W_K and the time-encoding
-        amplitude sqrt(1/d_t) in the time rows of W_K and W_V."""
+        per-head weights with log2(e)/sqrt(d_k) in W_K (the kernel's softmax
+        is base 2) and the time-encoding amplitude sqrt(1/d_t) in the time rows
+        of W_K and W_V."""
         p, dm = self.params, self.dims
         K, H, d_k, d = dm.layers, dm.heads, dm.d_k, dm.d
         Kq = _rup(d_k, 16)
@@ -575,7 +576,8 @@ class IncrementalEngine:
                                r4(d) + r4(dm.d_e) + np.arange(dm.d_t)])
         kpad = r4(d) + r4(dm.d_e) + r4(dm.d_t)
         wk = np.zeros((K, H, kpad, d_k))      # [n][k]
-        wk[:, :, kmap, :] = p.w_k / np.sqrt(d_k)
+        # log2(e) folded in: the kernel's softmax runs on exp2 (one MUFU.EX2 per weight)
+        wk[:, :, kmap, :] = p.w_k * (np.log2(np.e) / np.sqrt(d_k))
         wk[:, :, kmap[t0:], :] *= amp
         wv = np.zeros((K, H, d_k, kpad))      # [n][k]
         wv[:, :, :, kmap] = np.transpose(p.w_v, (0, 1, 3, 2))
