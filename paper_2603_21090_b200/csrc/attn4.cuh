@@ -517,12 +517,15 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
 #pragma unroll
       for (int v = 0; v < 2 * EC; ++v) lg[v] = __shfl_sync(0xffffffffu, part[0], stride * v);
     }
+    // entries past E (zero-filled stages) get logit -inf: out of the max, weight 0
+#pragma unroll
+    for (int u = 1; u < EC; ++u)
+      if (e0 + u >= E) lg[2 * u] = lg[2 * u + 1] = -INFINITY;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      float cm = -INFINITY;
+      float cm = lg[h];
 #pragma unroll
-      for (int u = 0; u < EC; ++u)
-        if (e0 + u < E) cm = fmaxf(cm, lg[2 * u + h]);
+      for (int u = 1; u < EC; ++u) cm = fmaxf(cm, lg[2 * u + h]);
       const float nm = fmaxf(mx[h], cm);
       const float sc = ex2f(mx[h] - nm);  // logits are in log2 units (W_K carries log2 e)
       const float2 sc2 = make_float2(sc, sc);
@@ -535,7 +538,7 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
       }
 #pragma unroll
       for (int u = 0; u < EC; ++u) {
-        const float p = (e0 + u < E) ? ex2f(lg[2 * u + h] - nm) : 0.f;
+        const float p = ex2f(lg[2 * u + h] - nm);
         const float2 p2 = make_float2(p, p);
         zs[h] += p;
         up[h][0] = ffma2(p2, make_float2(kp[u].x, kp[u].y), up[h][0]);
