@@ -291,6 +291,18 @@ int stgn_generate_stream(const uint64_t* rng_state, int64_t n, int64_t m, int32_
  * count copied (0 unless the library was built with -DA4_PROF); resets. */
 int stgn_debug_a4_prof(uint64_t* out, int cap);
 
+/*
+ * Native reader of the edge-stream CSV format (S/streamio.py:15-79). Returns
+ * the edge count in *m_out and d_e in *d_e_out; with cap >= *m_out and
+ * buffers (src, dst int64; t float64; feat float64 [m][d_e]) it also fills
+ * them, stably re-sorted by t when sort != 0. Any line it cannot parse as
+ * plain decimal fields, a negative id, or a decreasing timestamp without sort
+ * returns STGN_ERR_INVALID (*bad_line = the line, or -1): the Python shim then
+ * re-reads the file with the reference's parser for the exact error.
+ */
+int stgn_read_stream(const char* path, int32_t sort, int64_t cap, int64_t* m_out, int64_t* d_e_out,
+                     int64_t* src, int64_t* dst, double* t, double* feat, int64_t* bad_line);
+
 /* Library version string and the sm architecture it was built for. */
 const char* stgn_version(void);
 

@@ -18,6 +18,9 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <algorithm>
+#include <cstring>
+
 #include "stgn.h"
 
 namespace {
@@ -134,6 +137,166 @@ extern "C" int stgn_generate_stream(const uint64_t* rng_state, int64_t n, int64_
     rng_state_out[3] = (uint64_t)g.inc;
     rng_state_out[4] = (uint64_t)g.has32;
     rng_state_out[5] = g.u32;
+  }
+  return STGN_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Native reader of the edge-stream CSV format (S/streamio.py:15-79):
+//   "# streamtgn-edges v1 d_e=<k>" then "src,dst,t[,f_1..f_k]" per line.
+// A fast path only: any line it cannot take as plain decimal fields (or any
+// format error) returns STGN_ERR_INVALID with the line number, and the Python
+// shim re-reads the file with the reference-faithful parser, so error messages
+// and every accepted spelling stay exactly the reference's.
+#include <cctype>
+#include <cerrno>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+namespace {
+
+struct CsvFile {
+  std::vector<char> buf;
+  bool load(const char* path) {
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return false;
+    std::fseek(f, 0, SEEK_END);
+    const long n = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    buf.resize((size_t)(n > 0 ? n : 0) + 1);
+    const size_t got = n > 0 ? std::fread(buf.data(), 1, (size_t)n, f) : 0;
+    std::fclose(f);
+    buf[got] = '\0';
+    buf.resize(got + 1);
+    return true;
+  }
+};
+
+const char* skip_ws(const char* p, const char* e) {
+  while (p < e && (*p == ' ' || *p == '\t' || *p == '\r')) ++p;
+  return p;
+}
+
+// one field [p, e): strict integer / float, surrounding blanks allowed
+bool field_i64(const char* p, const char* e, int64_t* out) {
+  p = skip_ws(p, e);
+  if (p == e) return false;
+  char* end = nullptr;
+  errno = 0;
+  const long long v = std::strtoll(p, &end, 10);
+  if (end == p || errno) return false;
+  if (skip_ws(end, e) != e) return false;
+  *out = v;
+  return true;
+}
+bool field_f64(const char* p, const char* e, double* out) {
+  p = skip_ws(p, e);
+  if (p == e) return false;
+  for (const char* q = p; q < e; ++q)
+    if (*q == 'x' || *q == 'X') return false;  // strtod's hex floats are not Python floats
+  char* end = nullptr;
+  const double v = std::strtod(p, &end);
+  if (end == p) return false;
+  if (skip_ws(end, e) != e) return false;
+  *out = v;
+  return true;
+}
+
+// parse everything; on success fills the vectors
+int parse_csv(const char* path, int64_t* d_e_out, std::vector<int64_t>& src,
+              std::vector<int64_t>& dst, std::vector<double>& t, std::vector<double>& feat,
+              int64_t* bad_line) {
+  CsvFile f;
+  *bad_line = 0;
+  if (!f.load(path)) return STGN_ERR_INVALID;
+  const char* p = f.buf.data();
+  const char* end = p + f.buf.size() - 1;
+  static const char kHdr[] = "# streamtgn-edges v1 d_e=";
+  const char* nl = p;
+  while (nl < end && *nl != '\n') ++nl;
+  const size_t hl = sizeof(kHdr) - 1;
+  int64_t d_e = 0;
+  if ((size_t)(nl - p) < hl || std::strncmp(p, kHdr, hl) != 0 || !field_i64(p + hl, nl, &d_e) ||
+      d_e < 0) {
+    *bad_line = 1;
+    return STGN_ERR_INVALID;
+  }
+  *d_e_out = d_e;
+  int64_t line = 1;
+  std::vector<double> row((size_t)d_e);
+  p = nl < end ? nl + 1 : end;
+  while (p < end) {
+    ++line;
+    const char* le = p;
+    while (le < end && *le != '\n') ++le;
+    if (skip_ws(p, le) != le) {
+      const char* q = p;
+      int64_t s = 0, d = 0;
+      double tv = 0.0;
+      bool ok = true;
+      for (int k = 0; k < 3 + d_e && ok; ++k) {
+        const char* fe = q;
+        while (fe < le && *fe != ',') ++fe;
+        if (k == 0) ok = field_i64(q, fe, &s);
+        else if (k == 1) ok = field_i64(q, fe, &d);
+        else if (k == 2) ok = field_f64(q, fe, &tv);
+        else ok = field_f64(q, fe, &row[(size_t)(k - 3)]);
+        if (k < 2 + d_e) {
+          if (fe >= le) ok = false;  // too few fields
+          q = fe + 1;
+        } else {
+          if (fe != le) ok = false;  // too many fields
+        }
+      }
+      if (!ok || s < 0 || d < 0) {
+        *bad_line = line;
+        return STGN_ERR_INVALID;
+      }
+      src.push_back(s);
+      dst.push_back(d);
+      t.push_back(tv);
+      feat.insert(feat.end(), row.begin(), row.end());
+    }
+    p = le < end ? le + 1 : end;
+  }
+  return STGN_OK;
+}
+
+}  // namespace
+
+extern "C" int stgn_read_stream(const char* path, int32_t sort, int64_t cap, int64_t* m_out,
+                                int64_t* d_e_out, int64_t* src, int64_t* dst, double* t,
+                                double* feat, int64_t* bad_line) {
+  if (!path || !m_out || !d_e_out || !bad_line) return STGN_ERR_INVALID;
+  std::vector<int64_t> s, d;
+  std::vector<double> tv, fv;
+  const int rc = parse_csv(path, d_e_out, s, d, tv, fv, bad_line);
+  if (rc) return rc;
+  const int64_t m = (int64_t)s.size(), de = *d_e_out;
+  *m_out = m;
+  // timestamps must not decrease (S/streamio.py:63-67) unless sort: stable re-sort
+  std::vector<int64_t> order((size_t)m);
+  for (int64_t i = 0; i < m; ++i) order[(size_t)i] = i;
+  for (int64_t i = 1; i < m; ++i) {
+    if (tv[(size_t)i] < tv[(size_t)i - 1]) {
+      if (!sort) {
+        *bad_line = -1;  // the Python parser reports the exact line
+        return STGN_ERR_INVALID;
+      }
+    }
+  }
+  if (sort) {
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int64_t a, int64_t b) { return tv[(size_t)a] < tv[(size_t)b]; });
+  }
+  if (cap < m || !src || !dst || !t || (de && !feat)) return m > cap ? STGN_ERR_CAPACITY : STGN_OK;
+  for (int64_t i = 0; i < m; ++i) {
+    const int64_t o = order[(size_t)i];
+    src[i] = s[(size_t)o];
+    dst[i] = d[(size_t)o];
+    t[i] = tv[(size_t)o];
+    for (int64_t k = 0; k < de; ++k) feat[i * de + k] = fv[(size_t)(o * de + k)];
   }
   return STGN_OK;
 }

@@ -13,6 +13,7 @@ list[TemporalEdge] when a caller wants objects.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -155,6 +156,34 @@ def _generate_native(seed, n, m, attachment, burstiness) -> EdgeArrays:
     return EdgeArrays(src, dst, ts, np.empty((m, 0), dtype=np.float64))
 
 
+def _read_stream_native(path, sort):
+    import ctypes as C
+
+    from . import _lib
+    try:
+        L = _lib.lib()
+    except OSError:
+        return None
+    m, d_e, bad = C.c_int64(), C.c_int64(), C.c_int64()
+    bpath = os.fsencode(path)
+    rc = L.stgn_read_stream(bpath, int(sort), 0, C.byref(m), C.byref(d_e), None, None, None, None,
+                            C.byref(bad))
+    if rc not in (_lib.STGN_OK, _lib.STGN_ERR_CAPACITY):
+        return None
+    n, k = int(m.value), int(d_e.value)
+    src = np.empty(n, dtype=np.int64)
+    dst = np.empty(n, dtype=np.int64)
+    ts = np.empty(n, dtype=np.float64)
+    feat = np.empty((n, k), dtype=np.float64)
+    vp = C.c_void_p
+    rc = L.stgn_read_stream(bpath, int(sort), n, C.byref(m), C.byref(d_e), vp(src.ctypes.data),
+                            vp(dst.ctypes.data), vp(ts.ctypes.data),
+                            vp(feat.ctypes.data) if k else None, C.byref(bad))
+    if rc != _lib.STGN_OK:
+        return None
+    return EdgeArrays(src, dst, ts, feat), k
+
+
 def serialize_stream(edges: EdgeArrays, d_e: int) -> str:
     lines = [f"{HEADER_PREFIX}{d_e}"]
     for s, d, t, f in zip(edges.src, edges.dst, edges.t, edges.feat):
@@ -168,7 +197,14 @@ def write_stream(edges: EdgeArrays, d_e: int, path: str) -> None:
         fh.write(serialize_stream(edges, d_e))
 
 
-def read_stream(path: str, sort: bool = False) -> tuple[EdgeArrays, int]:
+def read_stream(path: str, sort: bool = False, native: bool = True) -> tuple[EdgeArrays, int]:
+    """S/streamio.py:53-79. The native reader (csrc/gen.cpp) parses plain
+    files; anything it declines (format errors, unusual spellings) is re-read
+    by the Python parser below, so results and errors are the reference's."""
+    if native:
+        got = _read_stream_native(path, sort)
+        if got is not None:
+            return got
     with open(path) as fh:
         header = fh.readline().rstrip("\n")
         if not header.startswith(HEADER_PREFIX):
