@@ -77,7 +77,7 @@ __device__ int g_a4_prof_n;
 #error "A4_STATIC assigns two rows of every 32-row quadrant to each of 16 warps"
 #endif
 #ifndef A4_HINTS
-#define A4_HINTS 0  // L2 eviction hints on the walk's loads
+#define A4_HINTS 1  // L2 eviction hints on the walk's loads
 #endif
 #ifndef A4_EC
 #define A4_EC 2  // ring entries per chunk of the walk (2 or 4)
