@@ -577,6 +577,7 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
 template <int KF>
 __global__ void __launch_bounds__(A4_THREADS, 1)
 attn4_kernel(Geo g, A4W w, RingSrc rs) {
+  PDL_WAIT();
 #ifdef STGN_SKIP_RECOMPUTE  // timing experiments only: results are wrong
   return;
 #endif

@@ -62,6 +62,7 @@ __device__ __forceinline__ bool rec_is_adj(const Scratch& s, int r) {
 // Reset per-batch results; derive t_batch (the last edge's timestamp,
 // S/engine.py:415) and the window cutoff on the device.
 __global__ void k_begin(Scratch s, double window) {
+  PDL_WAIT();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     BatchHdr* hd = s.hdr;
     hd->t_batch = s.in_t[hd->B - 1];
@@ -85,6 +86,7 @@ __global__ void k_begin(Scratch s, double window) {
 // toucher of a node claims its direct-set slot; counts per node; the
 // side-0 record also appends the edge to the temporal store.
 __global__ void k_claim(Geo g, StateView st, Scratch s) {
+  PDL_WAIT();
   const BatchHdr* hd = s.hdr;
   const int64_t B = hd->B;
   const uint32_t stamp = hd->stamp;
@@ -113,6 +115,7 @@ __global__ void k_claim(Geo g, StateView st, Scratch s) {
 // One block: exclusive scan of per-direct-node record counts; per-node
 // offsets; remembers each direct node's pre-batch cache state.
 __global__ void k_scan(Geo g, StateView st, Scratch s) {
+  PDL_WAIT();
   __shared__ int32_t warp_tot[32];
   __shared__ int32_t carry;
   const int nD = s.res->nD;
@@ -166,6 +169,7 @@ __global__ void k_scan(Geo g, StateView st, Scratch s) {
 }
 
 __global__ void k_place(StateView st, Scratch s) {
+  PDL_WAIT();
   const int64_t B = s.hdr->B;
   GRID_STRIDE(r, 2 * B) {
     const int node = rec_node(s, (int)r);
@@ -178,6 +182,7 @@ __global__ void k_place(StateView st, Scratch s) {
 // entry per incident batch edge), giving message order (ascending r) and
 // the newest-first adjacency rank.
 __global__ void k_rank(StateView st, Scratch s) {
+  PDL_WAIT();
   const int64_t B = s.hdr->B;
   GRID_STRIDE(r64, 2 * B) {
     const int r = (int)r64;
@@ -210,6 +215,7 @@ __device__ __forceinline__ int64_t entry_index(int64_t m0, int r) {
 // as the payload; link the append-only store's per-node chains. One warp
 // per record.
 __global__ void k_ring(Geo g, StateView st, Scratch s, const double* __restrict__ omega) {
+  PDL_WAIT();
   const BatchHdr* hd = s.hdr;
   const int64_t R = 2 * hd->B;
   const int lane = threadIdx.x & 31;
@@ -261,6 +267,7 @@ __global__ void k_ring(Geo g, StateView st, Scratch s, const double* __restrict_
 // Per direct node: advance ring head/count, set the post-insertion cache
 // length, and move the store chain head.
 __global__ void k_dupdate(Geo g, StateView st, Scratch s) {
+  PDL_WAIT();
   const int nD = s.res->nD;
   const int64_t m0 = s.hdr->m0;
   GRID_STRIDE(d64, nD) {
@@ -295,6 +302,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // One BFS hop: every (frontier node, list position) pair marks its
 // neighbour; first markers append with warp-ballot compaction.
 __global__ void k_hop(Geo g, StateView st, Scratch s, int hop) {
+  PDL_WAIT();
   const uint32_t stamp = s.hdr->stamp;
   const int f0 = s.res->hop_off[hop - 1], f1 = s.res->hop_off[hop];
   const int64_t total = (int64_t)(f1 - f0) * g.L;
@@ -327,12 +335,14 @@ __global__ void k_hop(Geo g, StateView st, Scratch s, int hop) {
 }
 
 __global__ void k_hop_fin(Scratch s, int hop) {
+  PDL_WAIT();
   if (threadIdx.x == 0 && blockIdx.x == 0) s.res->hop_off[hop + 1] = s.res->nA;
 }
 
 // Change records for every affected node (sizes only) + the window filter
 // + cache bookkeeping; S/engine.py:216-243.
 __global__ void k_records(Geo g, StateView st, Scratch s, int finite_window) {
+  PDL_WAIT();
   const int nA = s.res->nA, nD = s.res->nD;
   const uint32_t stamp = s.hdr->stamp;
   const double cutoff = s.hdr->cutoff;
@@ -407,6 +417,7 @@ __global__ void k_records(Geo g, StateView st, Scratch s, int finite_window) {
 // (L <= 32): the window prefix is a ballot, the distinct direct
 // neighbours a __match_any_sync, so a node costs a few parallel loads.
 __global__ void k_records_warp(Geo g, StateView st, Scratch s, int finite_window) {
+  PDL_WAIT();
   // floor(32 / L) affected nodes per warp, one L-lane segment each
   const int nA = s.res->nA, nD = s.res->nD;
   const uint32_t stamp = s.hdr->stamp;
@@ -484,6 +495,7 @@ __global__ void k_records_warp(Geo g, StateView st, Scratch s, int finite_window
 
 // valid / valid_at for A \ D when only V_direct is recomputed.
 __global__ void k_mark_valid(StateView st, Scratch s) {
+  PDL_WAIT();
   const int nA = s.res->nA, nD = s.res->nD;
   const double t = s.hdr->t_batch;
   GRID_STRIDE(a, nA) {
@@ -499,6 +511,7 @@ __global__ void k_mark_valid(StateView st, Scratch s) {
 // then commit the post-batch memory of V_direct (S/engine_base.py:241-244).
 __global__ void k_predict_commit(Geo g, StateView st, Scratch s, const double* wpred,
                                  double bpred) {
+  PDL_WAIT();
   const int64_t B = s.hdr->B;
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -810,6 +823,7 @@ __global__ void k_drift_reset_fin(StateView st, Scratch s) {
 
 // Clear per-node batch scratch of the direct nodes.
 __global__ void k_cleanup(StateView st, Scratch s) {
+  PDL_WAIT();
   const int nD = s.res->nD;
   GRID_STRIDE(d, nD) {
     const int v = s.alist[d];

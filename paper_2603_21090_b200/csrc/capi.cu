@@ -7,6 +7,7 @@
 #include <new>
 
 #include <algorithm>
+#include <utility>
 
 #include "batch.cuh"
 #include "attn3.cuh"
@@ -381,6 +382,28 @@ int stgn_engine_bind(stgn_engine* e, const stgn_state* s) {
 
 }  // extern "C"
 
+// Launch on the batch chain: with STGN_PDL, programmatic stream serialization
+// (the kernel waits for its predecessor in PDL_WAIT instead of at launch).
+template <typename... KArgs, typename... Args>
+static void chain_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                         cudaStream_t st, Args&&... args) {
+#ifdef STGN_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+#else
+  kern<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+#endif
+}
+
 static RingSrc ring_src(const stgn_engine* e) {
   RingSrc r;
   memset(&r, 0, sizeof(r));
@@ -392,8 +415,11 @@ static RingSrc ring_src(const stgn_engine* e) {
   return r;
 }
 
-static void launch_attn(const stgn_engine* e, const RingSrc& rs, cudaStream_t st) {
-  if (e->use_a4)
+static void launch_attn(const stgn_engine* e, const RingSrc& rs, cudaStream_t st,
+                        bool chain = false) {
+  if (e->use_a4 && chain)
+    chain_launch(e->attn4, e->num_sms, A4_THREADS, e->attn4_smem, st, e->g, e->a4w, rs);
+  else if (e->use_a4)
     e->attn4<<<e->num_sms, A4_THREADS, e->attn4_smem, st>>>(e->g, e->a4w, rs);
   else if (e->use_tc)
     e->attn3<<<e->num_sms, A3_THREADS, e->attn3_smem, st>>>(e->g, e->tcw, rs, e->attn3_tmax);
@@ -406,6 +432,7 @@ static const char* kStageNames[] = {"group+ring", "affected_bfs", "change_record
                                     "memory_update", "recompute", "predict+commit", "drift",
                                     "rebuild", "cleanup"};
 #define NSTAGES 9
+
 
 static void launch_memory(const stgn_engine* e, cudaStream_t st) {
   const Geo& g = e->g;
@@ -441,11 +468,11 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   };
   mark();
   // ingest: direct set, per-node record order, ring insert with payload freeze, store append
-  k_begin<<<1, 32, 0, st>>>(s, e->cfg.window);
-  k_claim<<<g_rec, T, 0, st>>>(g, v, s);
-  k_scan<<<1, 1024, 0, st>>>(g, v, s);
-  k_place<<<g_rec, T, 0, st>>>(v, s);
-  k_rank<<<g_rec, T, 0, st>>>(v, s);
+  chain_launch(k_begin, 1, 32, 0, st, s, e->cfg.window);
+  chain_launch(k_claim, g_rec, T, 0, st, g, v, s);
+  chain_launch(k_scan, 1, 1024, 0, st, g, v, s);
+  chain_launch(k_place, g_rec, T, 0, st, v, s);
+  chain_launch(k_rank, g_rec, T, 0, st, v, s);
   // Branch 0 (graph mode): the memory update needs only the grouped records
   // (rec_s, doff) and pre-batch memory and writes scratch only, so it runs
   // beside the ring insertion, the BFS and the change records.
@@ -459,18 +486,18 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
     n += 1;
     cudaEventRecord(e->ev_join[0], mst);
   }
-  k_ring<<<g_warp, T, 0, st>>>(g, v, s, e->w.omega);
-  k_dupdate<<<g_rec, T, 0, st>>>(g, v, s);
+  chain_launch(k_ring, g_warp, T, 0, st, g, v, s, e->w.omega);
+  chain_launch(k_dupdate, g_rec, T, 0, st, g, v, s);
   n += 7;
   mark();
   for (int hop = 1; hop <= g.K; ++hop) {
-    k_hop<<<g_wide, T, 0, st>>>(g, v, s, hop);
-    k_hop_fin<<<1, 32, 0, st>>>(s, hop);
+    chain_launch(k_hop, g_wide, T, 0, st, g, v, s, hop);
+    chain_launch(k_hop_fin, 1, 32, 0, st, s, hop);
     n += 2;
   }
   mark();
   if (g.L <= 32)
-    k_records_warp<<<8 * e->num_sms, T, 0, st>>>(g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
+    chain_launch(k_records_warp, 8 * e->num_sms, T, 0, st, g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
   else
     k_records<<<g_wide, T, 0, st>>>(g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
   n += 1;
@@ -508,14 +535,14 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   rs.dpred = s.dpred;
   rs.e_count = &s.res->E_A;
   rs.e_count_post = &s.res->E_D;
-  launch_attn(e, rs, st);
+  launch_attn(e, rs, st, true);
   n += 1;
   if (e->cfg.scope == STGN_SCOPE_DIRECT) {
     k_mark_valid<<<g_wide, T, 0, st>>>(v, s);
     n += 1;
   }
   mark();
-  k_predict_commit<<<g_warp, T, 0, st>>>(g, v, s, e->w.wpred, e->w.bpred);
+  chain_launch(k_predict_commit, g_warp, T, 0, st, g, v, s, e->w.wpred, e->w.bpred);
   n += 1;
   mark();
   // drift + rebuild policy
@@ -581,7 +608,7 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
     }
   }
   mark();
-  k_cleanup<<<g_rec, T, 0, st>>>(v, s);
+  chain_launch(k_cleanup, g_rec, T, 0, st, v, s);
   n += 1;
   mark();
   e->launches = n;

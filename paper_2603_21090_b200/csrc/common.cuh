@@ -178,6 +178,16 @@ __device__ __forceinline__ float phi_component(const double* __restrict__ omega,
 
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + expf(-x)); }
 
+// Programmatic dependent launch (STGN_PDL builds): the kernels of the batch
+// chain are launched with programmatic stream serialization, so a kernel's
+// launch overlaps its predecessor's tail; it must wait here before touching
+// anything the predecessor writes. A no-op for ordinary launches.
+#ifdef STGN_PDL
+#define PDL_WAIT() asm volatile("griddepcontrol.wait;\n" ::: "memory")
+#else
+#define PDL_WAIT() do {} while (0)
+#endif
+
 // Last CUDA failure (file:line + message), readable through stgn_last_error().
 void stgn_set_error(const char* file, int line, cudaError_t e);
 
