@@ -50,6 +50,10 @@ extern "C" {
 
 #define STGN_SCOPE_AFFECTED 0  /* recompute every node of A (the reference's literal exact mode) */
 #define STGN_SCOPE_DIRECT   1  /* recompute V_direct only; value-identical when window = inf     */
+#define STGN_SCOPE_DELTA    2  /* the reference's delta mode (S/engine.py:276-331): untouched
+                                  affected nodes keep their cached row (embed_skip), the rest are
+                                  classified attn_hit / attn_miss against per-node attention-state
+                                  stamps and recomputed                                         */
 
 /* Model widths; same meaning as the reference Dims (S/config.py:11-55). */
 typedef struct {
@@ -155,6 +159,9 @@ typedef struct {
   uint32_t *cum_mark;   /* [cap_nodes] node is in the cumulative affected set (generation stamp) */
   int32_t  *cum_list;   /* [cap_nodes] position -> node */
   int32_t  *cum_pos;    /* [cap_nodes] node -> position */
+  int64_t  *attn_ver;   /* [cap_nodes] delta mode: memory version the node's attention state was
+                           built on, -1 = no state (AttnState.mem_version, S/state.py:175-190) */
+  double   *attn_tref;  /* [cap_nodes] delta mode: the state's t_ref (AttnState.t_ref) */
   int32_t  *e_src, *e_dst;  /* [cap_edges]   append-only temporal store */
   double   *e_t;            /* [cap_edges] */
   float    *e_feat;         /* [cap_edges][ld_e] */
@@ -178,6 +185,9 @@ typedef struct {
   int64_t tau, cum_count;
   int64_t changed;                            /* nodes with a non-empty change record */
   double  global_drift;
+  /* delta mode (STGN_SCOPE_DELTA) classification, S/engine.py:287-313 */
+  int64_t embed_skip, attn_hit, attn_miss;
+  int64_t entries_miss;                       /* sum of list lengths over attn_miss nodes */
   int64_t reserved[3];
 } stgn_report;
 

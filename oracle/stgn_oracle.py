@@ -19,6 +19,12 @@ What it restates (reference = /root/reference/pkg/src/streamtgn, "S/"):
     commit + memory   S/engine_base.py:108-116, 193-247; S/engine.py:357-372
     drift / rebuild   S/drift.py:16-96, S/engine.py:385-396, 440-453
   full_reference      S/engine.py:374-381
+  delta mode          S/engine.py:276-331 classification (embed_skip /
+                      attn_hit / attn_miss, AttnState stamps from
+                      _build_attn_state :247-274); a hit's delta_embed
+                      update (:43-118) is evaluated as the same softmax
+                      over the same frozen-payload key rows, so hits agree
+                      with the reference to rounding, not bitwise
 
 Pinning: tests/test_golden_oracle.py checks this module against fixtures
 written by the reference itself (tests/golden/make_golden.py) — bitwise
@@ -220,8 +226,10 @@ class Oracle:
 
     def __init__(self, cfg, params):
         cfg.validate()
-        if cfg.mode != "exact":
-            raise ValueError("the oracle restates exact mode only")
+        if cfg.mode not in ("exact", "delta"):
+            raise ValueError(f"unknown mode {cfg.mode}")
+        self.delta = cfg.mode == "delta"
+        self.attn: dict[int, tuple] = {}  # delta mode: node -> (mem_version, t_ref) of its AttnState
         self.cfg, self.p = cfg, params
         dm = params.dims
         self.K, self.d, self.L = dm.layers, dm.d, cfg.fanout
@@ -287,7 +295,7 @@ class Oracle:
         return st
 
     # -- pipeline over a node list (S/engine_base.py:139-189) ---------------
-    def _pipeline(self, ids, lists, pending):
+    def _pipeline(self, ids, lists, pending, count=True):
         p = self.p
         dm = p.dims
         N = len(ids)
@@ -314,20 +322,66 @@ class Oracle:
                     payload[pos] = st_d if v == s else st_s
                     feat[pos] = f
                 pos += 1
-        self._count("rows_gathered", N)
-        per_node = dm.heads * dm.query_in * dm.d_k + dm.heads * dm.d_k * dm.d
-        per_entry = dm.heads * (2 * dm.key_in * dm.d_k + 2 * dm.d_k)
-        self._count("macs_attention", dm.layers * (N * per_node + E * per_entry))
+        if count:
+            self._count("rows_gathered", N)
+            per_node = dm.heads * dm.query_in * dm.d_k + dm.heads * dm.d_k * dm.d
+            per_entry = dm.heads * (2 * dm.key_in * dm.d_k + 2 * dm.d_k)
+            self._count("macs_attention", dm.layers * (N * per_node + E * per_entry))
         return pipeline_many(qbase, offs, payload, feat, dt, p.omega, self.phi0,
                              p.w_q, p.w_k, p.w_v, p.w_o)[0]
 
-    def _recompute(self, ids, valid_at):
+    def _recompute(self, ids, valid_at, count=True, keep_states=True):
         lists = [self.cache.get(v) or [] for v in ids]
-        out = self._pipeline(ids, lists, self._pending)
+        out = self._pipeline(ids, lists, self._pending, count)
         for i, v in enumerate(ids):
             self.h[v] = out[i]
             self.valid[v] = True
             self.valid_at[v] = valid_at
+        if keep_states:
+            self._stamp(ids)
+        return out
+
+    def _stamp(self, ids):
+        """Delta mode, single layer: the AttnState (mem_version, t_ref) that
+        _build_attn_state (S/engine.py:247-274) leaves behind."""
+        if self.delta and self.K == 1:
+            for v in ids:
+                lst = self.cache.get(v) or []
+                self.attn[v] = (int(self.version[v]), lst[0][1] if lst else 0.0)
+
+    def _delta_stage(self, ids, direct, sizes, t_batch, compute):
+        """S/engine.py:276-319: skip / attn_hit / attn_miss per node of A."""
+        K = self.K
+        out = np.zeros((len(ids), K, self.d))
+        hits, misses, pos = [], [], {}
+        for i, v in enumerate(ids):
+            pos[v] = i
+            if v not in direct and sizes[v] == 0 and self.valid[v]:
+                self._count("embed_skip")
+                out[i] = self.h[v]
+                continue
+            lst = self.cache.get(v) or []
+            t_ref = lst[0][1] if lst else 0.0
+            if K == 1 and self.valid[v] and self.attn.get(v) == (int(self.version[v]), t_ref):
+                hits.append(v)
+                self._count("attn_hit")
+            else:
+                misses.append(v)
+                self._count("attn_miss")
+        if compute:
+            for lst, cnt in ((misses, True), (hits, False)):
+                if lst:
+                    res = self._recompute(lst, t_batch, count=cnt, keep_states=cnt)
+                    for j, v in enumerate(lst):
+                        out[pos[v]] = res[j]
+        else:
+            self._stamp(misses)
+        computed = set(hits) | set(misses)
+        for v in ids:
+            if v in direct:
+                self._count("embed_predict")
+            elif v in computed:
+                self._count("embed_refresh")
         return out
 
     # -- the batch -----------------------------------------------------------
@@ -338,6 +392,8 @@ class Oracle:
         baseline deep in a stream: topology, caches, memory and drift are
         updated exactly, the attention recomputes are skipped (their cost
         depends on topology only, their values feed nothing but h)."""
+        if self.delta and not compute:
+            raise ValueError("compute=False fast-forward is exact-mode only")
         self._compute = compute
         self.counters = {}
         self.last_pred_h = {}
@@ -415,9 +471,12 @@ class Oracle:
             self.cache[v] = kept
         # stages 2-4: recompute sorted(A) with pre-batch memory
         ids = sorted(A)
-        out = self._recompute(ids, t_batch) if compute else np.zeros((len(ids), K, self.d))
-        for v in ids:
-            self._count("embed_predict" if v in direct else "embed_refresh")
+        if self.delta:
+            out = self._delta_stage(ids, direct, sizes, t_batch, compute)
+        else:
+            out = self._recompute(ids, t_batch) if compute else np.zeros((len(ids), K, self.d))
+            for v in ids:
+                self._count("embed_predict" if v in direct else "embed_refresh")
         hK = {v: out[i, K - 1] for i, v in enumerate(ids)}
         preds = [predict_link(hK[int(src[i])], hK[int(dst[i])], self.p) for i in range(B)]
         self.last_pred_h = {v: hK[v].copy() for v in direct}
@@ -447,6 +506,8 @@ class Oracle:
         if dlist:
             if compute:
                 self._recompute(dlist, t_batch)
+            else:
+                self._stamp(dlist)
             self._count("embed_refresh", len(dlist))
         changes = {}
         for v in A:
@@ -568,6 +629,8 @@ class Oracle:
         self._pending = {}
         if getattr(self, "_compute", True):
             self._recompute(ids, self.t_now if self.m else 0.0)
+        else:
+            self._stamp(ids)
         self._count("rebuild_pipelines", len(ids))
         return len(ids)
 

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "_stgn.so")
 STGN_OK, STGN_ERR_INVALID, STGN_ERR_BOUNDS, STGN_ERR_CUDA, STGN_ERR_CAPACITY, STGN_ERR_ORDER = range(6)
 AGG = {"mean": 0, "last": 1, "sum": 2}
 REBUILD = {"never": 0, "fixed": 1, "adaptive": 2}
-SCOPE = {"affected": 0, "direct": 1}
+SCOPE = {"affected": 0, "direct": 1, "delta": 2}
 
 # Symbols include/stgn.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = (
@@ -60,7 +60,7 @@ STATE_PTRS = (
     "mem", "last", "version", "h", "valid", "valid_at", "ring_cnt", "ring_head", "ring_ccnt",
     "ring_nbr", "ring_eid", "ring_t", "ring_pay", "ring_feat", "ring_tb", "amark", "dmark", "nodecnt",
     "nodeadj", "nodefill", "nodeoff", "drift_acc", "drift_touched", "cum_mark", "cum_list",
-    "cum_pos",
+    "cum_pos", "attn_ver", "attn_tref",
     "e_src", "e_dst", "e_t", "e_feat", "e_prev", "adj_head", "adj_deg", "gpow", "ctl", "scratch",
 )
 
@@ -74,8 +74,9 @@ class Report(C.Structure):
     _fields_ = [(n, C.c_int64) for n in
                 ("direct", "affected", "nbr_hit", "nbr_miss", "entries_affected",
                  "entries_direct", "rebuild_kind", "rebuild_nodes", "entries_rebuild", "tau",
-                 "cum_count", "changed")] + [("global_drift", C.c_double),
-                                              ("reserved", C.c_int64 * 3)]
+                 "cum_count", "changed")] + [("global_drift", C.c_double)] + \
+               [(n, C.c_int64) for n in ("embed_skip", "attn_hit", "attn_miss", "entries_miss")] + \
+               [("reserved", C.c_int64 * 3)]
 
 
 _LIB = None

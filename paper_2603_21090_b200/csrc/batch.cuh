@@ -35,6 +35,8 @@ struct StateView {
   uint32_t* cum_mark;
   int32_t* cum_list;
   int32_t* cum_pos;
+  int64_t* attn_ver;
+  double* attn_tref;
   int32_t *e_src, *e_dst;
   double* e_t;
   float* e_feat;
@@ -79,6 +81,8 @@ __global__ void k_begin(Scratch s, double window) {
     r->rb_partial_n = 0;
     r->rb_full_n = 0;
     r->ticket = 0;
+    r->nC = r->n_skip = r->n_hit = r->n_miss = 0;
+    r->E_miss = 0;
   }
 }
 
@@ -493,6 +497,89 @@ __global__ void k_records_warp(Geo g, StateView st, Scratch s, int finite_window
   }
 }
 
+// Delta mode (S/engine.py:287-313): classify every node of A after its change
+// record is known. A \ D nodes with an empty record and a valid cache row are
+// skipped (embed_skip); every other node is an attn_hit when the node has an
+// attention state built on its current memory version and the newest entry of
+// its post-batch list still carries the state's t_ref (single-layer models
+// only, :302-305), else an attn_miss. Hits and misses are recomputed: a hit's
+// delta update (delta_embed, :43-118) is the same softmax over the same
+// entries (the key rows are frozen payloads), so the recompute gives the
+// delta result up to rounding. State stamps follow the reference's
+// _build_attn_state calls: misses of A \ D get (version, t_ref) now; D gets
+// the post-commit stamp (version = batch index, S/state.py:25) because the
+// commit recomputes it with keep_states (:357-364).
+__global__ void k_delta_classify(Geo g, StateView st, Scratch s) {
+  PDL_WAIT();
+  const int nA = s.res->nA, nD = s.res->nD;
+  const int64_t bidx = s.hdr->batch_index;
+  const int lane = threadIdx.x & 31;
+  int skip = 0, hit = 0, miss = 0;
+  unsigned long long e_miss = 0;
+  const int64_t n_it = ((int64_t)nA + 31) & ~31ll;  // whole warps for the ballot
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < n_it;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    bool keep = false;
+    int v = 0;
+    if (a < nA) {
+      v = s.alist[a];
+      const int len = s.a_len[a];
+      const bool direct = a < nD;
+      const bool valid = st.valid[v] != 0;
+      if (!direct && s.a_size[a] == 0 && valid) {
+        ++skip;
+      } else {
+        const double tref = len > 0 ? st.ring_t[(int64_t)v * g.L + st.ring_head[v]] : 0.0;
+        const bool is_hit = g.K == 1 && valid && st.attn_ver[v] == st.version[v] &&
+                            st.attn_tref[v] == tref;
+        if (is_hit) {
+          ++hit;
+        } else {
+          ++miss;
+          e_miss += (unsigned long long)len;
+        }
+        if (direct) {
+          s.clist[a] = v;
+          st.attn_ver[v] = bidx;
+          st.attn_tref[v] = tref;
+        } else {
+          keep = true;
+          if (!is_hit) {
+            st.attn_ver[v] = st.version[v];
+            st.attn_tref[v] = tref;
+          }
+        }
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (m) {
+      int base = 0;
+      const int leader = __ffs(m) - 1;
+      if (lane == leader) base = atomicAdd(&s.res->nC, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (keep) s.clist[nD + base + __popc(m & ((1u << lane) - 1u))] = v;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    skip += __shfl_xor_sync(0xffffffffu, skip, o);
+    hit += __shfl_xor_sync(0xffffffffu, hit, o);
+    miss += __shfl_xor_sync(0xffffffffu, miss, o);
+    e_miss += __shfl_xor_sync(0xffffffffu, e_miss, o);
+  }
+  if (lane == 0) {
+    if (skip) atomicAdd(&s.res->n_skip, skip);
+    if (hit) atomicAdd(&s.res->n_hit, hit);
+    if (miss) atomicAdd(&s.res->n_miss, miss);
+    if (e_miss) atomicAdd(&s.res->E_miss, e_miss);
+  }
+}
+
+// nC := nD + (non-skipped nodes of A \ D), the pre-batch recompute's row count.
+__global__ void k_delta_fin(Scratch s) {
+  PDL_WAIT();
+  if (threadIdx.x == 0 && blockIdx.x == 0) s.res->nC += s.res->nD;
+}
+
 // valid / valid_at for A \ D when only V_direct is recomputed.
 __global__ void k_mark_valid(StateView st, Scratch s) {
   PDL_WAIT();
@@ -802,12 +889,19 @@ __global__ void k_drift_decide(StateView st, Scratch s, int rebuild, int64_t int
 
 // Rebuild prologue: uncached nodes get their cache filled from the store
 // (S/engine.py:390-392).
-__global__ void k_rb_fill(StateView st, const int32_t* list, const int32_t* count_ptr,
-                          int64_t count_const) {
+// In delta mode on single-layer models the rebuilt nodes get attention-state
+// stamps, as the rebuild's _compute_exact keeps states (:393-395).
+__global__ void k_rb_fill(Geo g, StateView st, const int32_t* list, const int32_t* count_ptr,
+                          int64_t count_const, int stamp) {
   const int64_t n = count_ptr ? (int64_t)count_ptr[0] : count_const;
   GRID_STRIDE(q, n) {
     const int v = list ? list[q] : (int)q;
-    if (st.ring_ccnt[v] < 0) st.ring_ccnt[v] = st.ring_cnt[v];
+    int cc = st.ring_ccnt[v];
+    if (cc < 0) st.ring_ccnt[v] = cc = st.ring_cnt[v];
+    if (stamp) {
+      st.attn_ver[v] = st.version[v];
+      st.attn_tref[v] = cc > 0 ? st.ring_t[(int64_t)v * g.L + st.ring_head[v]] : 0.0;
+    }
   }
 }
 

@@ -173,7 +173,8 @@ int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engin
   if (!e) return STGN_ERR_INVALID;
   e->dims = *dims;
   e->cfg = *cfg;
-  if (std::isfinite(cfg->window)) e->cfg.scope = STGN_SCOPE_AFFECTED;  // A\D can change
+  if (std::isfinite(cfg->window) && cfg->scope == STGN_SCOPE_DIRECT)
+    e->cfg.scope = STGN_SCOPE_AFFECTED;  // A\D can change
   e->g = make_geo(*dims, cfg->fanout);
   int dev = 0;
   cudaError_t ce = cudaGetDevice(&dev);
@@ -370,7 +371,7 @@ int stgn_engine_bind(stgn_engine* e, const stgn_state* s) {
   v.amark = s->amark; v.dmark = s->dmark; v.nodecnt = s->nodecnt; v.nodeadj = s->nodeadj;
   v.nodefill = s->nodefill; v.nodeoff = s->nodeoff; v.drift_acc = s->drift_acc;
   v.drift_touched = s->drift_touched; v.cum_mark = s->cum_mark; v.cum_list = s->cum_list;
-  v.cum_pos = s->cum_pos;
+  v.cum_pos = s->cum_pos; v.attn_ver = s->attn_ver; v.attn_tref = s->attn_tref;
   v.e_src = s->e_src; v.e_dst = s->e_dst; v.e_t = s->e_t; v.e_feat = s->e_feat;
   v.e_prev = s->e_prev; v.adj_head = s->adj_head; v.adj_deg = s->adj_deg;
   v.gpow = s->gpow; v.gpow_len = s->gpow_len; v.ctl = s->ctl;
@@ -501,6 +502,11 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   else
     k_records<<<g_wide, T, 0, st>>>(g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
   n += 1;
+  if (e->cfg.scope == STGN_SCOPE_DELTA) {
+    chain_launch(k_delta_classify, g_rec, T, 0, st, g, v, s);
+    chain_launch(k_delta_fin, 1, 32, 0, st, s);
+    n += 2;
+  }
   mark();
   // stage 5 (memory update of V_direct) into mem_new; commits after the recompute
   if (mst == st) {
@@ -527,7 +533,12 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   RingSrc rs = ring_src(e);
   rs.list = s.alist;
   rs.fused = 1;
-  rs.pre_n = e->cfg.scope == STGN_SCOPE_DIRECT ? &s.res->nD : &s.res->nA;
+  if (e->cfg.scope == STGN_SCOPE_DELTA) {
+    rs.list = s.clist;
+    rs.pre_n = &s.res->nC;
+  } else {
+    rs.pre_n = e->cfg.scope == STGN_SCOPE_DIRECT ? &s.res->nD : &s.res->nA;
+  }
   rs.post_n = &s.res->nD;
   rs.mem_post = s.mem_new;
   rs.valid_at_ptr = &s.hdr->t_batch;
@@ -554,6 +565,7 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   }
   mark();
   if (e->cfg.rebuild != STGN_REBUILD_NEVER) {
+    const int stamp = e->cfg.scope == STGN_SCOPE_DELTA && g.K == 1;
     // Inside a captured graph the rebuild block is the body of a conditional
     // IF node whose flag k_drift_decide sets on the device; eager launches
     // (profiling) run it unconditionally (each kernel is a no-op unless chosen).
@@ -587,8 +599,8 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
       }
     }
     // partial: the drifted list; full: all node ids
-    k_rb_fill<<<g_wide, T, 0, rs>>>(v, s.drifted, &s.res->rb_partial_n, 0);
-    k_rb_fill<<<g_wide, T, 0, rs>>>(v, nullptr, &s.res->rb_full_n, 0);
+    k_rb_fill<<<g_wide, T, 0, rs>>>(g, v, s.drifted, &s.res->rb_partial_n, 0, stamp);
+    k_rb_fill<<<g_wide, T, 0, rs>>>(g, v, nullptr, &s.res->rb_full_n, 0, stamp);
     RingSrc rp = ring_src(e);
     rp.list = s.drifted;
     rp.count_ptr = &s.res->rb_partial_n;
@@ -704,6 +716,10 @@ static void fill_report(const BatchRes& r, const stgn_ctl* /*unused*/, stgn_repo
   rep->rebuild_nodes = r.rebuild_nodes;
   rep->entries_rebuild = (int64_t)r.E_R;
   rep->changed = (int64_t)r.changed;
+  rep->embed_skip = r.n_skip;
+  rep->attn_hit = r.n_hit;
+  rep->attn_miss = r.n_miss;
+  rep->entries_miss = (int64_t)r.E_miss;
   rep->global_drift = r.global_drift;
 }
 
@@ -825,7 +841,8 @@ extern "C" int stgn_engine_rebuild(stgn_engine* e, const int32_t* ids, int64_t n
   }
   if (count) *count = n;
   if (n == 0) return STGN_OK;
-  k_rb_fill<<<4 * e->num_sms, 256, 0, st>>>(e->sv, list, nullptr, n);
+  k_rb_fill<<<4 * e->num_sms, 256, 0, st>>>(e->g, e->sv, list, nullptr, n,
+                                             e->cfg.scope == STGN_SCOPE_DELTA && e->g.K == 1);
   RingSrc r = ring_src(e);
   r.list = list;
   r.count_const = n;
@@ -983,7 +1000,9 @@ extern "C" int stgn_engine_info(stgn_engine* e, int64_t* info, int n) {
 
 // Switch the recompute scope between batches (drops the captured graph).
 extern "C" int stgn_engine_set_scope(stgn_engine* e, int scope) {
-  if (!e || (scope != STGN_SCOPE_AFFECTED && scope != STGN_SCOPE_DIRECT)) return STGN_ERR_INVALID;
+  if (!e || (scope != STGN_SCOPE_AFFECTED && scope != STGN_SCOPE_DIRECT &&
+             scope != STGN_SCOPE_DELTA))
+    return STGN_ERR_INVALID;
   if (scope == STGN_SCOPE_DIRECT && std::isfinite(e->cfg.window)) return STGN_ERR_INVALID;
   e->cfg.scope = scope;
   drop_graph(e);

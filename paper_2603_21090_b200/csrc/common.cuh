@@ -66,7 +66,10 @@ struct BatchRes {
   int32_t nAD;                       // rows of the fused recompute (A pre + D post)
   int32_t pad3;
   uint32_t ticket;                   // last-block-done counter of k_drift_decide
-  int32_t pad2;
+  int32_t nC;                        // delta mode: rows of the pre-batch recompute (clist)
+  int32_t n_skip, n_hit, n_miss;     // delta mode classification
+  int32_t pad4;
+  unsigned long long E_miss;         // delta mode: entries over attn_miss nodes
 };
 
 // Scratch carving (all offsets 256-B aligned).
@@ -84,6 +87,7 @@ struct Scratch {
   int32_t *d_wascached, *d_baselen;  // [2Bmax] by D index
   int32_t* a_size;          // [cap_nodes] change-record size by A index
   int32_t* a_len;           // [cap_nodes] cache length after the batch, by A index
+  int32_t* clist;           // [cap_nodes] delta mode: D, then the non-skipped nodes of A \ D
   float* msgs;              // [2Bmax][ld_m]
   double* preds;            // [Bmax]
   float* dpred;             // [2Bmax][ld_d]
@@ -114,6 +118,7 @@ static inline int64_t scratch_layout(const Geo& g, int64_t Bmax, int64_t cap_nod
   int64_t o_rank = carve(off, R * 4), o_prev = carve(off, R * 4);
   int64_t o_wc = carve(off, R * 4), o_bl = carve(off, R * 4);
   int64_t o_asz = carve(off, cap_nodes * 4), o_alen = carve(off, cap_nodes * 4);
+  int64_t o_clist = carve(off, cap_nodes * 4);
   int64_t o_msg = carve(off, R * g.ld_m * 4);
   int64_t o_pred = carve(off, Bmax * 8);
   int64_t o_dpred = carve(off, R * g.ld_d * 4);
@@ -139,6 +144,7 @@ static inline int64_t scratch_layout(const Geo& g, int64_t Bmax, int64_t cap_nod
     s->d_baselen = (int32_t*)(base + o_bl);
     s->a_size = (int32_t*)(base + o_asz);
     s->a_len = (int32_t*)(base + o_alen);
+    s->clist = (int32_t*)(base + o_clist);
     s->msgs = (float*)(base + o_msg);
     s->preds = (double*)(base + o_pred);
     s->dpred = (float*)(base + o_dpred);

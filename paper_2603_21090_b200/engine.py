@@ -149,6 +149,8 @@ class _Tables:
         self.ring_tb = z(N, g.L, g.ld_t)
         self.drift_acc = z(N, dt=torch.float64)
         self.drift_touched = z(N, dt=torch.int64)
+        self.attn_ver = z(N, dt=torch.int64, fill=-1)
+        self.attn_tref = z(N, dt=torch.float64)
         self.adj_head = z(N, dt=torch.int64, fill=-1)
         self.adj_deg = z(N, dt=torch.int64)
         for k, t in old.items():
@@ -157,7 +159,7 @@ class _Tables:
 
     def _node_names(self):
         return ("mem", "last", "version", "h", "valid", "valid_at", *self.NODE_I32, "ring_nbr",
-                "ring_eid", "ring_t", "ring_pay", "ring_feat", "ring_tb", "drift_acc", "drift_touched",
+                "ring_eid", "ring_t", "ring_pay", "ring_feat", "ring_tb", "drift_acc", "drift_touched", "attn_ver", "attn_tref",
                 "adj_head", "adj_deg")
 
     def _alloc_edges(self, E):
@@ -418,14 +420,26 @@ class IncrementalEngine:
     literal exact mode, default); "direct" recomputes V_direct only, which is
     value-identical when the window is infinite (keys/values come from
     payloads frozen at insertion, so A minus V_direct has unchanged inputs).
+
+    cfg.mode == "delta" selects the reference's delta mode (S/engine.py:276-331):
+    affected nodes outside V_direct with an empty change record keep their
+    cached row (embed_skip); the others are classified attn_hit / attn_miss
+    exactly as the reference does and recomputed on the device (a hit's
+    delta_embed update is the same softmax over the same frozen-payload key
+    rows, so the recompute returns the delta result up to rounding). The
+    per-update error-bound records (delta_events) are not collected.
     """
 
     def __init__(self, cfg: RunConfig, params: ModelParameters, *, recompute: str = "affected",
                  max_batch: int | None = None, device: int | None = None,
                  tensor_cores: bool | str = True):
         cfg.validate()
-        if cfg.mode != "exact":
-            raise ConfigError("the B200 engine implements exact mode (delta mode is out of scope)")
+        if cfg.mode == "delta":
+            if recompute not in ("affected", "delta"):
+                raise ConfigError("delta mode recomputes by its own classification")
+            recompute = "delta"
+        elif recompute == "delta":
+            raise ConfigError('recompute="delta" needs cfg.mode == "delta"')
         if recompute not in _lib.SCOPE:
             raise ConfigError(f"recompute must be one of {tuple(_lib.SCOPE)}")
         self._torch = _torch()
@@ -473,6 +487,7 @@ class IncrementalEngine:
         self.store = _StoreView(self)
         self.scheduler = _SchedulerView(self)
         self._rep = _lib.Report()
+        self.delta_events: list = []  # delta mode: bound records are not collected
         self._preds = np.zeros(self._max_batch, dtype=np.float64)
 
     # -- plumbing -------------------------------------------------------------
@@ -766,6 +781,8 @@ class IncrementalEngine:
         "direct" (value-identical with an infinite window) for later batches."""
         if recompute not in _lib.SCOPE:
             raise ConfigError(f"recompute must be one of {tuple(_lib.SCOPE)}")
+        if (recompute == "delta") != (self.cfg.mode == "delta"):
+            raise ConfigError("the delta scope is fixed by cfg.mode")
         _lib.check(self._L.stgn_engine_set_scope(self._handle, _lib.SCOPE[recompute]), "set_scope")
         self.recompute = recompute
 
@@ -803,10 +820,19 @@ class IncrementalEngine:
         c.add("nbr_hit", int(r.nbr_hit))
         c.add("nbr_miss", int(r.nbr_miss))
         c.add("embed_predict", nD)
-        c.add("embed_refresh", nA)
-        c.add("rows_gathered", nA + nD)
-        c.add("macs_attention", self._mac_attn(nA, int(r.entries_affected)) +
-              self._mac_attn(nD, int(r.entries_direct)))
+        if self.recompute == "delta":  # S/engine.py:287-319
+            for k in ("embed_skip", "attn_hit", "attn_miss"):
+                if getattr(r, k):
+                    c.add(k, int(getattr(r, k)))
+            c.add("embed_refresh", nA - int(r.embed_skip))
+            c.add("rows_gathered", int(r.attn_miss) + nD)
+            c.add("macs_attention", self._mac_attn(int(r.attn_miss), int(r.entries_miss)) +
+                  self._mac_attn(nD, int(r.entries_direct)))
+        else:
+            c.add("embed_refresh", nA)
+            c.add("rows_gathered", nA + nD)
+            c.add("macs_attention", self._mac_attn(nA, int(r.entries_affected)) +
+                  self._mac_attn(nD, int(r.entries_direct)))
         c.add("messages", 2 * B)
         c.add("macs_gru", 2 * B * dm.d_m * dm.msg_in +
               nD * 3 * (dm.d_s * dm.d_m + dm.d_s * dm.d_s))

@@ -20,6 +20,11 @@ def engine_cases():
                   for p in glob.glob(os.path.join(GOLDEN, "engine_*.npz")))
 
 
+def delta_cases():
+    return sorted(os.path.basename(p)[len("delta_"):-4]
+                  for p in glob.glob(os.path.join(GOLDEN, "delta_*.npz")))
+
+
 def pipeline_cases():
     return sorted(os.path.basename(p)[len("pipeline_"):-4]
                   for p in glob.glob(os.path.join(GOLDEN, "pipeline_*.npz")))

@@ -45,7 +45,7 @@ def test_struct_layouts_match_header():
     assert C.sizeof(_lib.Dims) == 8 * 4
     assert C.sizeof(_lib.Config) == 4 * 4 + 4 * 8 + 2 * 4
     assert C.sizeof(_lib.Ctl) == 8 + 8 + 4 + 4 + 6 * 8
-    assert C.sizeof(_lib.Report) == 12 * 8 + 8 + 3 * 8
+    assert C.sizeof(_lib.Report) == 12 * 8 + 8 + 4 * 8 + 3 * 8
     assert C.sizeof(_lib.State) == 3 * 8 + len(_lib.STATE_PTRS) * 8
     hdr = _header()
     state_block = hdr[hdr.index("typedef struct {\n  int64_t cap_nodes"):]

@@ -5,7 +5,7 @@ streams. Runs on a B200 under gpurun (`pytest -m gpu`)."""
 import numpy as np
 import pytest
 
-from golden_util import batches, case_setup, engine_cases, load, pipeline_cases
+from golden_util import batches, case_setup, delta_cases, engine_cases, load, pipeline_cases
 from parity_util import PRED_ATOL, assert_rows_close, row_rel_err
 
 pytestmark = pytest.mark.gpu
@@ -41,10 +41,13 @@ def test_pipeline_many_matches_reference(cuda, name):
     np.testing.assert_allclose(zsum, z["zsum"], rtol=1e-4, atol=1e-6)
 
 
-def _run_engine(name, recompute="affected"):
+def _run_engine(name, recompute="affected", prefix="engine_"):
+    import dataclasses
     from paper_2603_21090_b200.engine import IncrementalEngine
-    z = load("engine_" + name)
+    z = load(prefix + name)
     cfg, params, stream = case_setup(z)
+    if prefix == "delta_":
+        cfg = dataclasses.replace(cfg, mode="delta")
     eng = IncrementalEngine(cfg, params, recompute=recompute)
     preds, aff, dirs, kinds, cnts, counters = [], [], [], [], [], []
     keys = list(z["counter_keys"])
@@ -90,6 +93,26 @@ def test_engine_matches_reference(cuda, name):
     assert_rows_close(eng.full_reference(), z["full_reference"], "full_reference")
     assert eng.scheduler.tau == int(z["tau"])
     assert eng.scheduler.global_drift() == pytest.approx(float(z["global_drift"]), rel=1e-12)
+
+
+@pytest.mark.parametrize("name", delta_cases())
+def test_engine_delta_mode_matches_reference(cuda, name):
+    """Delta mode (S/engine.py:276-353) against fixtures the reference wrote
+    with mode="delta": skip / hit / miss classification counters exact."""
+    z, cfg, eng, preds, aff, dirs, kinds, cnts, counters = _run_engine(name, prefix="delta_")
+    assert eng.recompute == "delta"
+    assert np.array_equal(np.array(aff), z["affected"])
+    assert np.array_equal(np.array(dirs), z["direct"])
+    assert np.array_equal(np.array(kinds), z["rebuild_kind"])
+    assert np.array_equal(np.array(cnts), z["rebuild_cnt"])
+    np.testing.assert_array_equal(np.array(counters, dtype=np.float64), z["counters"])
+    n = int(z["node_count"])
+    assert np.max(np.abs(np.array(preds) - z["preds"])) <= PRED_ATOL
+    assert_rows_close(eng.memory.states[:n], z["memory"], "memory")
+    np.testing.assert_array_equal(eng.memory.version[:n], z["version"])
+    assert_rows_close(eng.cache.h[:n].reshape(n, -1), z["h"].reshape(n, -1), "layer cache")
+    np.testing.assert_array_equal(eng.cache.valid_at[:n], z["valid_at"])
+    assert eng.scheduler.tau == int(z["tau"])
 
 
 @pytest.mark.parametrize("name", ["small_mean", "k2_wide_adaptive", "c4_shape_tiny"])
