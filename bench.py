@@ -250,7 +250,7 @@ def run_ours(args, world, rank, local_rank):
     SW = args.sweep_steps
     tail = (W + K + KE + min(KE, 50) + P) * B
     total = max(args.edges, tail + B)
-    n_sweep = sum((3 + SW) * b for b in sweep) + (3 + min(K, 100)) * B + 50 * B  # + direct, sync legs
+    n_sweep = sum((3 + SW) * b for b in sweep) + 2 * (3 + min(K, 100)) * B + 50 * B  # + direct, delta, sync legs
     t_gen = time.perf_counter()
     st = make_stream(args, total + n_sweep, rank)
     t_gen = time.perf_counter() - t_gen
@@ -413,6 +413,28 @@ def run_ours(args, world, rank, local_rank):
         del df
         eng.set_recompute("affected")
 
+    # 3d) the reference's delta mode on the same state (S/engine.py:276-331; K = 2 has no
+    # attention states, so every non-skipped node of A is an attn_miss and is recomputed)
+    delta = None
+    if args.recompute == "affected" and not args.no_direct_leg:
+        eng.set_recompute("delta")
+        KD = min(K, 100)
+        df = DeviceStream(eng, st, B, pos, pos + (3 + KD) * B)
+        df.run(0, 3, report_last=True)
+        d_ms, d_per = _timed_batches(torch, stream, df, 3, KD)
+        d_ms = _max_over_ranks(torch, dist, world, dev, d_ms)
+        r = eng._rep
+        delta = {"value": world * KD * B / (d_ms / 1e3), "unit": UNIT, "steps": KD,
+                 "p50_ms": float(np.percentile(d_per, 50)),
+                 "p99_ms": float(np.percentile(d_per, 99)),
+                 "sample_batch": {"affected": int(r.affected), "embed_skip": int(r.embed_skip),
+                                "attn_hit": int(r.attn_hit), "attn_miss": int(r.attn_miss)},
+                 "note": "cfg.mode = delta: A \\ V_direct nodes with an empty change record "
+                         "keep their cached row; the rest are recomputed"}
+        pos += (3 + KD) * B
+        del df
+        eng.set_recompute("affected")
+
     # 4) batch-size sweep (C4: 100..10K edges/batch) at the end-of-stream state
     sweep_out = []
     for b in sweep:
@@ -472,6 +494,7 @@ def run_ours(args, world, rank, local_rank):
                 "speedup": rb["ms"] / (total_ms / K),
                 "direct_scope_speedup": (rb["ms"] / direct["p50_ms"]) if direct else None},
             "direct_scope": direct,
+            "delta_mode": delta,
             "setup_s": {"generate": t_gen, "fast_forward": t_ff},
         }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

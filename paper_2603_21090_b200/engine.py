@@ -781,8 +781,10 @@ class IncrementalEngine:
         "direct" (value-identical with an infinite window) for later batches."""
         if recompute not in _lib.SCOPE:
             raise ConfigError(f"recompute must be one of {tuple(_lib.SCOPE)}")
-        if (recompute == "delta") != (self.cfg.mode == "delta"):
-            raise ConfigError("the delta scope is fixed by cfg.mode")
+        # single-layer delta mode keeps attention-state stamps from its first batch;
+        # multi-layer models have none (S/engine.py:252-253), so there the switch is exact
+        if self.K == 1 and (recompute == "delta") != (self.cfg.mode == "delta"):
+            raise ConfigError("for single-layer models the delta scope is fixed by cfg.mode")
         _lib.check(self._L.stgn_engine_set_scope(self._handle, _lib.SCOPE[recompute]), "set_scope")
         self.recompute = recompute
 
