@@ -115,6 +115,30 @@ def test_engine_delta_mode_matches_reference(cuda, name):
     assert eng.scheduler.tau == int(z["tau"])
 
 
+@pytest.mark.parametrize("name", ["c4_shape_tiny", "k2_wide_adaptive"])
+def test_delta_mode_on_exact_fixtures(cuda, name):
+    """Multi-layer delta mode has no attention states (S/engine.py:252-253): it
+    only skips untouched affected nodes, so predictions and embeddings must match
+    the reference's exact-mode run while fewer rows are recomputed."""
+    import dataclasses
+    from paper_2603_21090_b200.engine import IncrementalEngine
+    z = load("engine_" + name)
+    cfg, params, stream = case_setup(z)
+    eng = IncrementalEngine(dataclasses.replace(cfg, mode="delta"), params)
+    assert eng.info()["bf16x3"] == 1  # the tcgen05 bf16x3 recompute reads the compacted list
+    preds, skips = [], 0
+    for b in batches(stream, cfg.batch_size):
+        preds.extend(eng.process_batch_arrays(b.src, b.dst, b.t, b.feat).tolist())
+        skips += eng.counters.get("embed_skip")
+        assert eng.counters.get("attn_hit") == 0
+    assert skips > 0
+    n = int(z["node_count"])
+    assert np.max(np.abs(np.array(preds) - z["preds"])) <= PRED_ATOL
+    assert_rows_close(eng.memory.states[:n], z["memory"], "memory")
+    assert_rows_close(eng.cache.h[:n].reshape(n, -1), z["h"].reshape(n, -1), "layer cache")
+    assert_rows_close(eng.full_reference(), z["full_reference"], "full_reference")
+
+
 @pytest.mark.parametrize("name", ["small_mean", "k2_wide_adaptive", "c4_shape_tiny"])
 def test_direct_scope_is_value_identical(cuda, name):
     a = _run_engine(name, "affected")
