@@ -120,7 +120,22 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_fence_init() {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
+// With MBAR_SUSPEND_NS > 0 a waiting thread is suspended by the hardware until
+// the phase completes (or the hint elapses) instead of spinning, so waiting
+// warps stop taking issue slots from the warps they wait for.
+#ifndef MBAR_SUSPEND_NS
+#define MBAR_SUSPEND_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+#if MBAR_SUSPEND_NS > 0
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(phase), "n"(MBAR_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
@@ -128,6 +143,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
       "r"(phase)
       : "memory");
+#endif
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
