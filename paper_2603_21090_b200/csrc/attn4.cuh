@@ -582,8 +582,10 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
   return;
 #endif
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* sbase = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by indexing the shared array (not by integer arithmetic on its
+  // address), so the compiler keeps the shared address space: LDS/STS instead
+  // of generic LD/ST on the row buffers and the cp.async stages
+  unsigned char* sbase = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint16_t* Wb0 = reinterpret_cast<uint16_t*>(sbase);
   uint16_t* Wb1 = reinterpret_cast<uint16_t*>(sbase + w.wblk_bytes);
   float* Ub0 = reinterpret_cast<float*>(sbase + (size_t)w.region_bytes);
