@@ -167,7 +167,7 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
   float* Ur = reinterpret_cast<float*>(smem4);  // [tmax][LDU]  q~ then ubar (both heads)
   float* Cr = Ur + (int64_t)tmax * LDU;          // [tmax][LDC]  c = [c_1..c_H]
   float* Wb = Cr + (int64_t)tmax * LDC;          // staged packed weight block
-  Wb = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(Wb) + 127) & ~uintptr_t(127));
+  Wb += ((128u - (smem_u32(Wb) & 127u)) & 127u) / 4;  // 128-B aligned, still a shared pointer
   __shared__ int s_node[A2_TMAX], s_E[A2_TMAX], s_head[A2_TMAX], s_mode[A2_TMAX];
   __shared__ int s_nnode[A2_TMAX], s_nE[A2_TMAX], s_nhead[A2_TMAX];  // next tile (prefetch)
   __shared__ double s_tref[A2_TMAX];
