@@ -354,7 +354,7 @@ __device__ __forceinline__ void a4_issue_next(const Geo& g, const A4W& w, const 
       const bool ev = e < E;
       int slot = hd + e;
       if (slot >= g.L) slot -= g.L;
-      if (!ev) slot = 0;
+      if (EC > 2 && !ev) slot = 0;  // EC = 2: hd + e < 2L, one wrap keeps it in the ring
       cp_async16(sb + (u * NSEG) * 32, payb + slot * g.ld_d, (ev && lp) ? 16 : 0);
       cp_async16(sb + (u * NSEG + 1) * 32, tbb + slot * g.ld_t, (ev && lt) ? 16 : 0);
       if (KF) cp_async16(sb + (u * NSEG + 2) * 32, ftb + slot * g.ld_e, (ev && lf) ? 16 : 0);
@@ -430,7 +430,7 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
         const bool ev = e < E;
         int slot = hd + e;
         if (slot >= g.L) slot -= g.L;
-        if (!ev) slot = 0;
+        if (EC > 2 && !ev) slot = 0;  // EC = 2: hd + e < 2L, one wrap keeps it in the ring
 #if A4_HINTS
         cp_async16_pol(sb + (u * NSEG) * 32, payb + slot * g.ld_d, (ev && lp) ? 16 : 0, pol_pay);
         cp_async16_pol(sb + (u * NSEG + 1) * 32, tbb + slot * g.ld_t, (ev && lt) ? 16 : 0, pol_tb);
