@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-batches", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--latency-steps", type=int, default=1000,
+                    help="device-timed batches of the end-of-stream latency leg (p50/p99)")
     return ap.parse_args()
 
 
@@ -80,17 +82,16 @@ def workload(args):
     return dims, cfg, init_params(0, dims)
 
 
-def config_json(args, n_gpus, pos0=None):
+def config_json(args, n_gpus):
+    """The workload (identical in both arms); where in the stream each arm's timed
+    batches sit is reported beside it under "timed_batches"."""
     return {"workload": "C4: TGN 2-layer exact-mode incremental inference, synthetic "
                         "preferential power-law stream, drift-aware rebuild",
             "nodes": args.nodes, "batch_edges": args.batch, "fanout_L": 10, "layers_K": 2,
             "d_memory": 100, "d_time": 100, "heads": 2, "d_k": 50, "d_edge": 0,
             "edges": args.edges,
-            "stream": (f"generate_stream(seed={args.seed}+rank, n={args.nodes}, m={args.edges}, "
-                       f"preferential, d_e=0); timed batches are the last of the stream, after "
-                       f"{pos0} edges are ingested" if pos0 is not None else
-                       f"generate_stream(seed={args.seed}, preferential, d_e=0); timed batches "
-                       f"start after the first {args.prefix} edges"),
+            "stream": f"generate_stream(seed={args.seed}, n={args.nodes}, m={args.edges}, "
+                      f"preferential, d_e=0)",
             "rebuild": args.rebuild, "recompute": args.recompute,
             "parallelism": f"replicas{n_gpus}" if n_gpus > 1 else "single",
             "l2": "inputs larger than L2 (26 GB resident state), no flush"}
@@ -152,60 +153,124 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def cpu_reference(args, B_count, stream_edges=None, warmup=0):
-    """Time the oracle port (the reference algorithm restated in float64,
-    numba kernel like the reference's) on the same stream window: fast-
-    forward the prefix exactly (topology, caches, memory, drift), then time
-    B_count full batches. Returns (edges/s, per-batch seconds, sample)."""
-    from oracle.stgn_oracle import Oracle, pipeline_many
-    dims, cfg, params = workload(args)
+REF_PKG = os.path.join(ROOT, "baseline", "_ref")
+
+
+def stock_reference():
+    """The unmodified reference package installed in baseline/_ref (pip --target of
+    /root/reference/pkg), or None when it is not installed there."""
+    if not os.path.isdir(os.path.join(REF_PKG, "streamtgn")):
+        return None
+    os.environ.setdefault("STREAMTGN_NUMBA", "1")
+    if REF_PKG not in sys.path:
+        sys.path.insert(0, REF_PKG)
+    import streamtgn
+    from streamtgn import engine, kernels, params, streamio
+    from streamtgn import config as rconfig
+    assert os.path.dirname(streamtgn.__file__).startswith(REF_PKG), streamtgn.__file__
+    return {"engine": engine, "kernels": kernels, "params": params, "streamio": streamio,
+            "config": rconfig}
+
+
+def _zero_pipeline(qbase, offsets, payload, feat, dt, omega, phi0, wq, wk, wv, wo):
+    """Shape-correct zero outputs of pipeline_many: the fast-forward to the timed
+    stream position skips the attention arithmetic (topology, caches, memory and
+    drift still advance through the stock code); the timed batches run the stock
+    kernel."""
+    N, d, E = qbase.shape[0], qbase.shape[1], payload.shape[0]
+    K, H, _, d_k = wq.shape
+    return (np.zeros((N, K, d)), np.zeros((E, K, H)), np.zeros((E, K, H, d_k)),
+            np.full((N, K, H), -np.inf), np.zeros((N, K, H)), np.zeros((N, K, H, d_k)))
+
+
+def cpu_reference(args, B_count, warmup=1):
+    """Time the reference CPU path on the host: the stock reference from
+    baseline/_ref (IncrementalEngine.process_batch, numba backend) when it is
+    installed, else the oracle port (oracle/, bitwise-pinned to the reference).
+    Both fast-forward the first `args.prefix` edges of the same stream, run
+    `warmup` untimed full batches, then time B_count full batches.
+    Returns (edges/s, per-batch seconds, sample description, kind)."""
     B = args.batch
-    st = stream_edges or make_stream(args, args.prefix + (warmup + B_count) * B, 0)
-    orc = Oracle(cfg, params)
-    # compile the numba kernel outside the timed batches
-    pipeline_many(np.zeros((1, 100)), np.array([0, 1]), np.zeros((1, 2, 100)), np.zeros((1, 0)),
-                  np.zeros(1), params.omega, np.ones(100), params.w_q, params.w_k, params.w_v,
-                  params.w_o)
-    for lo in range(0, args.prefix, B):
-        orc.process_batch(st.src[lo:lo + B], st.dst[lo:lo + B], st.t[lo:lo + B],
-                          st.feat[lo:lo + B], compute=False)
-    for k in range(warmup):  # untimed full batches (caches, numba) before the timed ones
-        lo = args.prefix + k * B
-        orc.process_batch(st.src[lo:lo + B], st.dst[lo:lo + B], st.t[lo:lo + B],
-                          st.feat[lo:lo + B])
+    m = args.prefix + (warmup + B_count) * B
+    ref = stock_reference()
+    if ref is not None:
+        rc = ref["config"]
+        dims = rc.Dims(d_s=100, d_e=0, d_t=100, d_x=0, d_m=100, d_k=50, heads=2, layers=2)
+        cfg = rc.RunConfig(dims=dims, batch_size=B, fanout=10, nodes=args.nodes,
+                           aggregator="last", rebuild=args.rebuild, gamma=0.9, delta_max=0.5,
+                           alpha=0.1, seed=0)
+        params = ref["params"].init_params(0, dims)
+        edges = ref["streamio"].generate_stream(args.seed, args.nodes, m,
+                                                attachment="preferential", d_e=0)
+        eng = ref["engine"].IncrementalEngine(cfg, params)
+        kern = ref["kernels"]
+        stock = kern.pipeline_many
+        kern.pipeline_many = _zero_pipeline
+        try:
+            for lo in range(0, args.prefix, B):
+                eng.process_batch(edges[lo:lo + B])
+        finally:
+            kern.pipeline_many = stock
+        step = lambda lo: eng.process_batch(edges[lo:lo + B])  # noqa: E731
+        what = ("stock reference streamtgn.engine.IncrementalEngine.process_batch from "
+                "baseline/_ref (float64, numba backend, 1 thread)")
+        kind = "reference"
+    else:
+        from oracle.stgn_oracle import Oracle
+        dims, cfg, params = workload(args)
+        st = make_stream(args, m, 0)
+        orc = Oracle(cfg, params)
+        for lo in range(0, args.prefix, B):
+            orc.process_batch(st.src[lo:lo + B], st.dst[lo:lo + B], st.t[lo:lo + B],
+                              st.feat[lo:lo + B], compute=False)
+        step = lambda lo: orc.process_batch(st.src[lo:lo + B], st.dst[lo:lo + B],  # noqa: E731
+                                            st.t[lo:lo + B], st.feat[lo:lo + B])
+        what = "oracle port (float64 numpy+numba, 1 thread; baseline/_ref not installed)"
+        kind = "port"
+    for k in range(warmup):  # untimed full batches (numba compile, caches)
+        step(args.prefix + k * B)
     times = []
     for k in range(warmup, warmup + B_count):
-        lo = args.prefix + k * B
         t0 = time.perf_counter()
-        orc.process_batch(st.src[lo:lo + B], st.dst[lo:lo + B], st.t[lo:lo + B],
-                          st.feat[lo:lo + B])
+        step(args.prefix + k * B)
         times.append(time.perf_counter() - t0)
     times = np.array(times)
     k0 = args.prefix // B + warmup
-    sample = (f"oracle port (float64 numpy+numba, 1 thread) on batches {k0}..{k0 + B_count - 1} "
-              f"of the same stream ({B_count} x {B} edges) after an exact fast-forward through "
-              f"the first {args.prefix} edges and {warmup} untimed batches")
-    return B_count * B / float(times.sum()), times, sample
+    sample = (f"{what} on batches {k0}..{k0 + B_count - 1} of the same stream ({B_count} x {B} "
+              f"edges) after a fast-forward through the first {args.prefix} edges (attention "
+              f"arithmetic skipped there, state advanced by the same code) and {warmup} untimed "
+              f"batches. Bounded sample: the CPU path takes ~1.5 s per batch here and would need "
+              f"~96 GB for the 30M-edge payload store; at the end of the stream its per-batch "
+              f"work (|A|) is ~25x larger, so this sample overstates the CPU's throughput there")
+    return B_count * B / float(times.sum()), times, sample, kind
+
+
+def timed_position(args, pos0=None):
+    if pos0 is None:
+        return (f"bounded CPU sample: batches right after the first {args.prefix} edges of the "
+                f"stream (the GPU arm reports this same position as its 'window' leg)")
+    return (f"the last batches of the {args.edges}-edge stream, after {pos0} edges are ingested "
+            f"(the 'window' leg times the position right after the first {args.prefix} edges)")
 
 
 def run_reference(args, world, rank):
     if rank != 0:
         return
-    dims, cfg, params = workload(args)
-    # one step = one 600-edge batch of the reference algorithm on the host (~0.3-2 s each);
-    # capped so the whole run stays within a few minutes
+    # one step = one 600-edge batch of the reference on the host (~1-2 s each); capped so the
+    # whole run (fast-forward ~1 min + warm-up + steps) stays within a few minutes
     steps = max(1, min(args.steps, 30))
-    warm = max(0, min(args.warmup, 3))
-    value, times, sample = cpu_reference(args, steps, warmup=warm)
+    warm = max(1, min(args.warmup, 5))
+    value, times, sample, kind = cpu_reference(args, steps, warmup=warm)
     ms = float(times.mean() * 1e3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
         "warmup": warm, "ms_per_step": ms, "p50_ms": float(np.percentile(times, 50) * 1e3),
         "p99_ms": float(np.percentile(times, 99) * 1e3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_json(args, 1), "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": sample},
+        "config": config_json(args, world), "impl": "reference",
+        "timed_batches": timed_position(args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind,
+                         "sample": sample, "host_nproc": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -224,6 +289,24 @@ def _timed_batches(torch, stream, feed, k0, K):
     torch.cuda.synchronize()
     per = np.array([ev[k].elapsed_time(ev[k + 1]) for k in range(K)])
     return float(ev[0].elapsed_time(ev[K])), per
+
+
+def _e2e_leg(torch, eng, st, pos, n, B):
+    """n batches from host arrays through StreamingEngine.submit/drain; returns
+    (edges/s, wall seconds) by the host clock around all steps."""
+    from paper_2603_21090_b200.streaming import StreamingEngine
+    se = StreamingEngine(eng, depth=3, max_batch=B)
+    host = [(np.ascontiguousarray(st.src[pos + k * B: pos + (k + 1) * B]),
+             np.ascontiguousarray(st.dst[pos + k * B: pos + (k + 1) * B]),
+             np.ascontiguousarray(st.t[pos + k * B: pos + (k + 1) * B])) for k in range(n)]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s_, d_, t_ in host:
+        se.submit(s_, d_, t_)
+    got = se.drain()
+    wall = time.perf_counter() - t0
+    assert len(got) == n
+    return n * B / wall, wall
 
 
 def _max_over_ranks(torch, dist, world, dev, x):
@@ -248,7 +331,8 @@ def run_ours(args, world, rank, local_rank):
     P = args.profile_batches
     sweep = [int(x) for x in args.sweep.split(",") if x] if args.sweep else []
     SW = args.sweep_steps
-    tail = (W + K + KE + min(KE, 50) + P) * B
+    LAT = args.latency_steps
+    tail = (W + K + LAT + KE + min(KE, 50) + P) * B
     total = max(args.edges, tail + B)
     n_sweep = sum((3 + SW) * b for b in sweep) + 2 * (3 + min(K, 100)) * B + 50 * B  # + direct, delta, sync legs
     t_gen = time.perf_counter()
@@ -270,8 +354,18 @@ def run_ours(args, world, rank, local_rank):
         win = {"value": args.window_steps * B / (w_ms / 1e3), "unit": UNIT,
                "p50_ms": float(np.percentile(w_per, 50)), "p99_ms": float(np.percentile(w_per, 99)),
                "stream_position": f"edges {wk0 * B}..{(wk0 + args.window_steps) * B}",
-               "steps": args.window_steps}
-        feed.run(wk0 + args.window_steps, None, report_last=True)
+               "steps": args.window_steps, "affected_last": None}
+        # the same window end to end through the public streaming API (pinned host batches,
+        # uploads and score read-backs inside the timed region), on the next window_steps batches
+        k_e = wk0 + args.window_steps
+        n_e = min(args.window_steps, feed.n_batches - k_e)
+        eng.sync()
+        e_val, e_wall = _e2e_leg(torch, eng, st, k_e * B, n_e, B)
+        win["e2e"] = {"value": e_val, "unit": UNIT, "steps": n_e, "wall_s": e_wall,
+                      "h2d_bytes_per_step": B * 16, "d2h_bytes_per_step": B * 8,
+                      "stream_position": f"edges {k_e * B}..{(k_e + n_e) * B}"}
+        feed.run(k_e + n_e, None, report_last=True)
+        win["affected_last"] = int(eng._rep.affected)
     else:
         feed.run(0, None, report_last=True)
     eng.sync()
@@ -294,6 +388,20 @@ def run_ours(args, world, rank, local_rank):
     value = world * K * B / (total_ms / 1e3)
     pos = pos0 + (W + K) * B
     del feed
+    # 1b) latency distribution: LAT device-timed batches (CUDA event per batch) right
+    # after the timed ones, at the end-of-stream state (p50/p99 over >= 1,000)
+    lat = None
+    if LAT:
+        lf = DeviceStream(eng, st, B, pos, pos + LAT * B)
+        l_ms, l_per = _timed_batches(torch, stream, lf, 0, LAT)
+        lat = {"steps": LAT, "value": LAT * B / (l_ms / 1e3), "unit": UNIT,
+               "p50_ms": float(np.percentile(l_per, 50)), "p90_ms": float(np.percentile(l_per, 90)),
+               "p99_ms": float(np.percentile(l_per, 99)), "p999_ms": float(np.percentile(l_per, 99.9)),
+               "max_ms": float(l_per.max()),
+               "frac_batches_under_1ms": float(np.mean(l_per < 1.0)),
+               "stream_position": f"edges {pos}..{pos + LAT * B} (end of the stream)"}
+        pos += LAT * B
+        del lf
 
     # 2) e2e: the public streaming API (StreamingEngine): every step copies its
     # batch from pinned host memory to the GPU and reads its scores back to
@@ -462,7 +570,8 @@ def run_ours(args, world, rank, local_rank):
             "p50_ms": float(np.percentile(per, 50)), "p99_ms": float(np.percentile(per, 99)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference generator, native replay; random-init weights)",
-            "config": config_json(args, world, pos0),
+            "config": config_json(args, world),
+            "timed_batches": timed_position(args, pos0),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "StreamingEngine.submit/drain "
                     "(pinned host batches, pipelined uploads and score read-backs), host "
@@ -485,6 +594,7 @@ def run_ours(args, world, rank, local_rank):
             "clocks": clk,
             "engine": info,
             "window": win,
+            "latency": lat,
             "sweep": sweep_out,
             "full_rebuild": rb,
             # the paper's "index refresh" comparison: one full recompute of
@@ -498,8 +608,8 @@ def run_ours(args, world, rank, local_rank):
             "setup_s": {"generate": t_gen, "fast_forward": t_ff},
         }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cv, ctimes, sample = cpu_reference(args, max(1, args.cpu_batches), st)
-        line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": 1, "kind": "port",
+        cv, ctimes, sample, kind = cpu_reference(args, max(1, args.cpu_batches))
+        line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": 1, "kind": kind,
                                 "sample": sample, "p50_ms": float(np.median(ctimes) * 1e3),
                                 "host_nproc": os.cpu_count()}
     if line is not None:

@@ -214,7 +214,7 @@ int stgn_engine_process_batch(stgn_engine* eng, int32_t B, const int32_t* src,
                               int64_t m0, int64_t batch_index, int64_t node_count,
                               double* preds_out, stgn_report* rep, void* stream);
 
-/* Same, inputs already on the device (src/dst int32, t f64, feat f32 [B][ld_e]);
+/* Same, inputs already on the device (src/dst int32, t f64, feat f32 [B][d_e], or NULL for zero features);
  * preds_dev f64 [B] stays on the device; the report is copied to rep (host)
  * only if rep != NULL (that forces a stream sync). */
 int stgn_engine_process_batch_dev(stgn_engine* eng, int32_t B, const int32_t* src_dev,
@@ -264,6 +264,12 @@ int stgn_pipeline_many(const stgn_dims* dims, int64_t N, int64_t E, const float*
 /* Recompute scope for the following batches (STGN_SCOPE_*); DIRECT needs an
  * infinite window (else STGN_ERR_INVALID). */
 int stgn_engine_set_scope(stgn_engine* eng, int scope);
+
+/* State-only fast-forward (test harness, no reference counterpart in the
+ * product API; mirrors the oracle's process_batch(compute=False)): while on,
+ * batches advance topology, rings, memory and drift but launch no attention
+ * recompute, so the layer cache keeps its values. */
+int stgn_engine_set_skip_recompute(stgn_engine* eng, int on);
 
 /* Per-stage device timing (CUDA events; disables graph replay while on).
  * stage_times writes up to cap stage durations (ms) of the last batch and

@@ -28,6 +28,7 @@ EXPORTS = (
     "stgn_engine_set_profiling", "stgn_engine_stage_times", "stgn_stage_name",
     "stgn_engine_info", "stgn_debug_tc_gemm", "stgn_generate_stream",
     "stgn_debug_a4_prof", "stgn_engine_set_scope", "stgn_read_stream",
+    "stgn_engine_set_skip_recompute",
 )
 
 
@@ -118,6 +119,7 @@ def lib():
     L.stgn_debug_tc_gemm.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, vp, C.c_int, vp]
     L.stgn_debug_a4_prof.argtypes = [vp, C.c_int]
     L.stgn_engine_set_scope.argtypes = [vp, C.c_int]
+    L.stgn_engine_set_skip_recompute.argtypes = [vp, C.c_int]
     L.stgn_read_stream.argtypes = [C.c_char_p, i32, i64, P(i64), P(i64), vp, vp, vp, vp, P(i64)]
     L.stgn_generate_stream.argtypes = [vp, i64, i64, i32, dbl, vp, vp, vp, vp]
     for name in EXPORTS:

@@ -101,6 +101,7 @@ struct stgn_engine {
   size_t attn4_smem = 0;
   A4W a4w;
   bool a4_ok = false, use_a4 = false;
+  bool skip_recompute = false;  // state-only fast-forward (tests): no attention launches
   EngW ew;
   size_t mem_smem = 0;
   int mem_wsm = 0;
@@ -418,6 +419,7 @@ static RingSrc ring_src(const stgn_engine* e) {
 
 static void launch_attn(const stgn_engine* e, const RingSrc& rs, cudaStream_t st,
                         bool chain = false) {
+  if (e->skip_recompute) return;
   if (e->use_a4 && chain)
     chain_launch(e->attn4, e->num_sms, A4_THREADS, e->attn4_smem, st, e->g, e->a4w, rs);
   else if (e->use_a4)
@@ -741,8 +743,13 @@ static void fill_hdr(stgn_engine* e, BatchHdr* h, int32_t B, double t_batch, int
   h->node_count = node_count;
   h->t_batch = t_batch;
   h->cutoff = std::isfinite(e->cfg.window) ? t_batch - e->cfg.window : -INFINITY;
-  if (++e->stamp == 0) e->stamp = 1;
-  h->stamp = e->stamp;
+  // The amark/dmark stamp is the engine's batch index (>= 1), which the host
+  // keeps across handle rebuilds: a stamp restarting at 1 in a new handle would
+  // alias the stamps an earlier handle left in the (preserved) node tables.
+  uint32_t stamp = (uint32_t)(batch_index & 0xffffffffll);
+  if (stamp == 0) stamp = 1;
+  e->stamp = stamp;
+  h->stamp = stamp;
 }
 
 extern "C" int stgn_engine_process_batch(stgn_engine* e, int32_t B, const int32_t* src,
@@ -807,9 +814,11 @@ extern "C" int stgn_engine_process_batch_dev(stgn_engine* e, int32_t B, const in
   CUDA_TRY(cudaMemcpyAsync(s.in_src, src_dev, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(s.in_dst, dst_dev, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(s.in_t, t_dev, sizeof(double) * B, cudaMemcpyDeviceToDevice, st));
-  if (e->g.d_e > 0)
+  if (e->g.d_e > 0 && feat_dev)
     k_pack_feat<<<(int)std::min<int64_t>(cdiv((int64_t)B * e->g.d_e, 256), 1024), 256, 0, st>>>(
         feat_dev, s.in_feat, B, e->g.d_e, e->g.ld_e);
+  else if (e->g.d_e > 0)  // no features given: zero rows, as the host-buffer path does
+    CUDA_TRY(cudaMemsetAsync(s.in_feat, 0, sizeof(float) * (size_t)B * e->g.ld_e, st));
   rc = run_sequence(e, st);
   if (rc) return rc;
   if (preds_dev)
@@ -995,6 +1004,17 @@ extern "C" int stgn_engine_info(stgn_engine* e, int64_t* info, int n) {
                          e->use_tc ? 1 : 0, e->attn3_tmax, e->use_a4 ? 1 : 0,
                          (int64_t)e->attn4_smem};
   for (int i = 0; i < n && i < 12; ++i) info[i] = v[i];
+  return STGN_OK;
+}
+
+// State-only fast-forward (test harness): batches advance topology, rings
+// (payloads frozen from the layer cache as it stands), memory and drift, but
+// the attention recomputes are not launched, so the layer cache is not
+// written. Mirrors the oracle's process_batch(compute=False).
+extern "C" int stgn_engine_set_skip_recompute(stgn_engine* e, int on) {
+  if (!e) return STGN_ERR_INVALID;
+  e->skip_recompute = on != 0;
+  drop_graph(e);
   return STGN_OK;
 }
 

@@ -19,6 +19,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 #include "stgn.h"
@@ -278,13 +279,21 @@ extern "C" int stgn_read_stream(const char* path, int32_t sort, int64_t cap, int
   // timestamps must not decrease (S/streamio.py:63-67) unless sort: stable re-sort
   std::vector<int64_t> order((size_t)m);
   for (int64_t i = 0; i < m; ++i) order[(size_t)i] = i;
-  for (int64_t i = 1; i < m; ++i) {
-    if (tv[(size_t)i] < tv[(size_t)i - 1]) {
-      if (!sort) {
-        *bad_line = -1;  // the Python parser reports the exact line
-        return STGN_ERR_INVALID;
-      }
+  // the reference compares each timestamp with the running maximum (NaN never
+  // raises it); any NaN is declined so the Python parser decides, and sorting
+  // NaN keys would break strict weak ordering
+  double run_max = -INFINITY;
+  for (int64_t i = 0; i < m; ++i) {
+    const double ti = tv[(size_t)i];
+    if (std::isnan(ti)) {
+      *bad_line = -1;
+      return STGN_ERR_INVALID;
     }
+    if (ti < run_max && !sort) {
+      *bad_line = -1;  // the Python parser reports the exact line
+      return STGN_ERR_INVALID;
+    }
+    run_max = std::max(run_max, ti);
   }
   if (sort) {
     std::stable_sort(order.begin(), order.end(),

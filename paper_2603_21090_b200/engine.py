@@ -506,6 +506,8 @@ class IncrementalEngine:
         if self._handle is not None:
             self._L.stgn_engine_destroy(self._handle)
         self._handle = h
+        if getattr(self, "_state_only", False):
+            self._L.stgn_engine_set_skip_recompute(h, 1)
 
     def _upload_weights(self):
         torch = self._torch
@@ -788,6 +790,14 @@ class IncrementalEngine:
         _lib.check(self._L.stgn_engine_set_scope(self._handle, _lib.SCOPE[recompute]), "set_scope")
         self.recompute = recompute
 
+    def set_state_only(self, on: bool):
+        """Test-harness fast-forward (the oracle's process_batch(compute=False)):
+        while on, batches advance topology, rings, memory and drift without the
+        attention recomputes, so the layer cache keeps its current rows."""
+        _lib.check(self._L.stgn_engine_set_skip_recompute(self._handle, int(bool(on))),
+                   "set_skip_recompute")
+        self._state_only = bool(on)
+
     # -- profiling ----------------------------------------------------------------
     def set_profiling(self, on: bool):
         _lib.check(self._L.stgn_engine_set_profiling(self._handle, int(bool(on))), "profiling")
@@ -950,6 +960,19 @@ class IncrementalEngine:
         tab.ring_ccnt[:n] = self._torch.where(cc < 0, tab.ring_cnt[:n], cc)
         tab.valid[:n] = 1
         tab.valid_at[:n] = self._t_now if self._m else 0.0
+        if self.recompute == "delta" and self.K == 1:
+            # attention-state stamps of every rebuilt node, as k_rb_fill stamps the local
+            # shard (S/engine.py:393-395): a single-device rebuild stamps all n
+            torch = self._torch
+            tab.attn_ver[:n] = tab.version[:n]
+            head = tab.ring_head[:n].to(torch.int64)
+            tref = tab.ring_t[:n].gather(1, head.unsqueeze(1)).squeeze(1)
+            tab.attn_tref[:n] = torch.where(tab.ring_ccnt[:n] > 0, tref, torch.zeros_like(tref))
+        # rebuild_range counted this rank's shard; a single-device rebuild counts all n
+        from .dist import shard_range
+        import torch.distributed as dist
+        lo, hi = shard_range(n, dist.get_world_size(group), dist.get_rank(group))
+        self.counters.add("rebuild_pipelines", n - (hi - lo))
         return n
 
     # convenience for the scheduler API

@@ -78,6 +78,8 @@ class EdgeRing:
     def enqueue_arrays(self, src, dst, t, feat=None) -> int:
         """Vectorised enqueue; returns how many edges were accepted (a prefix)."""
         src, dst, t = np.asarray(src), np.asarray(dst), np.asarray(t)
+        if feat is None and self.d_e:
+            raise FeatureDimError(f"edge features missing, expected width {self.d_e}")
         if feat is not None and self.d_e and np.asarray(feat).shape[-1] != self.d_e:
             raise FeatureDimError(f"edge features have width {np.asarray(feat).shape[-1]}, "
                                   f"expected {self.d_e}")
@@ -97,7 +99,7 @@ class EdgeRing:
         """Remove and return up to max_count oldest edges (S/graph_store.py:73-92)
         as contiguous arrays (src, dst, t, feat); `before` stops at the first
         edge with t >= before so FIFO order is kept."""
-        n = min(int(max_count), self._size)
+        n = max(0, min(int(max_count), self._size))
         if before is not None and n:
             idx = (self._head + np.arange(n)) % self.capacity
             late = np.nonzero(self.t[idx] >= before)[0]

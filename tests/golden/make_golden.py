@@ -60,7 +60,44 @@ ENGINE_CASES = [
     ("c4_shape_tiny", dict(d_s=100, d_e=0, d_t=100, d_m=100, d_k=50, heads=2, layers=2),
      dict(fanout=10, nodes=3000, aggregator="last"), 0, False,
      dict(seed=2, n=3000, m=3000, attachment="preferential", d_e=0), 600),
+    # round 2: the C2 / C1 widths (d_e = 172, k_in = 372), heads 1 / 3 / 4, a B = 3,000
+    # batch, and the C3 memoryless (TGAT) emulation at the C4 widths
+    ("c2_widths", dict(d_s=100, d_e=172, d_t=100, d_m=100, d_k=50, heads=2, layers=2),
+     dict(fanout=10, nodes=800, aggregator="last", rebuild="adaptive",
+          gamma=0.9, delta_max=0.5, alpha=0.1), 0, False,
+     dict(seed=1, n=800, m=6000, attachment="preferential", d_e=172), 600),
+    ("c1_widths", dict(d_s=100, d_e=172, d_t=100, d_m=100, d_k=50, heads=2, layers=1),
+     dict(fanout=10, nodes=1500, aggregator="last", rebuild="adaptive",
+          gamma=0.9, delta_max=0.5, alpha=0.1), 0, False,
+     dict(seed=0, n=1500, m=6000, attachment="preferential", d_e=172), 200),
+    ("heads1_k2", dict(d_s=8, d_e=2, d_t=8, d_m=8, d_k=6, heads=1, layers=2),
+     dict(fanout=5, nodes=80, aggregator="last", rebuild="adaptive",
+          gamma=0.9, delta_max=1.5, alpha=0.1), 21, True,
+     dict(seed=31, n=80, m=1200, attachment="preferential", d_e=2), 20),
+    ("heads4_k2", dict(d_s=12, d_e=3, d_t=8, d_m=8, d_k=4, heads=4, layers=2),
+     dict(fanout=6, nodes=80, aggregator="mean"), 22, True,
+     dict(seed=32, n=80, m=1200, attachment="preferential", d_e=3), 24),
+    ("heads3_k1", dict(d_s=10, d_e=0, d_t=6, d_m=7, d_k=5, heads=3, layers=1),
+     dict(fanout=7, nodes=60, aggregator="sum", rebuild="fixed", rebuild_interval=9), 23, True,
+     dict(seed=33, n=60, m=900, attachment="uniform", d_e=0), 15),
+    ("b3000", dict(d_s=16, d_e=0, d_t=16, d_m=16, d_k=8, heads=2, layers=2),
+     dict(fanout=10, nodes=20000, aggregator="last"), 0, False,
+     dict(seed=2, n=20000, m=15000, attachment="preferential", d_e=0), 3000),
+    ("c3_memoryless", dict(d_s=100, d_e=0, d_t=100, d_m=100, d_k=50, heads=2, layers=2),
+     dict(fanout=10, nodes=3000, aggregator="last"), "memoryless", False,
+     dict(seed=2, n=3000, m=6000, attachment="preferential", d_e=0), 600),
 ]
+
+GRU_TENSORS = ("w_z", "u_z", "b_z", "w_r", "u_r", "b_r", "w_h", "u_h", "b_h")
+
+
+def memoryless_params(dims):
+    """TGAT emulation: every GRU tensor zero, so s' = 0.5 s + 0.5 tanh(0)
+    and the memory stays 0 (S/kernels/reference.py:87-90, S/engine_base.py:237-241)."""
+    p = init_params(0, dims)
+    for name in GRU_TENSORS:
+        getattr(p, name)[...] = 0.0
+    return p
 
 
 def random_params(seed, dims):
@@ -91,7 +128,10 @@ COUNTER_KEYS = ("nbr_hit", "nbr_miss", "embed_refresh", "embed_predict", "gru_st
 def run_engine_case(name, dkw, ckw, pseed, rand_bias, skw, B):
     dims = Dims(**dkw)
     cfg = RunConfig(dims=dims, batch_size=B, **ckw)
-    params = random_params(pseed, dims) if rand_bias else init_params(pseed, dims)
+    if pseed == "memoryless":
+        params = memoryless_params(dims)
+    else:
+        params = random_params(pseed, dims) if rand_bias else init_params(pseed, dims)
     stream = handmade_stream(dims.d_e) if skw == "handmade" else generate_stream(**skw)
     eng = IncrementalEngine(cfg, params)
     preds, direct, affected, a_off, d_off = [], [], [], [0], [0]
@@ -170,6 +210,12 @@ def run_pipeline_case(name, dims, pseed, n_nodes, max_entries, case_seed):
 
 
 def main():
+    only = [a for a in sys.argv[1:] if not a.startswith("-")]
+    if only:  # regenerate the named engine fixtures only
+        for case in ENGINE_CASES:
+            if case[0] in only:
+                run_engine_case(*case)
+        return
     for case in ENGINE_CASES:
         run_engine_case(*case)
     run_pipeline_case("k1", Dims(d_s=6, d_e=3, d_t=6, d_m=5, d_k=4, heads=2, layers=1),
