@@ -82,6 +82,12 @@ __device__ int g_a4_prof_n;
 #ifndef A4_EC
 #define A4_EC 2  // ring entries per chunk of the walk (2 or 4)
 #endif
+#ifndef A4_TRIG
+#define A4_TRIG 0  // 1: time encoding computed per entry (fp64 phase) instead of read from ring_tb
+#endif
+#ifndef A4_BPF
+#define A4_BPF 0  // 1: TMA bulk L2 prefetch of a tile-layer's payload rows before its Q/K GEMMs
+#endif
 
 
 struct A4W {
@@ -120,7 +126,7 @@ static inline bool a4_plan(const Geo& g, A4W* w) {
   w->ldu = ldu;
   int mb = std::max(std::max(w->Nq * w->Kx, w->Nk * w->Kq), std::max(w->Nv * w->Ku, w->No * w->Kc));
   w->wblk_bytes = (mb * 2 * 2 + 1023) & ~1023;
-  const int stage_bytes = A4_WARPS * A4_NST * A4_EC * (g.d_e > 0 ? 3 : 2) * 32 * 16;
+  const int stage_bytes = A4_WARPS * A4_NST * A4_EC * (g.d_e > 0 ? 3 : 2) * 32 * 16;  // (TRIG: basis segment unused)
   w->region_bytes = std::max(2 * w->wblk_bytes, (stage_bytes + 1023) & ~1023);
   return w->Nk <= 256 && w->Nq <= 256 && w->No <= 256 && w->Ku <= w->Nk &&
          w->Kx + w->Nq <= w->qt0 &&            // ACCQ alive while K_0 writes QT0
@@ -259,6 +265,10 @@ __device__ __forceinline__ void a4_prefetch(const Geo& g, const RingSrc& rs, con
   }
 }
 
+// TMA bulk prefetch of [p, p + bytes) into L2 (16-byte aligned, multiple of 16)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
 // 16-byte global -> shared async copy (L1 bypass); src_bytes = 0 zero-fills
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
@@ -387,9 +397,22 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   const bool lp = lane < kfo / 4, lf = KF && lane < (kto - kfo) / 4, lt = lane < (kp - kto) / 4;
   float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
   // rotation of this row's reference time, frequencies 2l and 2l+1
+#if A4_TRIG
+  // phi(tref - t_e) per entry: lanes 0..E-1 hold t_e, the frequencies 2l, 2l+1 per lane
+  double te = 0.0;
+  if (lane < E) {
+    int s = hd + lane;
+    if (s >= g.L) s -= g.L;
+    te = rs.ring_t[(int64_t)node * g.L + s];
+  }
+  const bool f0 = lt && 2 * lane < g.half, f1 = lt && 2 * lane + 1 < g.half;
+  const double om0 = f0 ? __ldg(w.omega + 2 * lane) : 0.0;
+  const double om1 = f1 ? __ldg(w.omega + 2 * lane + 1) : 0.0;
+#else
   float ca0 = 1.f, sa0 = 0.f, ca1 = 1.f, sa1 = 0.f;
   if (lt && 2 * lane < g.half) phase_sincos(__ldg(w.omega + 2 * lane), tref, &sa0, &ca0);
   if (lt && 2 * lane + 1 < g.half) phase_sincos(__ldg(w.omega + 2 * lane + 1), tref, &sa1, &ca1);
+#endif
   float4 qp[2], qf[2], qt[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -397,8 +420,12 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
     qp[h] = lp ? *reinterpret_cast<const float4*>(Uh + 4 * lane) : zero4;
     qf[h] = lf ? *reinterpret_cast<const float4*>(Uh + kfo + 4 * lane) : zero4;
     float4 q = lt ? *reinterpret_cast<const float4*>(Uh + kto + 4 * lane) : zero4;
+#if A4_TRIG
+    qt[h] = q;
+#else
     qt[h] = make_float4(q.x * ca0 + q.y * sa0, q.x * sa0 - q.y * ca0,
                         q.z * ca1 + q.w * sa1, q.z * sa1 - q.w * ca1);
+#endif
   }
   float2 up[2][2], uf[2][2], ut[2][2];
   float mx[2] = {-INFINITY, -INFINITY}, zs[2] = {0.f, 0.f};
@@ -433,7 +460,7 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
         if (EC > 2 && !ev) slot = 0;  // EC = 2: hd + e < 2L, one wrap keeps it in the ring
 #if A4_HINTS
         cp_async16_pol(sb + (u * NSEG) * 32, payb + slot * g.ld_d, (ev && lp) ? 16 : 0, pol_pay);
-        cp_async16_pol(sb + (u * NSEG + 1) * 32, tbb + slot * g.ld_t, (ev && lt) ? 16 : 0, pol_tb);
+        if (!A4_TRIG) cp_async16_pol(sb + (u * NSEG + 1) * 32, tbb + slot * g.ld_t, (ev && lt) ? 16 : 0, pol_tb);
 #else
         cp_async16(sb + (u * NSEG) * 32, payb + slot * g.ld_d, (ev && lp) ? 16 : 0);
         cp_async16(sb + (u * NSEG + 1) * 32, tbb + slot * g.ld_t, (ev && lt) ? 16 : 0);
@@ -465,7 +492,16 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
 #pragma unroll
       for (int u = 0; u < EC; ++u) {
         kp[u] = sb[(u * NSEG) * 32];
+#if A4_TRIG
+        const double tu = __shfl_sync(0xffffffffu, te, (e0 + u) & 31);
+        const double dt = tref - tu;
+        float s0 = 0.f, c0 = 0.f, s1 = 0.f, c1 = 0.f;
+        if (f0) phase_sincos(om0, dt, &s0, &c0);
+        if (f1) phase_sincos(om1, dt, &s1, &c1);
+        kt[u] = make_float4(c0, s0, c1, s1);
+#else
         kt[u] = sb[(u * NSEG + 1) * 32];
+#endif
         kf[u] = KF ? sb[(u * NSEG + 2) * 32] : zero4;
       }
     }
@@ -564,12 +600,16 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
     if (lf)
       *reinterpret_cast<float4*>(Uh + kfo + 4 * lane) =
           make_float4(uf[h][0].x * inv, uf[h][0].y * inv, uf[h][1].x * inv, uf[h][1].y * inv);
-    if (lt) {  // rotate the accumulated basis back by w tref
+    if (lt) {
       const float uc0 = ut[h][0].x * inv, us0 = ut[h][0].y * inv;
       const float uc1 = ut[h][1].x * inv, us1 = ut[h][1].y * inv;
+#if A4_TRIG
+      *reinterpret_cast<float4*>(Uh + kto + 4 * lane) = make_float4(uc0, us0, uc1, us1);
+#else  // rotate the accumulated basis back by w tref
       *reinterpret_cast<float4*>(Uh + kto + 4 * lane) =
           make_float4(ca0 * uc0 + sa0 * us0, sa0 * uc0 - ca0 * us0, ca1 * uc1 + sa1 * us1,
                       sa1 * uc1 - ca1 * us1);
+#endif
     }
   }
 }
@@ -717,6 +757,17 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
 
     for (int l = 0; l < g.K; ++l) {
       const bool last = (l == g.K - 1);
+#if A4_BPF
+      if (tid < T) {  // this tile-layer's payload rows -> L2, one bulk prefetch per contiguous run
+        const int node = s_node[tid], E = s_E[tid], hd = s_head[tid];
+        if (node >= 0 && E > 0) {
+          const int n1 = min(E, g.L - hd), n2 = E - n1;
+          const float* pay = rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d;
+          bulk_prefetch_l2(pay + (int64_t)hd * g.ld_d, (uint32_t)(n1 * g.ld_d * 4));
+          if (n2 > 0) bulk_prefetch_l2(pay, (uint32_t)(n2 * g.ld_d * 4));
+        }
+      }
+#endif
 #if A4_PREFETCH == 2
       a4_prefetch(g, rs, s_node, s_E, s_head, 0, T, l, tid);  // this layer's ring rows
 #elif A4_PREFETCH == 1
