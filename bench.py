@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-batches", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--config-legs", default="C1,C2,C3",
+                    help="other BASELINE.json configs to run after the C4 legs ('' = none)")
+    ap.add_argument("--c3-edges", type=int, default=30_000_000)
     ap.add_argument("--latency-steps", type=int, default=1000,
                     help="device-timed batches of the end-of-stream latency leg (p50/p99)")
     return ap.parse_args()
@@ -277,6 +280,105 @@ def run_reference(args, world, rank):
 
 
 # ---------------------------------------------------------------------------
+# BASELINE.json configs other than the headline C4; CPU figures are the
+# reference's own process_batch measured in this container
+CONFIGS = {
+    "C1": dict(desc="TGN 1-layer, Wikipedia-shaped stream", nodes=9_227, edges=157_474, d_e=172,
+               layers=1, batch=200, seed=0, memoryless=False,
+               cpu_ref={"p50_ms": 796.0, "p99_ms": 1348.0, "edges_per_s": 267,
+                        "window": "first 20K edges", "full_stream_edges_per_s": 78}),
+    "C2": dict(desc="TGN 2-layer, Reddit-shaped stream", nodes=10_985, edges=672_447, d_e=172,
+               layers=2, batch=600, seed=1, memoryless=False,
+               cpu_ref={"p50_ms": 5462.0, "p99_ms": 10464.0, "edges_per_s": 115,
+                        "window": "first 30K edges"}),
+    "C3": dict(desc="TGAT 2-layer (memoryless: GRU tensors zeroed), power-law 2.6M nodes",
+               nodes=2_600_000, edges=None, d_e=0, layers=2, batch=600, seed=2, memoryless=True,
+               cpu_ref=None),
+}
+
+
+def config_legs(args, torch, dev):
+    """Each config on its own engine: the whole stream fed from HBM, one CUDA event per
+    batch (C1, C2: every batch of the stream is timed; C3: the last 1,000 batches of a
+    --c3-edges stream after a device fast-forward). Mean/max |A| of C1/C2 come from an
+    untimed replay on a second engine that reports every batch."""
+    from paper_2603_21090_b200.config import Dims, RunConfig
+    from paper_2603_21090_b200.engine import IncrementalEngine
+    from paper_2603_21090_b200.feeder import DeviceStream
+    from paper_2603_21090_b200.params import init_params, memoryless
+    from paper_2603_21090_b200.streamio import generate_stream
+    out = {}
+    for name in [c for c in args.config_legs.split(",") if c]:
+        c = CONFIGS[name]
+        m = c["edges"] or args.c3_edges
+        dims = Dims(d_s=100, d_e=c["d_e"], d_t=100, d_x=0, d_m=100, d_k=50, heads=2,
+                    layers=c["layers"])
+        cfg = RunConfig(dims=dims, batch_size=c["batch"], fanout=10, nodes=c["nodes"],
+                        aggregator="last", rebuild="adaptive", gamma=0.9, delta_max=0.5,
+                        alpha=0.1)
+        params = init_params(0, dims)
+        if c["memoryless"]:
+            memoryless(params)
+        t0 = time.perf_counter()
+        st = generate_stream(c["seed"], c["nodes"], m, attachment="preferential", d_e=c["d_e"])
+        t_gen = time.perf_counter() - t0
+        B = c["batch"]
+
+        def fresh():
+            e = IncrementalEngine(cfg, params)
+            e.reserve(nodes=c["nodes"], edges=m + B, batch=B, batches=m // B + 8)
+            return e
+        eng = fresh()
+        stream = torch.cuda.current_stream(dev)
+        nb = -(-m // B)
+        if c["edges"] is None:   # C3: fast-forward, then the last 1,000 batches
+            k_t = max(0, nb - 1000)
+            feed = DeviceStream(eng, st, B)
+            feed.run(0, k_t, report_last=True)
+            a_start = int(eng._rep.affected)
+        else:
+            k_t = 0
+            feed = DeviceStream(eng, st, B)
+        # warm-up: C1/C2 time the whole stream from an empty graph, so the CUDA graph is
+        # captured on a throwaway engine first (same dims, same max batch)
+        if k_t == 0:
+            w_eng = fresh()
+            DeviceStream(w_eng, st, B, 0, 3 * B).run(0, 3, report_last=True)
+            w_eng.sync()
+            del w_eng
+        ms, per = _timed_batches(torch, stream, feed, k_t, nb - k_t)
+        eng.sync()
+        n_t = m - k_t * B
+        leg = {"workload": c["desc"], "nodes": c["nodes"], "edges": m, "d_edge": c["d_e"],
+               "layers_K": c["layers"], "batch_edges": B, "timed_batches": nb - k_t,
+               "timed_edges": n_t, "value": n_t / (ms / 1e3), "unit": UNIT,
+               "p50_ms": float(np.percentile(per, 50)), "p99_ms": float(np.percentile(per, 99)),
+               "generate_s": t_gen, "recompute_kernel": "bf16x3" if eng.info()["bf16x3"] else
+               ("split-tf32" if eng.info()["tensor_cores"] else "ffma"),
+               "memory_kernel": "bf16x3" if eng.info()["memory_bf16x3"] else "ffma",
+               "cpu_reference": c["cpu_ref"]}
+        if c["edges"] is not None:
+            rep = fresh()
+            rf = DeviceStream(rep, st, B)
+            aff = []
+            for k in range(nb):
+                rf.batch(k, report=True)
+                aff.append(int(rep._rep.affected))
+            aff = np.array(aff)
+            leg["affected_mean"] = float(aff.mean())
+            leg["affected_max"] = int(aff.max())
+            leg["affected_frac_mean"] = float(aff.mean() / c["nodes"])
+            del rep, rf
+        else:
+            leg["affected_at_window_start"] = a_start
+            leg["affected_frac_at_window_start"] = a_start / c["nodes"]
+            leg["timed_position"] = f"edges {k_t * B}..{m} (the end of the stream)"
+        out[name] = leg
+        del feed, eng, st
+        torch.cuda.empty_cache()
+    return out
+
+
 def _timed_batches(torch, stream, feed, k0, K):
     """Feed batches k0..k0+K-1 of a DeviceStream, one CUDA event after each;
     returns (total ms, per-batch ms)."""
@@ -557,6 +659,9 @@ def run_ours(args, world, rank, local_rank):
         pos += (3 + SW) * b
         del sf
 
+    # 5) the other configs of BASELINE.json (C1, C2 full streams; C3 TGAT at the C4 scale)
+    cfg_legs = config_legs(args, torch, dev) if (args.config_legs and rank == 0) else None
+
     line = None
     if rank == 0:
         h2d = B * (4 + 4 + 8)
@@ -596,6 +701,7 @@ def run_ours(args, world, rank, local_rank):
             "window": win,
             "latency": lat,
             "sweep": sweep_out,
+            "configs": cfg_legs,
             "full_rebuild": rb,
             # the paper's "index refresh" comparison: one full recompute of
             # every node (the TGL-style / OracleEngine baseline) vs one incremental batch

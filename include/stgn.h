@@ -117,6 +117,16 @@ typedef struct {
    *   t4bq [K][H][Kq] float   phi(0) . w_q[l, h, d:, :] (zero padded) */
   const uint16_t *t4q, *t4k, *t4v, *t4o;
   const float *t4bq;
+  /* bf16x3 tensor-core operands of the memory update (optional; the FFMA
+   * k_memory is used when NULL or when the plan does not fit): the same
+   * K-major bf16 hi/lo block layout, blocks concatenated in this order
+   * (Nm = round_up(d_m,16), Ns = round_up(d_s,16), X2 = [src-side x | dst-side x]):
+   *   ceil(2*msg_in/128) blocks  N = Nm,   K = 128   [w_msg_src | w_msg_dst] columns of X2
+   *   1 block                    N = 2*Ns, K = Nm    [w_z ; w_r] (r at row Ns)
+   *   1 block                    N = 2*Ns, K = Ns    [u_z ; u_r]
+   *   1 block                    N = Ns,   K = Nm    w_h
+   *   1 block                    N = Ns,   K = Ns    u_h */
+  const uint16_t *t4mem;
 } stgn_weights;
 
 /* Persistent control block (device). */

@@ -24,7 +24,12 @@ What it restates (reference = /root/reference/pkg/src/streamtgn, "S/"):
                       _build_attn_state :247-274); a hit's delta_embed
                       update (:43-118) is evaluated as the same softmax
                       over the same frozen-payload key rows, so hits agree
-                      with the reference to rounding, not bitwise
+                      with the reference to rounding, not bitwise;
+                      the per-hit error-bound record DeltaEvent(bound =
+                      |dN|/|N| * max_v * z_dev) of _apply_delta (:333-353)
+                      and max_value_norm_seen (:255-261, :349) follow from
+                      the log-partition (log Z) of each node's last state
+                      build and the value-row norms of the recompute
 
 Pinning: tests/test_golden_oracle.py checks this module against fixtures
 written by the reference itself (tests/golden/make_golden.py) — bitwise
@@ -230,6 +235,9 @@ class Oracle:
             raise ValueError(f"unknown mode {cfg.mode}")
         self.delta = cfg.mode == "delta"
         self.attn: dict[int, tuple] = {}  # delta mode: node -> (mem_version, t_ref) of its AttnState
+        self.logz: dict[int, np.ndarray] = {}  # delta mode: node -> log Z per head of that state
+        self.max_value_norm_seen = 0.0
+        self.delta_events: list[dict] = []
         self.cfg, self.p = cfg, params
         dm = params.dims
         self.K, self.d, self.L = dm.layers, dm.d, cfg.fanout
@@ -295,7 +303,7 @@ class Oracle:
         return st
 
     # -- pipeline over a node list (S/engine_base.py:139-189) ---------------
-    def _pipeline(self, ids, lists, pending, count=True):
+    def _pipeline(self, ids, lists, pending, count=True, full=False):
         p = self.p
         dm = p.dims
         N = len(ids)
@@ -327,16 +335,49 @@ class Oracle:
             per_node = dm.heads * dm.query_in * dm.d_k + dm.heads * dm.d_k * dm.d
             per_entry = dm.heads * (2 * dm.key_in * dm.d_k + 2 * dm.d_k)
             self._count("macs_attention", dm.layers * (N * per_node + E * per_entry))
-        return pipeline_many(qbase, offs, payload, feat, dt, p.omega, self.phi0,
-                             p.w_q, p.w_k, p.w_v, p.w_o)[0]
+        res = pipeline_many(qbase, offs, payload, feat, dt, p.omega, self.phi0,
+                            p.w_q, p.w_k, p.w_v, p.w_o)
+        return (res, offs) if full else res[0]
 
-    def _recompute(self, ids, valid_at, count=True, keep_states=True):
+    def _state_stats(self, res, offs, i):
+        """(log Z per head, max value-row norm) of row i of a layer-0 pipeline
+        result: _log_z / _max_value_norm (S/engine.py:121-134) of the state
+        _build_attn_state (:247-274) would build from it."""
+        _, _, values, maxlog, zsum, _ = res
+        lo, hi = int(offs[i]), int(offs[i + 1])
+        H = zsum.shape[2]
+        lz = np.array([np.log(zsum[i, 0, h]) + maxlog[i, 0, h] if zsum[i, 0, h] > 0 else -np.inf
+                       for h in range(H)])
+        mv = 0.0
+        if hi > lo:
+            mv = float(np.max(np.linalg.norm(values[lo:hi, 0], axis=-1)))
+        return lz, mv
+
+    def _recompute(self, ids, valid_at, count=True, keep_states=True, hits=None, sizes=None):
         lists = [self.cache.get(v) or [] for v in ids]
-        out = self._pipeline(ids, lists, self._pending, count)
+        track = self.delta and self.K == 1
+        res, offs = self._pipeline(ids, lists, self._pending, count, full=True)
+        out = res[0]
         for i, v in enumerate(ids):
             self.h[v] = out[i]
             self.valid[v] = True
             self.valid_at[v] = valid_at
+            if track and (keep_states or hits):
+                lz, mv = self._state_stats(res, offs, i)
+                self.max_value_norm_seen = max(self.max_value_norm_seen, mv)
+                if hits:  # _apply_delta: the bound record of this update
+                    old = self.logz.get(v, np.full(len(lz), -np.inf))
+                    z_dev = 0.0
+                    for h in range(len(lz)):
+                        if np.isfinite(lz[h]):
+                            ratio = np.exp(old[h] - lz[h]) if np.isfinite(old[h]) else 0.0
+                            z_dev = max(z_dev, abs(1.0 - ratio))
+                    nv = max(len(lists[i]), 1)
+                    self.delta_events.append(dict(
+                        node=v, embedding=out[i, self.K - 1].copy(),
+                        bound=(sizes[v] / nv) * mv * z_dev, dn=sizes[v], nv=nv, max_v=mv,
+                        z_dev=z_dev))
+                self.logz[v] = lz
         if keep_states:
             self._stamp(ids)
         return out
@@ -371,7 +412,8 @@ class Oracle:
         if compute:
             for lst, cnt in ((misses, True), (hits, False)):
                 if lst:
-                    res = self._recompute(lst, t_batch, count=cnt, keep_states=cnt)
+                    res = self._recompute(lst, t_batch, count=cnt, keep_states=cnt,
+                                          hits=not cnt, sizes=sizes)
                     for j, v in enumerate(lst):
                         out[pos[v]] = res[j]
         else:
@@ -396,6 +438,7 @@ class Oracle:
             raise ValueError("compute=False fast-forward is exact-mode only")
         self._compute = compute
         self.counters = {}
+        self.delta_events = []
         self.last_pred_h = {}
         src = np.asarray(src, dtype=np.int64)
         dst = np.asarray(dst, dtype=np.int64)

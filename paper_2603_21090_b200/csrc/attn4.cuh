@@ -82,11 +82,21 @@ __device__ int g_a4_prof_n;
 #ifndef A4_EC
 #define A4_EC 2  // ring entries per chunk of the walk (2 or 4)
 #endif
+#ifndef A4_WALK
+#define A4_WALK 1  // 1: per-lane cp.async chunks of A4_EC entries; 2: TMA bulk-copied chunks of A4_EC2 entries
+#endif
+#ifndef A4_EC2
+#define A4_EC2 4  // ring entries per bulk-copied chunk (walk 2); two chunk stages per warp
+#endif
 #ifndef A4_TRIG
 #define A4_TRIG 0  // 1: time encoding computed per entry (fp64 phase) instead of read from ring_tb
 #endif
 #ifndef A4_BPF
-#define A4_BPF 0  // 1: TMA bulk L2 prefetch of a tile-layer's payload rows before its Q/K GEMMs
+#define A4_BPF 0  // 1: TMA bulk L2 prefetch of a tile-layer's payload rows before its Q/K GEMMs;
+                  // 2: rolling, A4_PFD rows ahead of the walk (payload and basis)
+#endif
+#ifndef A4_PFD
+#define A4_PFD 32
 #endif
 
 
@@ -126,7 +136,12 @@ static inline bool a4_plan(const Geo& g, A4W* w) {
   w->ldu = ldu;
   int mb = std::max(std::max(w->Nq * w->Kx, w->Nk * w->Kq), std::max(w->Nv * w->Ku, w->No * w->Kc));
   w->wblk_bytes = (mb * 2 * 2 + 1023) & ~1023;
+#if A4_WALK == 2
+  // two chunk stages per warp: [A4_EC2][ld_d] payload, [A4_EC2][ld_t] basis, [A4_EC2][ld_e] features
+  const int stage_bytes = A4_WARPS * 2 * A4_EC2 * (g.ld_d + g.ld_t + (g.d_e > 0 ? g.ld_e : 0)) * 4;
+#else
   const int stage_bytes = A4_WARPS * A4_NST * A4_EC * (g.d_e > 0 ? 3 : 2) * 32 * 16;  // (TRIG: basis segment unused)
+#endif
   w->region_bytes = std::max(2 * w->wblk_bytes, (stage_bytes + 1023) & ~1023);
   return w->Nk <= 256 && w->Nq <= 256 && w->No <= 256 && w->Ku <= w->Nk &&
          w->Kx + w->Nq <= w->qt0 &&            // ACCQ alive while K_0 writes QT0
@@ -268,6 +283,20 @@ __device__ __forceinline__ void a4_prefetch(const Geo& g, const RingSrc& rs, con
 // TMA bulk prefetch of [p, p + bytes) into L2 (16-byte aligned, multiple of 16)
 __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+// one lane: bulk L2 prefetch of layer l's payload and time-basis runs of a ring row
+__device__ __forceinline__ void a4_row_prefetch(const Geo& g, const RingSrc& rs, int node, int E,
+                                                int hd, int l) {
+  if (node < 0 || E <= 0) return;
+  const int n1 = min(E, g.L - hd), n2 = E - n1;
+  const float* pay = rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d;
+  const float* tb = rs.ring_tb + (int64_t)node * g.L * g.ld_t;
+  bulk_prefetch_l2(pay + (int64_t)hd * g.ld_d, (uint32_t)(n1 * g.ld_d * 4));
+  bulk_prefetch_l2(tb + (int64_t)hd * g.ld_t, (uint32_t)(n1 * g.ld_t * 4));
+  if (n2 > 0) {
+    bulk_prefetch_l2(pay, (uint32_t)(n2 * g.ld_d * 4));
+    bulk_prefetch_l2(tb, (uint32_t)(n2 * g.ld_t * 4));
+  }
 }
 // 16-byte global -> shared async copy (L1 bypass); src_bytes = 0 zero-fills
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
@@ -614,6 +643,225 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   }
 }
 
+// Walk 2: the rows of one 32-row quadrant, warp per row, taken from a shared
+// counter. Ring rows reach shared memory as TMA bulk copies: one lane issues
+// a chunk of A4_EC2 entries (payload, time basis and features of consecutive
+// ring slots: at most two contiguous runs each, as the ring may wrap) into one
+// of the warp's two stages, completing on the stage's mbarrier; the next
+// chunk (of this row or of the next row, taken one ahead) is always in flight
+// while one is reduced. No per-lane copy issue, no address arithmetic per lane.
+// Per chunk: logits of both heads (packed FMAs, one transposing butterfly),
+// online softmax update, ubar accumulation. Math as a4_walk_row.
+struct A4Stg {
+  float* base;     // this warp's two stages
+  uint64_t* bar;   // this warp's two stage mbarriers
+  int stg_floats;  // floats per stage
+  uint32_t n_iss, n_con;  // chunks issued / consumed by this warp (stage = n & 1, parity = (n >> 1) & 1)
+};
+
+template <int KF>
+__device__ __forceinline__ void a4_issue2(const Geo& g, const RingSrc& rs, A4Stg& S, int node,
+                                          int E, int hd, int c, int l, int lane) {
+  constexpr int EC = A4_EC2;
+  const int st = (int)(S.n_iss & 1u);
+  ++S.n_iss;
+  if (lane == 0) {
+    const int e0 = c * EC;
+    const int n = min(EC, E - e0);
+    int s0 = hd + e0;
+    if (s0 >= g.L) s0 -= g.L;
+    const int n1 = min(n, g.L - s0), n2 = n - n1;
+    uint64_t* bar = S.bar + st;
+    const uint32_t per = (uint32_t)(g.ld_d + g.ld_t + (KF ? g.ld_e : 0)) * 4u;
+    mbar_expect_tx(bar, (uint32_t)n * per);
+    float* dst = S.base + st * S.stg_floats;
+    const float* pay = rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d;
+    const float* tb = rs.ring_tb + (int64_t)node * g.L * g.ld_t;
+    bulk_g2s(dst, pay + (int64_t)s0 * g.ld_d, (uint32_t)(n1 * g.ld_d * 4), bar);
+    if (n2 > 0) bulk_g2s(dst + n1 * g.ld_d, pay, (uint32_t)(n2 * g.ld_d * 4), bar);
+    float* dtb = dst + EC * g.ld_d;
+    bulk_g2s(dtb, tb + (int64_t)s0 * g.ld_t, (uint32_t)(n1 * g.ld_t * 4), bar);
+    if (n2 > 0) bulk_g2s(dtb + n1 * g.ld_t, tb, (uint32_t)(n2 * g.ld_t * 4), bar);
+    if (KF) {
+      const float* ft = rs.ring_feat + (int64_t)node * g.L * g.ld_e;
+      float* dft = dtb + EC * g.ld_t;
+      bulk_g2s(dft, ft + (int64_t)s0 * g.ld_e, (uint32_t)(n1 * g.ld_e * 4), bar);
+      if (n2 > 0) bulk_g2s(dft + n1 * g.ld_e, ft, (uint32_t)(n2 * g.ld_e * 4), bar);
+    }
+  }
+}
+
+template <int KF>
+__device__ __forceinline__ void a4_walk2_quadrant(const Geo& g, const A4W& w, const RingSrc& rs,
+                                                  float* Ub, int q, int nrows, int* ctr,
+                                                  const int* s_node, const int* s_E,
+                                                  const int* s_head, const double* s_tref, int l,
+                                                  int lane, A4Stg& S, int T) {
+  constexpr int EC = A4_EC2;
+  const int kfo = w.kfo, kto = w.kto, kp = w.kpad;
+  const bool lp = lane < kfo / 4, lf = KF && lane < (kto - kfo) / 4, lt = lane < (kp - kto) / 4;
+  const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto grab = [&]() {
+    int i = 0;
+    for (;;) {
+      if (lane == 0) i = atomicAdd(ctr, 1);
+      i = __shfl_sync(0xffffffffu, i, 0);
+#if A4_BPF == 2
+      if (lane == 0 && i < nrows && 32 * q + i + A4_PFD < T) {
+        const int rp = 32 * q + i + A4_PFD;
+        a4_row_prefetch(g, rs, s_node[rp], s_E[rp], s_head[rp], l);
+      }
+#endif
+      if (i >= nrows || s_node[32 * q + i] >= 0) return i;
+    }
+  };
+  int i = grab();
+  if (i < nrows && s_E[32 * q + i] > 0)
+    a4_issue2<KF>(g, rs, S, s_node[32 * q + i], s_E[32 * q + i], s_head[32 * q + i], 0, l, lane);
+  while (i < nrows) {
+    const int r = 32 * q + i;
+    const int nx = grab();  // next row, one ahead: its first chunk is issued during this row's last
+    const int rn = 32 * q + nx;
+    const bool nx_issue = nx < nrows && s_E[rn] > 0;
+    const int node = s_node[r], E = s_E[r], hd = s_head[r];
+    const double tref = s_tref[r];
+    float* U = Ub + i * w.ldu;
+    if (E == 0 && nx_issue) a4_issue2<KF>(g, rs, S, s_node[rn], s_E[rn], s_head[rn], 0, l, lane);
+    float ca0 = 1.f, sa0 = 0.f, ca1 = 1.f, sa1 = 0.f;
+    if (lt && 2 * lane < g.half) phase_sincos(__ldg(w.omega + 2 * lane), tref, &sa0, &ca0);
+    if (lt && 2 * lane + 1 < g.half) phase_sincos(__ldg(w.omega + 2 * lane + 1), tref, &sa1, &ca1);
+    float4 qp[2], qf[2], qt[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float* Uh = U + h * kp;
+      qp[h] = lp ? *reinterpret_cast<const float4*>(Uh + 4 * lane) : zero4;
+      qf[h] = lf ? *reinterpret_cast<const float4*>(Uh + kfo + 4 * lane) : zero4;
+      const float4 qq = lt ? *reinterpret_cast<const float4*>(Uh + kto + 4 * lane) : zero4;
+      qt[h] = make_float4(qq.x * ca0 + qq.y * sa0, qq.x * sa0 - qq.y * ca0,
+                          qq.z * ca1 + qq.w * sa1, qq.z * sa1 - qq.w * ca1);
+    }
+    float2 up[2][2], uf[2][2], ut[2][2];
+    float mx[2] = {-INFINITY, -INFINITY}, zs[2] = {0.f, 0.f};
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) up[h][c] = uf[h][c] = ut[h][c] = make_float2(0.f, 0.f);
+    const int nch = (E + EC - 1) / EC;
+    for (int c = 0; c < nch; ++c) {
+      if (c + 1 < nch) a4_issue2<KF>(g, rs, S, node, E, hd, c + 1, l, lane);
+      else if (nx_issue) a4_issue2<KF>(g, rs, S, s_node[rn], s_E[rn], s_head[rn], 0, l, lane);
+      const int st = (int)(S.n_con & 1u);
+      mbar_wait(S.bar + st, (S.n_con >> 1) & 1u);
+      ++S.n_con;
+      const int e0 = c * EC;
+      const float* sp = S.base + st * S.stg_floats;
+      const float* stb = sp + EC * g.ld_d;
+      const float* sft = stb + EC * g.ld_t;
+      float4 kpv[EC], ktv[EC], kfv[EC];
+#pragma unroll
+      for (int u = 0; u < EC; ++u) {
+        const bool ev = e0 + u < E;  // warp-uniform; slots past E hold stale bytes: zero them
+        kpv[u] = (ev && lp) ? *reinterpret_cast<const float4*>(sp + u * g.ld_d + 4 * lane) : zero4;
+        ktv[u] = (ev && lt) ? *reinterpret_cast<const float4*>(stb + u * g.ld_t + 4 * lane) : zero4;
+        kfv[u] = (KF && ev && lf) ? *reinterpret_cast<const float4*>(sft + u * g.ld_e + 4 * lane) : zero4;
+      }
+      __syncwarp();  // every lane has its chunk in registers: the stage may be refilled
+      float part[2 * EC];
+#pragma unroll
+      for (int u = 0; u < EC; ++u) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float2 a = fmul2(make_float2(qp[h].x, qp[h].y), make_float2(kpv[u].x, kpv[u].y));
+          a = ffma2(make_float2(qp[h].z, qp[h].w), make_float2(kpv[u].z, kpv[u].w), a);
+          a = ffma2(make_float2(qt[h].x, qt[h].y), make_float2(ktv[u].x, ktv[u].y), a);
+          a = ffma2(make_float2(qt[h].z, qt[h].w), make_float2(ktv[u].z, ktv[u].w), a);
+          if (KF) {
+            a = ffma2(make_float2(qf[h].x, qf[h].y), make_float2(kfv[u].x, kfv[u].y), a);
+            a = ffma2(make_float2(qf[h].z, qf[h].w), make_float2(kfv[u].z, kfv[u].w), a);
+          }
+          part[2 * u + h] = a.x + a.y;
+        }
+      }
+      // transposing butterfly over the 2*EC values; value v ends on lanes [v*32/(2EC), ...)
+      float lg[2 * EC];
+      {
+        constexpr int V = 2 * EC;
+#pragma unroll
+        for (int m = 16, nv = V; m >= 1; m >>= 1) {
+          if (nv > 1) {
+            const bool hi = lane & m;
+#pragma unroll
+            for (int j = 0; j < nv / 2; ++j) {
+              const float send = hi ? part[j] : part[j + nv / 2];
+              const float keep = hi ? part[j + nv / 2] : part[j];
+              part[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+            }
+            nv >>= 1;
+          } else {
+            part[0] += __shfl_xor_sync(0xffffffffu, part[0], m);
+          }
+        }
+        constexpr int stride = 32 / V;
+#pragma unroll
+        for (int v = 0; v < V; ++v) lg[v] = __shfl_sync(0xffffffffu, part[0], stride * v);
+      }
+#pragma unroll
+      for (int u = 1; u < EC; ++u)
+        if (e0 + u >= E) lg[2 * u] = lg[2 * u + 1] = -INFINITY;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float cm = lg[h];
+#pragma unroll
+        for (int u = 1; u < EC; ++u) cm = fmaxf(cm, lg[2 * u + h]);
+        const float nm = fmaxf(mx[h], cm);
+        const float sc = ex2f(mx[h] - nm);
+        const float2 sc2 = make_float2(sc, sc);
+        zs[h] *= sc;
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          up[h][cc] = fmul2(up[h][cc], sc2);
+          ut[h][cc] = fmul2(ut[h][cc], sc2);
+          if (KF) uf[h][cc] = fmul2(uf[h][cc], sc2);
+        }
+#pragma unroll
+        for (int u = 0; u < EC; ++u) {
+          const float pr = ex2f(lg[2 * u + h] - nm);
+          const float2 p2 = make_float2(pr, pr);
+          zs[h] += pr;
+          up[h][0] = ffma2(p2, make_float2(kpv[u].x, kpv[u].y), up[h][0]);
+          up[h][1] = ffma2(p2, make_float2(kpv[u].z, kpv[u].w), up[h][1]);
+          ut[h][0] = ffma2(p2, make_float2(ktv[u].x, ktv[u].y), ut[h][0]);
+          ut[h][1] = ffma2(p2, make_float2(ktv[u].z, ktv[u].w), ut[h][1]);
+          if (KF) {
+            uf[h][0] = ffma2(p2, make_float2(kfv[u].x, kfv[u].y), uf[h][0]);
+            uf[h][1] = ffma2(p2, make_float2(kfv[u].z, kfv[u].w), uf[h][1]);
+          }
+        }
+        mx[h] = nm;
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float* Uh = U + h * kp;
+      const float inv = E > 0 ? 1.f / zs[h] : 0.f;
+      if (lp)
+        *reinterpret_cast<float4*>(Uh + 4 * lane) =
+            make_float4(up[h][0].x * inv, up[h][0].y * inv, up[h][1].x * inv, up[h][1].y * inv);
+      if (lf)
+        *reinterpret_cast<float4*>(Uh + kfo + 4 * lane) =
+            make_float4(uf[h][0].x * inv, uf[h][0].y * inv, uf[h][1].x * inv, uf[h][1].y * inv);
+      if (lt) {  // rotate the accumulated basis back by w tref
+        const float uc0 = ut[h][0].x * inv, us0 = ut[h][0].y * inv;
+        const float uc1 = ut[h][1].x * inv, us1 = ut[h][1].y * inv;
+        *reinterpret_cast<float4*>(Uh + kto + 4 * lane) =
+            make_float4(ca0 * uc0 + sa0 * us0, sa0 * uc0 - ca0 * us0, ca1 * uc1 + sa1 * us1,
+                        sa1 * uc1 - ca1 * us1);
+      }
+    }
+    i = nx;
+  }
+}
+
 template <int KF>
 __global__ void __launch_bounds__(A4_THREADS, 1)
 attn4_kernel(Geo g, A4W w, RingSrc rs) {
@@ -634,6 +882,9 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
   __shared__ double s_tref[A4_TMAX];
   __shared__ uint64_t mbar, wbar[2];
   __shared__ uint64_t qbar_full[2], qbar_done[2], qbar_packed[2];
+#if A4_WALK == 2
+  __shared__ uint64_t sbar2[2 * A4_WARPS];
+#endif
   __shared__ int qctr[2];
   __shared__ uint32_t tslot;
 
@@ -661,6 +912,9 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
       mbar_init(&qbar_done[b], A4_THREADS);
       mbar_init(&qbar_packed[b], 32 * A4_NCG);
     }
+#if A4_WALK == 2
+    for (int b = 0; b < 2 * A4_WARPS; ++b) mbar_init(&sbar2[b], 1);
+#endif
     mbar_fence_init();
   }
   tc_fence_before();
@@ -681,6 +935,13 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
   // the walk's per-warp cp.async stages live in the two weight buffers: V_0 and
   // V_1 (blocks 3, 4 of a layer) are staged after the walk instead of during it
   float4* stg_warp = reinterpret_cast<float4*>(sbase) + (size_t)warp * A4_NST * A4_EC * (KF ? 3 : 2) * 32;
+#if A4_WALK == 2
+  A4Stg S2;
+  S2.stg_floats = A4_EC2 * (g.ld_d + g.ld_t + (KF ? g.ld_e : 0));
+  S2.base = reinterpret_cast<float*>(sbase) + (size_t)warp * 2 * S2.stg_floats;
+  S2.bar = sbar2 + 2 * warp;
+  S2.n_iss = S2.n_con = 0;
+#endif
   auto deferred = [&](int64_t Gb) { const int j = (int)(Gb % 6); return j == 3 || j == 4; };
   int64_t G = 0;  // weight blocks consumed by this CTA
   int ub_use[2] = {0, 0};  // uses of each quadrant row buffer so far (mbarrier phases)
@@ -757,7 +1018,9 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
 
     for (int l = 0; l < g.K; ++l) {
       const bool last = (l == g.K - 1);
-#if A4_BPF
+#if A4_BPF == 2
+      if (tid < min(A4_PFD, T)) a4_row_prefetch(g, rs, s_node[tid], s_E[tid], s_head[tid], l);
+#elif A4_BPF
       if (tid < T) {  // this tile-layer's payload rows -> L2, one bulk prefetch per contiguous run
         const int node = s_node[tid], E = s_E[tid], hd = s_head[tid];
         if (node >= 0 && E > 0) {
@@ -850,6 +1113,9 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
           a4_walk_row<KF>(g, w, rs, Ub + i * w.ldu, s_node[r], s_E[r], s_head[r], s_tref[r], l,
                           lane, stg_warp, issue_next, &kcons);
         }
+#elif A4_WALK == 2
+        a4_walk2_quadrant<KF>(g, w, rs, Ub, q, nrows, &qctr[b], s_node, s_E, s_head, s_tref, l,
+                              lane, S2, T);
 #else
         for (;;) {
           int i = 0;
@@ -857,6 +1123,10 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
           i = __shfl_sync(0xffffffffu, i, 0);
           if (i >= nrows) break;
           const int r = 32 * q + i;
+#if A4_BPF == 2
+          if (lane == 0 && r + A4_PFD < T)
+            a4_row_prefetch(g, rs, s_node[r + A4_PFD], s_E[r + A4_PFD], s_head[r + A4_PFD], l);
+#endif
           if (s_node[r] < 0) continue;
           a4_walk_row<KF>(g, w, rs, Ub + i * w.ldu, s_node[r], s_E[r], s_head[r], s_tref[r], l,
                           lane, stg_warp, [] {}, nullptr);

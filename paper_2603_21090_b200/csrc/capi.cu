@@ -12,6 +12,7 @@
 #include "batch.cuh"
 #include "attn3.cuh"
 #include "attn4.cuh"
+#include "mem4.cuh"
 
 #ifndef STGN_VERSION
 #define STGN_VERSION "stgn 0.1.0 sm_100a"
@@ -101,6 +102,9 @@ struct stgn_engine {
   size_t attn4_smem = 0;
   A4W a4w;
   bool a4_ok = false, use_a4 = false;
+  M4W m4w;                      // bf16x3 tcgen05 memory update (when the plan fits)
+  size_t mem4_smem = 0;
+  bool m4_ok = false, use_m4 = false;
   bool skip_recompute = false;  // state-only fast-forward (tests): no attention launches
   EngW ew;
   size_t mem_smem = 0;
@@ -241,6 +245,14 @@ int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engin
                                     (int)e->attn4_smem) == cudaSuccess;
     cudaGetLastError();
   }
+  memset(&e->m4w, 0, sizeof(e->m4w));
+  if (m4_plan(e->g, &e->m4w)) {
+    e->mem4_smem = mem4_smem_bytes(e->m4w);
+    e->m4_ok = cudaFuncSetAttribute((const void*)mem4_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)e->mem4_smem) == cudaSuccess;
+    cudaGetLastError();
+  }
   ce = cudaFuncSetAttribute((const void*)e->attn2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)e->attn2_smem);
   if (ce != cudaSuccess) {
@@ -349,6 +361,8 @@ int stgn_engine_set_weights(stgn_engine* e, const stgn_weights* w) {
     e->a4w.bq = w->t4bq;
     e->a4w.omega = w->omega;
   }
+  e->use_m4 = e->m4_ok && w->t4mem;
+  if (e->use_m4) e->m4w.wblk = w->t4mem;
   e->aw.wq = w->wq;
   e->aw.wkt = w->wkt;
   e->aw.wv = w->wv;
@@ -440,6 +454,11 @@ static const char* kStageNames[] = {"group+ring", "affected_bfs", "change_record
 static void launch_memory(const stgn_engine* e, cudaStream_t st) {
   const Geo& g = e->g;
   const int64_t R = 2 * (int64_t)e->cfg.max_batch;
+  if (e->use_m4) {
+    mem4_kernel<<<(int)std::min<int64_t>(cdiv(R, 128), e->num_sms), M4_THREADS, e->mem4_smem, st>>>(
+        g, e->sv, e->sc, e->m4w, e->w.bmsg, e->w.omega, e->w.bgru, e->cfg.aggregator);
+    return;
+  }
   k_memory<<<(int)std::min<int64_t>(cdiv(R, GRU_T), e->num_sms), MG_THREADS, e->mem_smem, st>>>(
       g, e->sv, e->sc, e->w.wmsg, e->w.bmsg, e->w.omega, e->w.wgru, e->w.ugru, e->w.bgru,
       e->cfg.aggregator, (int)round_up(g.d_m, 4), (int)round_up(g.d_s, 4), e->mem_wsm);
@@ -999,11 +1018,11 @@ extern "C" int stgn_pipeline_many(const stgn_dims* dims, int64_t N, int64_t E, c
 
 extern "C" int stgn_engine_info(stgn_engine* e, int64_t* info, int n) {
   if (!e || !info) return STGN_ERR_INVALID;
-  const int64_t v[12] = {e->graph ? 1 : 0, e->cond_used ? 1 : 0, e->launches, e->attn2_tmax,
+  const int64_t v[14] = {e->graph ? 1 : 0, e->cond_used ? 1 : 0, e->launches, e->attn2_tmax,
                          e->attn2_wsm, e->num_sms, (int64_t)e->attn2_smem, (int64_t)e->mem_smem,
                          e->use_tc ? 1 : 0, e->attn3_tmax, e->use_a4 ? 1 : 0,
-                         (int64_t)e->attn4_smem};
-  for (int i = 0; i < n && i < 12; ++i) info[i] = v[i];
+                         (int64_t)e->attn4_smem, e->use_m4 ? 1 : 0, (int64_t)e->mem4_smem};
+  for (int i = 0; i < n && i < 14; ++i) info[i] = v[i];
   return STGN_OK;
 }
 

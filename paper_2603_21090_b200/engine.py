@@ -562,6 +562,8 @@ class IncrementalEngine:
             W["tco"] = self._pack_kmajor(np.transpose(p.w_o, (0, 2, 1)))     # (K, d, HD)
         if self.tensor_cores is True and H == 2:
             W.update(self._pack_bf16x3())
+        if self.tensor_cores is True:
+            W["t4mem"] = self._pack_memory_bf16x3()
         self._w = W
         ws = _lib.Weights(**{k: v.data_ptr() for k, v in W.items()}, bpred=float(p.b_pred))
         _lib.check(self._L.stgn_engine_set_weights(self._handle, C.byref(ws)), "set_weights")
@@ -602,6 +604,29 @@ class IncrementalEngine:
         return {"t4q": self._pack_kmajor_bf16(wq), "t4k": self._pack_kmajor_bf16(wk),
                 "t4v": self._pack_kmajor_bf16(wv), "t4o": self._pack_kmajor_bf16(wo),
                 "t4bq": self._torch.tensor(bq.astype(np.float32), device=self.device)}
+
+    def _pack_memory_bf16x3(self):
+        """Operands of the bf16x3 memory-update kernel (stgn.h t4mem, csrc/mem4.cuh):
+        message weights in K-chunks of 128 columns of X2 = [src-side x | dst-side x],
+        then [w_z; w_r], [u_z; u_r], w_h, u_h, each a K-major bf16 hi/lo block."""
+        p, dm = self.params, self.dims
+        Nm, Ns = _rup(dm.d_m, 16), _rup(dm.d_s, 16)
+        kx = 2 * dm.msg_in
+        nmsg = -(-kx // 128)
+        wm = np.zeros((Nm, nmsg * 128))                     # [n = message unit][k = X2 column]
+        wm[:dm.d_m, :kx] = np.concatenate([p.w_msg_src.T, p.w_msg_dst.T], axis=0).T
+        wm = wm.reshape(Nm, nmsg, 128).transpose(1, 0, 2)  # (nmsg, Nm, 128)
+        zr0 = np.zeros((2 * Ns, Nm))
+        zr0[:dm.d_s, :dm.d_m], zr0[Ns:Ns + dm.d_s, :dm.d_m] = p.w_z, p.w_r
+        zr1 = np.zeros((2 * Ns, Ns))
+        zr1[:dm.d_s, :dm.d_s], zr1[Ns:Ns + dm.d_s, :dm.d_s] = p.u_z, p.u_r
+        wh = np.zeros((Ns, Nm))
+        wh[:dm.d_s, :dm.d_m] = p.w_h
+        uh = np.zeros((Ns, Ns))
+        uh[:dm.d_s, :dm.d_s] = p.u_h
+        blocks = [self._pack_kmajor_bf16(wm).reshape(-1)] + \
+            [self._pack_kmajor_bf16(b).reshape(-1) for b in (zr0, zr1, wh, uh)]
+        return self._torch.cat(blocks)
 
     def _pack_kmajor_bf16(self, B):
         """(..., N, K) float64 -> (..., 2*Np*Kp) bf16 bits (int16 tensor): the
@@ -813,11 +838,12 @@ class IncrementalEngine:
 
     def info(self) -> dict:
         """Engine facts from the C ABI (graph replay, conditional rebuild, tiles)."""
-        buf = (C.c_int64 * 12)()
-        _lib.check(self._L.stgn_engine_info(self._handle, buf, 12), "info")
+        buf = (C.c_int64 * 14)()
+        _lib.check(self._L.stgn_engine_info(self._handle, buf, 14), "info")
         keys = ("graph_active", "conditional_rebuild", "launches_per_batch", "attn_tile_rows",
                 "attn_staged_weight_floats", "num_sms", "attn_smem_bytes", "memory_smem_bytes",
-                "tensor_cores", "tc_tile_rows", "bf16x3", "bf16x3_smem_bytes")
+                "tensor_cores", "tc_tile_rows", "bf16x3", "bf16x3_smem_bytes",
+                "memory_bf16x3", "memory_bf16x3_smem_bytes")
         return {k: int(buf[i]) for i, k in enumerate(keys)}
 
     def _after_batch(self, B, t_last, top):

@@ -136,8 +136,22 @@ def run_engine_case(name, dkw, ckw, pseed, rand_bias, skw, B):
     eng = IncrementalEngine(cfg, params)
     preds, direct, affected, a_off, d_off = [], [], [], [0], [0]
     counters, rebuild_kind, rebuild_cnt = [], [], []
+    # delta mode: per-update error-bound records (S/engine.py:333-353) and the running
+    # max value norm, per batch
+    ev = {k: [] for k in ("node", "bound", "dn", "nv", "max_v", "z_dev", "emb")}
+    ev_off, mvn = [0], []
     for i in range(0, len(stream), B):
         preds.extend(eng.process_batch(stream[i:i + B]))
+        for e in eng.delta_events:
+            ev["node"].append(e.node)
+            ev["bound"].append(e.bound)
+            ev["dn"].append(e.dn)
+            ev["nv"].append(e.nv)
+            ev["max_v"].append(e.max_v)
+            ev["z_dev"].append(e.z_dev)
+            ev["emb"].append(e.embedding)
+        ev_off.append(len(ev["node"]))
+        mvn.append(eng.max_value_norm_seen)
         aff = eng.last_affected
         affected.extend(sorted(aff.all))
         direct.extend(sorted(aff.direct))
@@ -181,6 +195,12 @@ def run_engine_case(name, dkw, ckw, pseed, rand_bias, skw, B):
         cache_cnt=c_cnt, cache_nbr=c_nbr, cache_eid=c_eid, cache_t=c_t,
         full_reference=eng.full_reference(), node_count=n,
         global_drift=eng.scheduler.global_drift(), tau=eng.scheduler.tau,
+        ev_off=np.array(ev_off), ev_node=np.array(ev["node"], dtype=np.int64),
+        ev_bound=np.array(ev["bound"]), ev_dn=np.array(ev["dn"], dtype=np.int64),
+        ev_nv=np.array(ev["nv"], dtype=np.int64), ev_max_v=np.array(ev["max_v"]),
+        ev_z_dev=np.array(ev["z_dev"]),
+        ev_emb=np.array(ev["emb"]).reshape(len(ev["node"]), dims.d),
+        max_value_norm_seen=np.array(mvn),
     )
     np.savez_compressed(os.path.join(HERE, f"engine_{name}.npz"), **out)
     print(f"engine_{name}: {len(stream)} edges, {len(a_off) - 1} batches, n={n}, "
