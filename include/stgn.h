@@ -181,6 +181,14 @@ typedef struct {
   double   *gpow;           /* [gpow_len] gamma^k, k = 0..gpow_len-1 (host-computed) */
   stgn_ctl *ctl;
   uint8_t  *scratch;        /* stgn_scratch_bytes(...) bytes */
+  /* delta mode, K = 1 (S/engine.py:247-274, 333-353): log Z per head of each node's
+   * attention state, and the per-batch error-bound records of its attn_hit updates
+   * (ctl->reserved[0] = record count, ctl->reserved[1] = max_value_norm_seen as
+   * float64 bits). Unused (may be NULL, ev_cap 0) otherwise. */
+  double   *attn_logz;      /* [cap_nodes][4] */
+  int32_t  *ev_node, *ev_dpos, *ev_dn, *ev_nv;  /* [ev_cap] node, direct index or -1, |dN|, |N| */
+  double   *ev_bound, *ev_maxv, *ev_zdev;        /* [ev_cap] */
+  int64_t  ev_cap;
 } stgn_state;
 
 /* Per-batch report written by process_batch (host memory). Counter
@@ -294,6 +302,14 @@ const char* stgn_stage_name(int i);
  * memory-update smem bytes, split-TF32 tensor-core kernel active, its tile
  * rows, bf16x3 128-row kernel active, its smem bytes]. */
 int stgn_engine_info(stgn_engine* eng, int64_t* info, int n);
+
+/* Delta mode, K = 1: the last batch's error-bound records (DeltaEvent,
+ * S/engine.py:20-29, 333-353), copied to host arrays of capacity max (sorted
+ * by node id); emb receives each record's embedding (d floats per record).
+ * *mvn = max_value_norm_seen. Returns the record count (>= 0) or an error. */
+int stgn_engine_delta_events(stgn_engine* eng, int64_t max, int32_t* node, double* bound,
+                             int32_t* dn, int32_t* nv, double* max_v, double* z_dev, float* emb,
+                             double* mvn);
 
 /* Tensor-core self-test: D[N][F] = X[N][K] W[K][F] (device f32 buffers)
  * through the split-TF32 tcgen05 path (F <= 128, N <= 256). mode 0 = the

@@ -28,7 +28,7 @@ EXPORTS = (
     "stgn_engine_set_profiling", "stgn_engine_stage_times", "stgn_stage_name",
     "stgn_engine_info", "stgn_debug_tc_gemm", "stgn_generate_stream",
     "stgn_debug_a4_prof", "stgn_engine_set_scope", "stgn_read_stream",
-    "stgn_engine_set_skip_recompute",
+    "stgn_engine_set_skip_recompute", "stgn_engine_delta_events",
 )
 
 
@@ -66,9 +66,13 @@ STATE_PTRS = (
 )
 
 
+DELTA_PTRS = ("attn_logz", "ev_node", "ev_dpos", "ev_dn", "ev_nv", "ev_bound", "ev_maxv",
+              "ev_zdev")
+
+
 class State(C.Structure):
     _fields_ = [("cap_nodes", C.c_int64), ("cap_edges", C.c_int64), ("gpow_len", C.c_int64)] + \
-               [(n, C.c_void_p) for n in STATE_PTRS]
+               [(n, C.c_void_p) for n in STATE_PTRS + DELTA_PTRS] + [("ev_cap", C.c_int64)]
 
 
 class Report(C.Structure):

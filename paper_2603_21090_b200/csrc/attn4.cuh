@@ -88,6 +88,12 @@ __device__ int g_a4_prof_n;
 #ifndef A4_EC2
 #define A4_EC2 4  // ring entries per bulk-copied chunk (walk 2); two chunk stages per warp
 #endif
+#ifndef A4_EVQ
+#define A4_EVQ 1  // quadrant fill/pack duties as an event loop (see the walk phase)
+#endif
+#ifndef A4_LPT
+#define A4_LPT 0  // rows of a tile sorted by descending entry count (see the tile header)
+#endif
 #ifndef A4_TRIG
 #define A4_TRIG 0  // 1: time encoding computed per entry (fp64 phase) instead of read from ring_tb
 #endif
@@ -879,6 +885,10 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
   float* Ub0 = reinterpret_cast<float*>(sbase + (size_t)w.region_bytes);
   float* Ub1 = A4_NUB > 1 ? Ub0 + 32 * w.ldu : Ub0;
   __shared__ int s_node[A4_TMAX], s_E[A4_TMAX], s_head[A4_TMAX], s_mode[A4_TMAX];
+#if A4_LPT
+  __shared__ int s_idx[A4_TMAX], t_node[A4_TMAX], t_E[A4_TMAX], t_head[A4_TMAX], t_mode[A4_TMAX];
+  __shared__ double t_tref[A4_TMAX];
+#endif
   __shared__ double s_tref[A4_TMAX];
   __shared__ uint64_t mbar, wbar[2];
   __shared__ uint64_t qbar_full[2], qbar_done[2], qbar_packed[2];
@@ -979,7 +989,11 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
         head = rs.ring_head[node];
         if (E > 0) tref = rs.ring_t[(int64_t)node * g.L + head];
       }
+#if A4_LPT
+      t_node[i] = node; t_E[i] = E; t_head[i] = head; t_tref[i] = tref; t_mode[i] = mode;
+#else
       s_node[i] = node; s_E[i] = E; s_head[i] = head; s_tref[i] = tref; s_mode[i] = mode;
+#endif
       if (rs.e_count) {
         unsigned long long e_pre = mode == 2 ? 0ull : (unsigned long long)E;
         unsigned long long e_post = mode == 2 ? (unsigned long long)E : 0ull;
@@ -993,6 +1007,30 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
       }
     }
     __syncthreads();
+#if A4_LPT
+    // rows by descending entry count (longest first, stable): the walk takes
+    // rows in this order, so the last rows of a tile-layer are the short ones
+    // and the tail before the V GEMMs shrinks; s_idx maps back to the row index
+    if (tid < A4_TMAX) {
+      const int i = tid;
+      if (i < T) {
+        const int Ei = t_E[i];
+        int rank = 0;
+        for (int j = 0; j < T; ++j) {
+          const int Ej = t_E[j];
+          rank += (Ej > Ei) || (Ej == Ei && j < i);
+        }
+        s_node[rank] = t_node[i]; s_E[rank] = Ei; s_head[rank] = t_head[i];
+        s_tref[rank] = t_tref[i]; s_mode[rank] = t_mode[i]; s_idx[rank] = i;
+      } else {
+        s_node[i] = -1; s_E[i] = 0; s_head[i] = 0; s_tref[i] = 0.0; s_mode[i] = 0; s_idx[i] = i;
+      }
+    }
+    __syncthreads();
+#define A4_ROWIDX(r) (base + s_idx[r])
+#else
+#define A4_ROWIDX(r) (base + (r))
+#endif
     const int nq = (T + 31) / 32;
     const bool quad_live = quad < nq;
     // x_0 -> X_A (bf16 hi|lo)
@@ -1000,7 +1038,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
       const int node = row < T ? s_node[row] : -1;
       const float* src = nullptr;
       if (node >= 0)
-        src = s_mode[row] == 2 ? rs.mem_post + (base + row - pre_rows) * g.ld_s
+        src = s_mode[row] == 2 ? rs.mem_post + (A4_ROWIDX(row) - pre_rows) * g.ld_s
                                : rs.mem + (int64_t)node * g.ld_s;
       for (int j = cg; j < w.Kx / 16; j += A4_NCG) {
         float v[16];
@@ -1075,6 +1113,82 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
 #pragma unroll
       for (int p0 = 0; p0 < A4_NST - 1; ++p0) issue_next();
 #endif
+#if A4_EVQ && A4_WALK == 1 && !A4_STATIC
+      // Quadrant pipeline as an event loop: the copy-out of quadrant q's q~
+      // (fill) and the pack of its ubar (pack) are duties of the quadrant's
+      // own four warps (TMEM lane access), done as soon as their mbarrier
+      // condition holds (fill of q >= 2: quadrant q - 2 packed; pack: every
+      // warp done with q), polled between walked rows and while waiting for
+      // the next quadrant, so no warp blocks on a duty another warp has not
+      // reached yet. Quadrant q uses row buffer q & 1.
+      {
+        const int ub0 = ub_use[0], ub1 = ub_use[1];
+        auto uphase = [&](int qq) { return (uint32_t)((((qq & 1) ? ub1 : ub0) + (qq >> 1)) & 1); };
+        bool fill_done = quad >= nq, pack_done = quad >= nq;
+        auto duties = [&]() {
+          const int b = quad & 1;
+          float* Ubq = b ? Ub1 : Ub0;
+          if (!fill_done && (quad < 2 || mbar_test(&qbar_packed[b], uphase(quad - 2)))) {
+            const int nch = (w.kpad + 7) / 8;  // q~ rows of this quadrant -> Ub
+            for (int c = cg; c < 2 * nch; c += A4_NCG) {
+              const int h = c / nch, j = c % nch;
+              float v[8];
+              tmem_ld8_nw(tmem + lane_base + (uint32_t)((h == 0 ? w.qt0 : w.qt1) + 8 * j), v);
+              tmem_ld_wait();
+              float* dst = Ubq + lane * w.ldu + h * w.kpad + 8 * j;
+              *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+              if (8 * j + 8 <= w.kpad)
+                *reinterpret_cast<float4*>(dst + 4) = make_float4(v[4], v[5], v[6], v[7]);
+            }
+            if (cg == 0 && lane == 0) qctr[b] = 0;
+            mbar_arrive(&qbar_full[b]);
+            fill_done = true;
+          }
+          if (fill_done && !pack_done && mbar_test(&qbar_done[b], uphase(quad))) {
+            const int nch = w.Ku / 16;  // ubar rows -> TMEM (bf16 hi|lo) where q~ was
+            for (int c = cg; c < 2 * nch; c += A4_NCG) {
+              const int h = c / nch, j = c % nch;
+              const float* srow = Ubq + lane * w.ldu + h * w.kpad;
+              float v[16];
+#pragma unroll
+              for (int k4 = 0; k4 < 4; ++k4) {
+                const int k = 16 * j + 4 * k4;
+                float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (k < w.kpad) x = *reinterpret_cast<const float4*>(srow + k);
+                v[4 * k4] = x.x; v[4 * k4 + 1] = x.y; v[4 * k4 + 2] = x.z; v[4 * k4 + 3] = x.w;
+              }
+              const int base_col = h == 0 ? w.qt0 : w.qt1;
+              a4_st16(tmem + lane_base + (uint32_t)(base_col + 8 * j),
+                      tmem + lane_base + (uint32_t)(base_col + w.Ku / 2 + 8 * j), v);
+            }
+            tmem_st_wait();
+            mbar_arrive(&qbar_packed[b]);
+            pack_done = true;
+          }
+        };
+        for (int q = 0; q < nq; ++q) {
+          const int b = q & 1;
+          float* Ub = b ? Ub1 : Ub0;
+          const int nrows = min(32, T - 32 * q);
+          while (!mbar_test(&qbar_full[b], uphase(q))) duties();
+          for (;;) {
+            int i = 0;
+            if (lane == 0) i = atomicAdd(&qctr[b], 1);
+            i = __shfl_sync(0xffffffffu, i, 0);
+            if (i >= nrows) break;
+            const int r = 32 * q + i;
+            if (s_node[r] >= 0)
+              a4_walk_row<KF>(g, w, rs, Ub + i * w.ldu, s_node[r], s_E[r], s_head[r], s_tref[r],
+                              l, lane, stg_warp, [] {}, nullptr);
+            duties();
+          }
+          mbar_arrive(&qbar_done[b]);
+        }
+        while (!fill_done || !pack_done) duties();
+        ub_use[0] += (nq + 1) / 2;
+        ub_use[1] += nq / 2;
+      }
+#else
       // Quadrant pipeline over two row buffers, ordered by mbarriers instead of
       // CTA barriers: the quadrant's own warps copy q~ out of TMEM (full), every
       // warp takes rows of the buffer from a shared counter and walks them
@@ -1156,6 +1270,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
         }
         ++ub_use[b];
       }
+#endif
       A4_MARK(3);
       cta_sync_tc();
       if (tid == 0) {  // the walk is done with the weight buffers: stage V_0, V_1
@@ -1196,7 +1311,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
       if (quad_live) {
         const int node = row < T ? s_node[row] : -1;
         const int mode = row < T ? s_mode[row] : 0;
-        const int64_t idx = base + row;
+        const int64_t idx = A4_ROWIDX(row);
         float* dst = nullptr;
         if (node >= 0) {
           if (mode == 1) dst = last ? rs.dpred + idx * g.ld_d : nullptr;

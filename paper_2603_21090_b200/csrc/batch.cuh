@@ -37,6 +37,10 @@ struct StateView {
   int32_t* cum_pos;
   int64_t* attn_ver;
   double* attn_tref;
+  double* attn_logz;  // [n][4] delta mode K = 1: log Z per head of the node's attention state
+  int32_t *ev_node, *ev_dpos, *ev_dn, *ev_nv;
+  double *ev_bound, *ev_maxv, *ev_zdev;
+  int64_t ev_cap;
   int32_t *e_src, *e_dst;
   double* e_t;
   float* e_feat;
@@ -516,6 +520,7 @@ __global__ void k_delta_classify(Geo g, StateView st, Scratch s) {
   const int lane = threadIdx.x & 31;
   int skip = 0, hit = 0, miss = 0;
   unsigned long long e_miss = 0;
+  int info = 0;
   const int64_t n_it = ((int64_t)nA + 31) & ~31ll;  // whole warps for the ballot
   for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < n_it;
        a += (int64_t)gridDim.x * blockDim.x) {
@@ -532,6 +537,7 @@ __global__ void k_delta_classify(Geo g, StateView st, Scratch s) {
         const double tref = len > 0 ? st.ring_t[(int64_t)v * g.L + st.ring_head[v]] : 0.0;
         const bool is_hit = g.K == 1 && valid && st.attn_ver[v] == st.version[v] &&
                             st.attn_tref[v] == tref;
+        info = (s.a_size[a] << 1) | (is_hit ? 1 : 0);
         if (is_hit) {
           ++hit;
         } else {
@@ -540,6 +546,7 @@ __global__ void k_delta_classify(Geo g, StateView st, Scratch s) {
         }
         if (direct) {
           s.clist[a] = v;
+          s.c_info[a] = (s.a_size[a] << 1) | (is_hit ? 1 : 0);
           st.attn_ver[v] = bidx;
           st.attn_tref[v] = tref;
         } else {
@@ -557,7 +564,11 @@ __global__ void k_delta_classify(Geo g, StateView st, Scratch s) {
       const int leader = __ffs(m) - 1;
       if (lane == leader) base = atomicAdd(&s.res->nC, __popc(m));
       base = __shfl_sync(0xffffffffu, base, leader);
-      if (keep) s.clist[nD + base + __popc(m & ((1u << lane) - 1u))] = v;
+      if (keep) {
+        const int pos = nD + base + __popc(m & ((1u << lane) - 1u));
+        s.clist[pos] = v;
+        s.c_info[pos] = info;
+      }
     }
   }
   for (int o = 16; o > 0; o >>= 1) {

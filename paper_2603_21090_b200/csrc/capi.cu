@@ -8,11 +8,13 @@
 
 #include <algorithm>
 #include <utility>
+#include <vector>
 
 #include "batch.cuh"
 #include "attn3.cuh"
 #include "attn4.cuh"
 #include "mem4.cuh"
+#include "delta.cuh"
 
 #ifndef STGN_VERSION
 #define STGN_VERSION "stgn 0.1.0 sm_100a"
@@ -361,7 +363,11 @@ int stgn_engine_set_weights(stgn_engine* e, const stgn_weights* w) {
     e->a4w.bq = w->t4bq;
     e->a4w.omega = w->omega;
   }
+#ifdef STGN_NO_MEM4  // experiments: the FFMA memory update
+  e->use_m4 = false;
+#else
   e->use_m4 = e->m4_ok && w->t4mem;
+#endif
   if (e->use_m4) e->m4w.wblk = w->t4mem;
   e->aw.wq = w->wq;
   e->aw.wkt = w->wkt;
@@ -387,6 +393,9 @@ int stgn_engine_bind(stgn_engine* e, const stgn_state* s) {
   v.nodefill = s->nodefill; v.nodeoff = s->nodeoff; v.drift_acc = s->drift_acc;
   v.drift_touched = s->drift_touched; v.cum_mark = s->cum_mark; v.cum_list = s->cum_list;
   v.cum_pos = s->cum_pos; v.attn_ver = s->attn_ver; v.attn_tref = s->attn_tref;
+  v.attn_logz = s->attn_logz; v.ev_node = s->ev_node; v.ev_dpos = s->ev_dpos; v.ev_dn = s->ev_dn;
+  v.ev_nv = s->ev_nv; v.ev_bound = s->ev_bound; v.ev_maxv = s->ev_maxv; v.ev_zdev = s->ev_zdev;
+  v.ev_cap = s->attn_logz ? s->ev_cap : 0;
   v.e_src = s->e_src; v.e_dst = s->e_dst; v.e_t = s->e_t; v.e_feat = s->e_feat;
   v.e_prev = s->e_prev; v.adj_head = s->adj_head; v.adj_deg = s->adj_deg;
   v.gpow = s->gpow; v.gpow_len = s->gpow_len; v.ctl = s->ctl;
@@ -489,6 +498,8 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
     ++stage;
   };
   mark();
+  if (e->cfg.scope == STGN_SCOPE_DELTA && g.K == 1 && v.attn_logz)
+    cudaMemsetAsync(&v.ctl->reserved[0], 0, sizeof(int64_t), st);  // this batch's bound records
   // ingest: direct set, per-node record order, ring insert with payload freeze, store append
   chain_launch(k_begin, 1, 32, 0, st, s, e->cfg.window);
   chain_launch(k_claim, g_rec, T, 0, st, g, v, s);
@@ -569,6 +580,12 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   rs.e_count_post = &s.res->E_D;
   launch_attn(e, rs, st, true);
   n += 1;
+  const bool dstate = e->cfg.scope == STGN_SCOPE_DELTA && g.K == 1 && v.attn_logz;
+  if (dstate) {  // attention-state statistics + bound records, before the memory commit
+    k_delta_state<<<4 * e->num_sms, DS_THREADS, delta_state_smem(g), st>>>(g, v, s, e->ew, nullptr,
+                                                                          nullptr, 0, 0);
+    n += 1;
+  }
   if (e->cfg.scope == STGN_SCOPE_DIRECT) {
     k_mark_valid<<<g_wide, T, 0, st>>>(v, s);
     n += 1;
@@ -629,10 +646,16 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
     rp.write_valid = 1;
     rp.e_count = &s.res->E_R;
     launch_attn(e, rp, rs);
+    if (stamp && v.attn_logz)
+      k_delta_state<<<4 * e->num_sms, DS_THREADS, delta_state_smem(g), rs>>>(
+          g, v, s, e->ew, s.drifted, &s.res->rb_partial_n, 0, 1);
     RingSrc rf = rp;
     rf.list = nullptr;
     rf.count_ptr = &s.res->rb_full_n;
     launch_attn(e, rf, rs);
+    if (stamp && v.attn_logz)
+      k_delta_state<<<4 * e->num_sms, DS_THREADS, delta_state_smem(g), rs>>>(
+          g, v, s, e->ew, nullptr, &s.res->rb_full_n, 0, 1);
     k_drift_reset_fin<<<1, 32, 0, rs>>>(v, s);
     n += 5;
     if (body) {
@@ -877,9 +900,54 @@ extern "C" int stgn_engine_rebuild(stgn_engine* e, const int32_t* ids, int64_t n
   r.valid_at_const = valid_at_value;
   r.write_valid = 1;
   launch_attn(e, r, st);
+  if (e->cfg.scope == STGN_SCOPE_DELTA && e->g.K == 1 && e->sv.attn_logz)
+    k_delta_state<<<4 * e->num_sms, DS_THREADS, delta_state_smem(e->g), st>>>(
+        e->g, e->sv, s, e->ew, list, nullptr, (int)n, 1);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(st));
   return STGN_OK;
+}
+
+extern "C" int stgn_engine_delta_events(stgn_engine* e, int64_t max, int32_t* node, double* bound,
+                                        int32_t* dn, int32_t* nv, double* max_v, double* z_dev,
+                                        float* emb, double* mvn) {
+  if (!e || !e->bound) return STGN_ERR_INVALID;
+  const StateView& v = e->sv;
+  int64_t ctl_r[2] = {0, 0};
+  CUDA_TRY(cudaMemcpy(ctl_r, &v.ctl->reserved[0], sizeof(ctl_r), cudaMemcpyDeviceToHost));
+  if (mvn) memcpy(mvn, &ctl_r[1], sizeof(double));
+  if (!v.attn_logz || v.ev_cap == 0) return 0;
+  const int64_t n = std::min<int64_t>(ctl_r[0], v.ev_cap);
+  if (n > max) return STGN_ERR_CAPACITY;
+  if (n == 0) return 0;
+  std::vector<int32_t> hn(n), hp(n), hdn(n), hnv(n);
+  std::vector<double> hb(n), hm(n), hz(n);
+  CUDA_TRY(cudaMemcpy(hn.data(), v.ev_node, 4 * n, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(hp.data(), v.ev_dpos, 4 * n, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(hdn.data(), v.ev_dn, 4 * n, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(hnv.data(), v.ev_nv, 4 * n, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(hb.data(), v.ev_bound, 8 * n, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(hm.data(), v.ev_maxv, 8 * n, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(hz.data(), v.ev_zdev, 8 * n, cudaMemcpyDeviceToHost));
+  std::vector<float> he((size_t)n * e->g.d);
+  if (emb) {
+    float* dout = nullptr;
+    CUDA_TRY(cudaMalloc(&dout, sizeof(float) * n * e->g.d));
+    k_delta_ev_gather<<<4 * e->num_sms, 256>>>(e->g, v, e->sc, v.ev_node, v.ev_dpos, (int)n, dout);
+    cudaError_t ce = cudaMemcpy(he.data(), dout, sizeof(float) * n * e->g.d, cudaMemcpyDeviceToHost);
+    cudaFree(dout);
+    CUDA_TRY(ce);
+  }
+  std::vector<int64_t> ord(n);
+  for (int64_t i = 0; i < n; ++i) ord[i] = i;
+  std::sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return hn[a] < hn[b]; });
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t i = ord[k];
+    node[k] = hn[i]; bound[k] = hb[i]; dn[k] = hdn[i]; nv[k] = hnv[i];
+    max_v[k] = hm[i]; z_dev[k] = hz[i];
+    if (emb) memcpy(emb + k * e->g.d, he.data() + i * e->g.d, sizeof(float) * e->g.d);
+  }
+  return (int)n;
 }
 
 extern "C" int stgn_engine_full_reference(stgn_engine* e, int64_t node_count, float* out_dev,

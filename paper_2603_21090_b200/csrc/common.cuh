@@ -88,6 +88,7 @@ struct Scratch {
   int32_t* a_size;          // [cap_nodes] change-record size by A index
   int32_t* a_len;           // [cap_nodes] cache length after the batch, by A index
   int32_t* clist;           // [cap_nodes] delta mode: D, then the non-skipped nodes of A \ D
+  int32_t* c_info;          // [cap_nodes] delta mode, by clist row: change-record size << 1 | attn_hit
   float* msgs;              // [2Bmax][ld_m]
   double* preds;            // [Bmax]
   float* dpred;             // [2Bmax][ld_d]
@@ -119,6 +120,7 @@ static inline int64_t scratch_layout(const Geo& g, int64_t Bmax, int64_t cap_nod
   int64_t o_wc = carve(off, R * 4), o_bl = carve(off, R * 4);
   int64_t o_asz = carve(off, cap_nodes * 4), o_alen = carve(off, cap_nodes * 4);
   int64_t o_clist = carve(off, cap_nodes * 4);
+  int64_t o_cinfo = carve(off, cap_nodes * 4);
   int64_t o_msg = carve(off, R * g.ld_m * 4);
   int64_t o_pred = carve(off, Bmax * 8);
   int64_t o_dpred = carve(off, R * g.ld_d * 4);
@@ -145,6 +147,7 @@ static inline int64_t scratch_layout(const Geo& g, int64_t Bmax, int64_t cap_nod
     s->a_size = (int32_t*)(base + o_asz);
     s->a_len = (int32_t*)(base + o_alen);
     s->clist = (int32_t*)(base + o_clist);
+    s->c_info = (int32_t*)(base + o_cinfo);
     s->msgs = (float*)(base + o_msg);
     s->preds = (double*)(base + o_pred);
     s->dpred = (float*)(base + o_dpred);

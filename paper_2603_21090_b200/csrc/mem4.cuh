@@ -207,15 +207,41 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
         float x[16];
 #pragma unroll
         for (int t = 0; t < 16; ++t) x[t] = 0.f;
-        if (v >= 0) {
+        if (v >= 0 && last_agg) {
+          // one record: x on its side's half of X2; 16 independent loads, then the
+          // time-encoding columns (no load in flight waits for another)
+          const int side = s_lside[row];
+          const float* pv = st.mem + (int64_t)v * g.ld_s;
+          const float* po = st.mem + (int64_t)s_loth[row] * g.ld_s;
+          const float* pf = s.in_feat + (int64_t)s_le[row] * g.ld_e;
+          const int c0 = j * M4_KC + 16 * b - side * g.msg_in;  // x column of t = 0
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const int cs = c0 + t;
+            if (cs >= 0 && cs < phi0) {
+              const float* p = cs < g.d_s ? pv + cs : (cs < 2 * g.d_s ? po + (cs - g.d_s)
+                                                                      : pf + (cs - 2 * g.d_s));
+              x[t] = __ldg(p);
+            }
+          }
+          const double dt = s_ldt[row];
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const int cs = c0 + t;
+            if (cs >= phi0 && cs < g.msg_in) {
+              const int p = cs - phi0;
+              float sv, cv;
+              phase_sincos(omega[p >> 1], dt, &sv, &cv);
+              x[t] = ((p & 1) ? sv : cv) * g.phi_amp;
+            }
+          }
+        } else if (v >= 0) {
           for (int t = 0; t < 16; ++t) {
             const int c = j * M4_KC + 16 * b + t;
             if (c >= 2 * g.msg_in) break;
             const int side = c >= g.msg_in;
             const int cc = c - side * g.msg_in;
-            if (last_agg) {
-              if (s_lside[row] == side) x[t] = xval(cc, s_le[row], s_loth[row], s_ldt[row]);
-            } else {
+            {
               float acc = 0.f;
               for (int q = s_lo[row]; q < s_hi[row]; ++q) {
                 const int r = s.rec_s[q];

@@ -103,6 +103,19 @@ class Counters:
 _REBUILD_NAMES = {0: "none", 1: "partial", 2: "full"}
 
 
+@dataclass
+class DeltaEvent:
+    """One delta-mode embedding update, kept for bound verification (S/engine.py:20-29)."""
+
+    node: int
+    embedding: np.ndarray
+    bound: float
+    dn: int
+    nv: int
+    max_v: float
+    z_dev: float
+
+
 class _Tables:
     """PyTorch-allocated device tables bound into the C engine. Node tables,
     edge tables, the gamma^k table and the scratch grow independently."""
@@ -151,6 +164,15 @@ class _Tables:
         self.drift_touched = z(N, dt=torch.int64)
         self.attn_ver = z(N, dt=torch.int64, fill=-1)
         self.attn_tref = z(N, dt=torch.float64)
+        # delta mode, K = 1: log Z per head of each node's attention state, and the
+        # per-batch bound-record buffers (stgn.h stgn_state; csrc/delta.cuh)
+        self.attn_logz = z(N, 4, dt=torch.float64, fill=-math.inf)
+        ne = N if g.K == 1 else 1
+        self.ev_cap = ne if g.K == 1 else 0
+        for name in ("ev_node", "ev_dpos", "ev_dn", "ev_nv"):
+            setattr(self, name, z(ne, dt=torch.int32))
+        for name in ("ev_bound", "ev_maxv", "ev_zdev"):
+            setattr(self, name, z(ne, dt=torch.float64))
         self.adj_head = z(N, dt=torch.int64, fill=-1)
         self.adj_deg = z(N, dt=torch.int64)
         for k, t in old.items():
@@ -160,7 +182,7 @@ class _Tables:
     def _node_names(self):
         return ("mem", "last", "version", "h", "valid", "valid_at", *self.NODE_I32, "ring_nbr",
                 "ring_eid", "ring_t", "ring_pay", "ring_feat", "ring_tb", "drift_acc", "drift_touched", "attn_ver", "attn_tref",
-                "adj_head", "adj_deg")
+                "attn_logz", "adj_head", "adj_deg")
 
     def _alloc_edges(self, E):
         torch, g = self.eng._torch, self.eng
@@ -209,8 +231,9 @@ class _Tables:
     def struct(self) -> _lib.State:
         s = _lib.State()
         s.cap_nodes, s.cap_edges, s.gpow_len = self.cap_nodes, self.cap_edges, self.gpow.numel()
-        for name in _lib.STATE_PTRS:
+        for name in _lib.STATE_PTRS + _lib.DELTA_PTRS:
             setattr(s, name, getattr(self, name).data_ptr())
+        s.ev_cap = self.ev_cap
         return s
 
 
@@ -426,8 +449,9 @@ class IncrementalEngine:
     cached row (embed_skip); the others are classified attn_hit / attn_miss
     exactly as the reference does and recomputed on the device (a hit's
     delta_embed update is the same softmax over the same frozen-payload key
-    rows, so the recompute returns the delta result up to rounding). The
-    per-update error-bound records (delta_events) are not collected.
+    rows, so the recompute returns the delta result up to rounding). For
+    K = 1 the per-update error-bound records (delta_events, S/engine.py:333-353)
+    and max_value_norm_seen are computed on the device (csrc/delta.cuh).
     """
 
     def __init__(self, cfg: RunConfig, params: ModelParameters, *, recompute: str = "affected",
@@ -487,7 +511,8 @@ class IncrementalEngine:
         self.store = _StoreView(self)
         self.scheduler = _SchedulerView(self)
         self._rep = _lib.Report()
-        self.delta_events: list = []  # delta mode: bound records are not collected
+        self._ev_batch = -1     # batch whose bound records self._events holds
+        self._events: list = []
         self._preds = np.zeros(self._max_batch, dtype=np.float64)
 
     # -- plumbing -------------------------------------------------------------
@@ -845,6 +870,42 @@ class IncrementalEngine:
                 "tensor_cores", "tc_tile_rows", "bf16x3", "bf16x3_smem_bytes",
                 "memory_bf16x3", "memory_bf16x3_smem_bytes")
         return {k: int(buf[i]) for i, k in enumerate(keys)}
+
+    @property
+    def delta_events(self) -> list:
+        """The last batch's DeltaEvent records (delta mode, K = 1; else [])."""
+        if self.cfg.mode != "delta" or self.K != 1:
+            return []
+        if self._ev_batch != self.batch_index:
+            self._events = self._fetch_delta_events()
+            self._ev_batch = self.batch_index
+        return self._events
+
+    @property
+    def max_value_norm_seen(self) -> float:
+        """Running max of the attention states' value-row norms (S/engine.py:255-261, 349)."""
+        if self.cfg.mode != "delta" or self.K != 1:
+            return 0.0
+        return float(self._tab.ctl[4:5].cpu().view(self._torch.float64).item())
+
+    def _fetch_delta_events(self):
+        cap = max(self._tab.ev_cap, 1)
+        d = self.dims.d
+        node = np.zeros(cap, np.int32)
+        dn = np.zeros(cap, np.int32)
+        nv = np.zeros(cap, np.int32)
+        bound, mv, zd = np.zeros(cap), np.zeros(cap), np.zeros(cap)
+        emb = np.zeros((cap, d), np.float32)
+        mvn = C.c_double()
+        P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self.sync()
+        n = self._L.stgn_engine_delta_events(self._handle, C.c_int64(cap), P(node), P(bound), P(dn),
+                                             P(nv), P(mv), P(zd), P(emb), C.byref(mvn))
+        if n < 0:
+            _lib.check(n, "delta_events")
+        return [DeltaEvent(node=int(node[i]), embedding=emb[i].astype(np.float64),
+                           bound=float(bound[i]), dn=int(dn[i]), nv=int(nv[i]),
+                           max_v=float(mv[i]), z_dev=float(zd[i])) for i in range(n)]
 
     def _after_batch(self, B, t_last, top):
         r = self._rep

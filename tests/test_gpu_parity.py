@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from golden_util import batches, case_setup, delta_cases, engine_cases, load, pipeline_cases
-from parity_util import PRED_ATOL, assert_rows_close, row_rel_err
+from parity_util import check_delta_events, PRED_ATOL, assert_rows_close, row_rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -50,9 +50,13 @@ def _run_engine(name, recompute="affected", prefix="engine_"):
         cfg = dataclasses.replace(cfg, mode="delta")
     eng = IncrementalEngine(cfg, params, recompute=recompute)
     preds, aff, dirs, kinds, cnts, counters = [], [], [], [], [], []
+    eng.events_by_batch, eng.mvn_by_batch = [], []
     keys = list(z["counter_keys"])
     for b in batches(stream, cfg.batch_size):
         preds.extend(eng.process_batch_arrays(b.src, b.dst, b.t, b.feat).tolist())
+        if prefix == "delta_":
+            eng.events_by_batch.append([vars(e) for e in eng.delta_events])
+            eng.mvn_by_batch.append(eng.max_value_norm_seen)
         la = eng.last_affected
         aff.extend(sorted(la.all))
         dirs.extend(sorted(la.direct))
@@ -113,6 +117,9 @@ def test_engine_delta_mode_matches_reference(cuda, name):
     assert_rows_close(eng.cache.h[:n].reshape(n, -1), z["h"].reshape(n, -1), "layer cache")
     np.testing.assert_array_equal(eng.cache.valid_at[:n], z["valid_at"])
     assert eng.scheduler.tau == int(z["tau"])
+    # the error-bound records of every attn_hit update (S/engine.py:333-353) and
+    # max_value_norm_seen, batch by batch (csrc/delta.cuh; fp32 logits and value rows)
+    check_delta_events(eng.events_by_batch, eng.mvn_by_batch, z, tol_rel=1e-4, tol_abs=1e-4)
 
 
 @pytest.mark.parametrize("name", ["c4_shape_tiny", "k2_wide_adaptive"])
