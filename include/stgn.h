@@ -120,8 +120,9 @@ typedef struct {
   /* bf16x3 tensor-core operands of the memory update (optional; the FFMA
    * k_memory is used when NULL or when the plan does not fit): the same
    * K-major bf16 hi/lo block layout, blocks concatenated in this order
-   * (Nm = round_up(d_m,16), Ns = round_up(d_s,16), X2 = [src-side x | dst-side x]):
-   *   ceil(2*msg_in/128) blocks  N = Nm,   K = 128   [w_msg_src | w_msg_dst] columns of X2
+   * (Nm = round_up(d_m,16), Ns = round_up(d_s,16)):
+   *   for j < ceil(msg_in/128):  N = Nm,   K = 128   w_msg_src columns [128j, 128j+128),
+   *                              N = Nm,   K = 128   then w_msg_dst columns [128j, 128j+128)
    *   1 block                    N = 2*Ns, K = Nm    [w_z ; w_r] (r at row Ns)
    *   1 block                    N = 2*Ns, K = Ns    [u_z ; u_r]
    *   1 block                    N = Ns,   K = Nm    w_h
@@ -302,6 +303,14 @@ const char* stgn_stage_name(int i);
  * memory-update smem bytes, split-TF32 tensor-core kernel active, its tile
  * rows, bf16x3 128-row kernel active, its smem bytes]. */
 int stgn_engine_info(stgn_engine* eng, int64_t* info, int n);
+
+/* Per-batch result block (counters of the last enqueued batch), for pipelined
+ * callers that do not block on a report: stgn_engine_result_copy copies it
+ * (stream-ordered) to device memory (to_device != 0) or pinned host memory;
+ * stgn_report_from_result turns a host copy into a stgn_report. */
+int64_t stgn_batch_result_bytes(void);
+int stgn_engine_result_copy(stgn_engine* eng, void* dst, int32_t to_device, void* stream);
+int stgn_report_from_result(const void* res, stgn_report* rep);
 
 /* Delta mode, K = 1: the last batch's error-bound records (DeltaEvent,
  * S/engine.py:20-29, 333-353), copied to host arrays of capacity max (sorted

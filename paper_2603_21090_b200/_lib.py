@@ -28,7 +28,8 @@ EXPORTS = (
     "stgn_engine_set_profiling", "stgn_engine_stage_times", "stgn_stage_name",
     "stgn_engine_info", "stgn_debug_tc_gemm", "stgn_generate_stream",
     "stgn_debug_a4_prof", "stgn_engine_set_scope", "stgn_read_stream",
-    "stgn_engine_set_skip_recompute", "stgn_engine_delta_events",
+    "stgn_engine_set_skip_recompute", "stgn_engine_delta_events", "stgn_batch_result_bytes",
+    "stgn_engine_result_copy", "stgn_report_from_result",
 )
 
 
@@ -118,6 +119,7 @@ def lib():
     L.stgn_engine_set_profiling.argtypes = [vp, C.c_int]
     L.stgn_engine_stage_times.argtypes = [vp, vp, C.c_int, P(i64)]
     L.stgn_stage_name.restype = C.c_char_p
+    L.stgn_batch_result_bytes.restype = i64
     L.stgn_stage_name.argtypes = [C.c_int]
     L.stgn_engine_info.argtypes = [vp, vp, C.c_int]
     L.stgn_debug_tc_gemm.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, vp, C.c_int, vp]
@@ -128,7 +130,7 @@ def lib():
     L.stgn_generate_stream.argtypes = [vp, i64, i64, i32, dbl, vp, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("stgn_version", "stgn_last_error", "stgn_scratch_bytes",
-                        "stgn_stage_name"):
+                        "stgn_stage_name", "stgn_batch_result_bytes"):
             getattr(L, name).restype = C.c_int
     _LIB = L
     return L

@@ -767,6 +767,27 @@ static void fill_report(const BatchRes& r, const stgn_ctl* /*unused*/, stgn_repo
   rep->global_drift = r.global_drift;
 }
 
+extern "C" int64_t stgn_batch_result_bytes(void) { return (int64_t)sizeof(BatchRes); }
+
+// Copy the last enqueued batch's device result block (stream-ordered after its
+// sequence) to dst: device memory (to_device != 0, e.g. a per-slot buffer on the
+// engine stream, before the next batch reuses the scratch) or pinned host memory.
+extern "C" int stgn_engine_result_copy(stgn_engine* e, void* dst, int32_t to_device,
+                                       void* stream) {
+  if (!e || !e->bound || !dst) return STGN_ERR_INVALID;
+  CUDA_TRY(cudaMemcpyAsync(dst, e->sc.res, sizeof(BatchRes),
+                           to_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                           (cudaStream_t)stream));
+  return STGN_OK;
+}
+
+// Host: the report of a result block copied by stgn_engine_result_copy.
+extern "C" int stgn_report_from_result(const void* res, stgn_report* rep) {
+  if (!res || !rep) return STGN_ERR_INVALID;
+  fill_report(*reinterpret_cast<const BatchRes*>(res), nullptr, rep);
+  return STGN_OK;
+}
+
 static int check_batch(stgn_engine* e, int32_t B, int64_t m0, int64_t batch_index,
                        int64_t node_count) {
   if (!e->bound || !e->have_w) return STGN_ERR_INVALID;

@@ -8,24 +8,27 @@
 //   m_v   = last / mean / sum of msg_q over v's records (message order)
 //   z = sig(W_z m + U_z s + b_z), r = sig(W_r m + U_r s + b_r)
 //   s' = (1 - z) tanh(W_h m + U_h (r * s) + b_h) + z s
-// Messages are linear in x, so m_v = X2_v Wmsg2 + (n_src b_src + n_dst b_dst)
-// [/ cnt] with X2_v = [sum of src-side x || sum of dst-side x] (k_memory's
-// formulation); the last aggregator keeps the last record only.
+// Messages are linear in x, so with the last aggregator (one record per node)
+// m_v = x_last W_side^T + b_side, and with sum / mean
+// m_v = X_src W_src^T + X_dst W_dst^T + n_src b_src + n_dst b_dst [/ cnt],
+// X_side = the sum of the node's side-`side` x rows.
 //
-// Per tile (one CTA, 512 threads = 4 TMEM lane quadrants x 4 column groups;
-// thread (quadrant, cg) owns row 32*quadrant + lane, column blocks cg, cg+4, ...):
-//   1. X2 in K-chunks of 128 elements, bf16 hi|lo into one of two TMEM A
-//      buffers while the previous chunk's MMA runs: D_AG += X2_j Wmsg_j.
+// Per tile (one CTA, 1024 threads = 4 TMEM lane quadrants x 8 column groups;
+// thread (quadrant, cg) owns row 32*quadrant + lane and 16-column block cg):
+//   1. x in K-chunks of 128 columns, bf16 hi|lo into one of two TMEM A
+//      buffers while the previous chunk's MMAs run: D_SRC += x_j W_src,j,
+//      D_DST += x_j W_dst,j (both sides; the row's side is picked after).
+//      sum / mean: X_src,j and X_dst,j in A0 / A1, one chunk at a time.
 //   2. A2 = [Ag + bias (/cnt) || s] (bf16 hi|lo); D_ZR = A2 [W_z W_r; U_z U_r].
 //   3. z kept in registers, A3 = r * s written over A2's s half;
 //      D_H = Ag W_h + A3 U_h (into D_ZR's z columns).
 //   4. s' = (1 - z) tanh(D_H + b_h) + z s -> mem_new (committed after the recompute).
 // Weight blocks (K-major bf16 hi block then lo block, stgn.h t4mem) are staged
-// by TMA bulk copies into two shared buffers, one block ahead.
+// by TMA bulk copies into two shared buffers, two blocks ahead.
 //
 // TMEM columns (Nm = r16(d_m), Ks = Ns = r16(d_s), half = (Nm + Ks) / 2):
-//   A0 [0,128) A1 [128,256)   message chunks (hi [.,+64) lo [+64,+128))
-//   D_AG [256, 256+Nm)
+//   A0 [0,128) A1 [128,256)   x chunks (hi [.,+64) lo [+64,+128))
+//   D_SRC [256, 256+Nm)  D_DST [256+Nm, 256+2Nm)
 //   A2: Ag hi [0,Nm/2) s hi [Nm/2,half) | Ag lo [half,half+Nm/2) s lo [.., 2 half)
 //   D_ZR [2 half, 2 half + 2 Ns)  (z at +0, r at +Ns); D_H reuses z's columns
 //   A3 = r * s in A2's s columns
@@ -33,7 +36,10 @@
 
 #include "attn4.cuh"
 
-#define M4_THREADS 512
+#ifndef M4_THREADS
+#define M4_THREADS 1024  // 4 TMEM lane quadrants x M4_NCG column groups
+#endif
+#define M4_NCG (M4_THREADS / 128)
 #define M4_KC 128
 #define M4_MAXBLK 24
 
@@ -51,9 +57,9 @@ static inline bool m4_plan(const Geo& g, M4W* w) {
   w->Nm = r16(g.d_m);
   w->Ks = r16(g.d_s);
   w->Ns = w->Ks;
-  if (w->Nm > 128 || w->Ks > 128) return false;
-  w->nmsg = (int)cdiv(2 * g.msg_in, M4_KC);
-  w->nblk = w->nmsg + 4;
+  if (w->Nm > 16 * M4_NCG || w->Ks > 16 * M4_NCG) return false;  // one 16-column block per thread
+  w->nmsg = (int)cdiv(g.msg_in, M4_KC);  // K-chunks of x; two weight blocks (src, dst) each
+  w->nblk = 2 * w->nmsg + 4;
   if (w->nblk > M4_MAXBLK) return false;
   int64_t off = 0;
   int maxb = 0;
@@ -64,14 +70,15 @@ static inline bool m4_plan(const Geo& g, M4W* w) {
     off += 2ll * np * kp;
     maxb = std::max(maxb, 2 * np * kp * 2);
   };
-  for (int j = 0; j < w->nmsg; ++j) add(j, w->Nm, M4_KC);
-  add(w->nmsg, 2 * w->Ns, w->Nm);      // [W_z; W_r]
-  add(w->nmsg + 1, 2 * w->Ns, w->Ks);  // [U_z; U_r]
-  add(w->nmsg + 2, w->Ns, w->Nm);      // W_h
-  add(w->nmsg + 3, w->Ns, w->Ks);      // U_h
+  for (int j = 0; j < 2 * w->nmsg; ++j) add(j, w->Nm, M4_KC);  // W_src chunk j, W_dst chunk j
+  const int z0 = 2 * w->nmsg;
+  add(z0, 2 * w->Ns, w->Nm);      // [W_z; W_r]
+  add(z0 + 1, 2 * w->Ns, w->Ks);  // [U_z; U_r]
+  add(z0 + 2, w->Ns, w->Nm);      // W_h
+  add(z0 + 3, w->Ns, w->Ks);      // U_h
   w->wbuf_bytes = (maxb + 1023) & ~1023;
   const int half = (w->Nm + w->Ks) / 2;
-  return 2 * w->Ns <= 256 && 2 * half + 2 * w->Ns <= 512 && 256 + w->Nm <= 512 &&
+  return 2 * w->Ns <= 256 && 2 * half + 2 * w->Ns <= 512 && 256 + 2 * w->Nm <= 512 &&
          2 * w->wbuf_bytes + 1024 <= 220 * 1024;
 }
 static inline int64_t m4_total_elems(const M4W& w) {
@@ -112,10 +119,13 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
   __shared__ double s_ldt[128];                         // its t - last[owner]
   __shared__ uint64_t mbar, wbar[2];
   __shared__ uint32_t tslot;
+  __shared__ float s_bmsg[2 * 16 * M4_NCG], s_bgru[3 * 16 * M4_NCG];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int quad = warp & 3, cg = warp >> 2;
   const int nD = s.res->nD;
+  for (int i = tid; i < 2 * g.d_m; i += M4_THREADS) s_bmsg[i] = bmsg[i];
+  for (int i = tid; i < 3 * g.d_s; i += M4_THREADS) s_bgru[i] = bgru[i];
   const int64_t ntiles = cdiv(nD, 128);
   if ((int64_t)blockIdx.x >= ntiles) return;
   const int64_t my_tiles = cdiv(ntiles - blockIdx.x, (int64_t)gridDim.x);
@@ -145,10 +155,11 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
     if (total_blocks > 1) stage(1);
   }
   int64_t G = 0;
-  auto issue = [&](int a_hi, int a_lo, int dcol, bool acc) {  // tid 0
-    const int j = (int)(G % w.nblk);
-    mbar_wait(&wbar[G & 1], (uint32_t)((G >> 1) & 1));
-    m4_mma(tmem, a_hi, a_lo, (G & 1) ? Wb1 : Wb0, w.np[j], w.kp[j], dcol, acc, &mbar);
+  auto issue = [&](int a_hi, int a_lo, int dcol, bool acc, int off = 0) {  // tid 0: block G + off
+    const int64_t Gi = G + off;
+    const int j = (int)(Gi % w.nblk);
+    mbar_wait(&wbar[Gi & 1], (uint32_t)((Gi >> 1) & 1));
+    m4_mma(tmem, a_hi, a_lo, (Gi & 1) ? Wb1 : Wb0, w.np[j], w.kp[j], dcol, acc, &mbar);
   };
   auto finish = [&]() {  // every thread: the MMA of block G is done; refill its buffer
     mbar_wait(&mbar, (uint32_t)(G & 1));
@@ -176,9 +187,10 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
         v = s.alist[d];
         lo = s.doff[d];
         hi = s.doff[d + 1];
-        for (int q = lo; q < hi; ++q) {
-          if (s.rec_s[q] & 1) ++n1; else ++n0;
-        }
+        if (!last_agg)
+          for (int q = lo; q < hi; ++q) {
+            if (s.rec_s[q] & 1) ++n1; else ++n0;
+          }
         const int r = s.rec_s[hi - 1];
         le = r >> 1;
         lside = r & 1;
@@ -189,6 +201,7 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
       s_le[tid] = le; s_lside[tid] = lside; s_loth[tid] = loth; s_ldt[tid] = ldt;
     }
     __syncthreads();
+    A4_MARK(8);
     const int v = s_node[row];
     // x_q[cc] of one record (owner v)
     auto xval = [&](int cc, int e, int oth, double dt) -> float {
@@ -200,21 +213,22 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
       phase_sincos(omega[p >> 1], dt, &sv, &cv);
       return ((p & 1) ? sv : cv) * g.phi_amp;
     };
-    // X2 chunk j (elements [128 j, 128 j + 128)) of this thread's row -> A buffer j & 1
-    auto build = [&](int j) {
-      const int abase = (j & 1) ? 128 : 0;
-      for (int b = cg; b < M4_KC / 16; b += 4) {
+    // chunk j (x columns [128 j, 128 j + 128)) of this thread's row -> A buffer `buf`:
+    // side < 0: the last record's x (last aggregator); side 0 / 1: the sum of that
+    // side's x over the row's records (sum / mean)
+    auto build = [&](int j, int buf, int side_sel) {
+      const int abase = buf ? 128 : 0;
+      for (int b = cg; b < M4_KC / 16; b += M4_NCG) {
         float x[16];
 #pragma unroll
         for (int t = 0; t < 16; ++t) x[t] = 0.f;
-        if (v >= 0 && last_agg) {
-          // one record: x on its side's half of X2; 16 independent loads, then the
-          // time-encoding columns (no load in flight waits for another)
-          const int side = s_lside[row];
+        if (v >= 0 && side_sel < 0) {
+          // one record: 16 independent loads, then the time-encoding columns
+          // (no load in flight waits for another)
           const float* pv = st.mem + (int64_t)v * g.ld_s;
           const float* po = st.mem + (int64_t)s_loth[row] * g.ld_s;
           const float* pf = s.in_feat + (int64_t)s_le[row] * g.ld_e;
-          const int c0 = j * M4_KC + 16 * b - side * g.msg_in;  // x column of t = 0
+          const int c0 = j * M4_KC + 16 * b;  // x column of t = 0
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
             const int cs = c0 + t;
@@ -237,10 +251,9 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
           }
         } else if (v >= 0) {
           for (int t = 0; t < 16; ++t) {
-            const int c = j * M4_KC + 16 * b + t;
-            if (c >= 2 * g.msg_in) break;
-            const int side = c >= g.msg_in;
-            const int cc = c - side * g.msg_in;
+            const int cc = j * M4_KC + 16 * b + t;
+            if (cc >= g.msg_in) break;
+            const int side = side_sel;
             {
               float acc = 0.f;
               for (int q = s_lo[row]; q < s_hi[row]; ++q) {
@@ -259,21 +272,80 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
       tmem_st_wait();
     };
 
-    // ---- 1. D_AG = X2 Wmsg2 ----
-    build(0);
-    cta_sync_tc();
-    for (int j = 0; j < w.nmsg; ++j) {
-      if (tid == 0) issue((j & 1) ? 128 : 0, ((j & 1) ? 128 : 0) + 64, 256, j > 0);
-      if (j + 1 < w.nmsg) build(j + 1);  // into the other buffer, beside MMA j
-      finish();
+    // ---- 1. D_SRC = X_src W_src^T, D_DST = X_dst W_dst^T (TMEM 256 / 256 + Nm) ----
+    const int dsrc = 256, ddst = 256 + w.Nm;
+    if (last_agg) {  // one x per row, both weight sides; the epilogue keeps the row's side
+      build(0, 0, -1);
       cta_sync_tc();
+      A4_MARK(9);
+      for (int j = 0; j < w.nmsg; ++j) {
+        const int ab = (j & 1) ? 128 : 0;
+        if (tid == 0) {  // both weight sides (two staged buffers) back to back
+          issue(ab, ab + 64, dsrc, j > 0);
+          issue(ab, ab + 64, ddst, j > 0, 1);
+        }
+        if (j + 1 < w.nmsg) build(j + 1, (j + 1) & 1, -1);  // the other buffer, beside the MMAs
+        finish();
+        finish();
+        cta_sync_tc();
+      }
+    } else {  // per-side sums: A0 = src side, A1 = dst side
+      A4_MARK(9);
+      for (int j = 0; j < w.nmsg; ++j) {
+        build(j, 0, 0);
+        build(j, 1, 1);
+        cta_sync_tc();
+        if (tid == 0) issue(0, 64, dsrc, j > 0);
+        finish();
+        if (tid == 0) issue(128, 128 + 64, ddst, j > 0);
+        finish();
+        cta_sync_tc();
+      }
     }
+    A4_MARK(10);
     // ---- 2. A2 = [Ag + bias || s] ----
-    for (int j = cg; j < w.Nm / 16; j += 4) {
+    // the row's pre-batch memory, this thread's 16 columns (float4 loads; padding is 0)
+    float sv[16];
+    {
+      const int c0 = 16 * cg;
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        float4 x4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (v >= 0 && c0 + 4 * q4 + 4 <= g.ld_s)
+          x4 = __ldg(reinterpret_cast<const float4*>(st.mem + (int64_t)v * g.ld_s + c0 + 4 * q4));
+        sv[4 * q4] = x4.x; sv[4 * q4 + 1] = x4.y; sv[4 * q4 + 2] = x4.z; sv[4 * q4 + 3] = x4.w;
+      }
+#pragma unroll
+      for (int t = 0; t < 16; ++t)
+        if (c0 + t >= g.d_s) sv[t] = 0.f;
+    }
+    if (cg < w.Nm / 16) {
+      const int j = cg;
       float a[8], b[8], x[16];
-      tmem_ld8_nw(trow + (uint32_t)(256 + 16 * j), a);
-      tmem_ld8_nw(trow + (uint32_t)(256 + 16 * j + 8), b);
-      tmem_ld_wait();
+      if (last_agg) {
+        const int dcol = s_lside[row] ? ddst : dsrc;  // per-lane column: the row's side
+        tmem_ld8_nw(trow + (uint32_t)(dsrc + 16 * j), a);
+        tmem_ld8_nw(trow + (uint32_t)(dsrc + 16 * j + 8), b);
+        float a2[8], b2[8];
+        tmem_ld8_nw(trow + (uint32_t)(ddst + 16 * j), a2);
+        tmem_ld8_nw(trow + (uint32_t)(ddst + 16 * j + 8), b2);
+        tmem_ld_wait();
+        if (dcol == ddst) {
+#pragma unroll
+          for (int t = 0; t < 8; ++t) { a[t] = a2[t]; b[t] = b2[t]; }
+        }
+      } else {
+        float a2[8], b2[8];
+        tmem_ld8_nw(trow + (uint32_t)(dsrc + 16 * j), a);
+        tmem_ld8_nw(trow + (uint32_t)(dsrc + 16 * j + 8), b);
+        tmem_ld8_nw(trow + (uint32_t)(ddst + 16 * j), a2);
+        tmem_ld8_nw(trow + (uint32_t)(ddst + 16 * j + 8), b2);
+        tmem_ld_wait();
+#pragma unroll
+        for (int t = 0; t < 8; ++t) { a[t] += a2[t]; b[t] += b2[t]; }
+      }
+      const float n0 = (float)s_n0[row], n1 = (float)s_n1[row];
+      const float* bl = s_bmsg + (last_agg ? s_lside[row] * g.d_m : 0);
 #pragma unroll
       for (int t = 0; t < 16; ++t) {
         const int c = 16 * j + t;
@@ -281,36 +353,31 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
         if (v < 0 || c >= g.d_m) {
           y = 0.f;
         } else if (last_agg) {
-          y += bmsg[s_lside[row] * g.d_m + c];
+          y += bl[c];
         } else {
-          y += (float)s_n0[row] * bmsg[c] + (float)s_n1[row] * bmsg[g.d_m + c];
-          if (aggregator == STGN_AGG_MEAN) y /= (float)(s_n0[row] + s_n1[row]);
+          y += n0 * s_bmsg[c] + n1 * s_bmsg[g.d_m + c];
+          if (aggregator == STGN_AGG_MEAN) y /= (n0 + n1);
         }
         x[t] = y;
       }
       a4_st16(trow + (uint32_t)(8 * j), trow + (uint32_t)(half + 8 * j), x);
     }
-    for (int j = cg; j < w.Ks / 16; j += 4) {
-      float x[16];
-#pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const int c = 16 * j + t;
-        x[t] = (v >= 0 && c < g.d_s) ? st.mem[(int64_t)v * g.ld_s + c] : 0.f;
-      }
-      a4_st16(trow + (uint32_t)(w.Nm / 2 + 8 * j), trow + (uint32_t)(half + w.Nm / 2 + 8 * j), x);
-    }
+    if (cg < w.Ks / 16)
+      a4_st16(trow + (uint32_t)(w.Nm / 2 + 8 * cg), trow + (uint32_t)(half + w.Nm / 2 + 8 * cg), sv);
     tmem_st_wait();
     cta_sync_tc();
+    A4_MARK(11);
     // ---- D_ZR = Ag [W_z W_r] + s [U_z U_r] ----
     if (tid == 0) issue(0, half, dz, false);
     finish();
     if (tid == 0) issue(w.Nm / 2, half + w.Nm / 2, dz, true);
     finish();
+    A4_MARK(12);
     // ---- z (registers), A3 = r * s over A2's s half ----
-    float zk[2][16];
-    for (int jj = 0; jj < 2; ++jj) {
-      const int j = cg + 4 * jj;
-      if (j >= w.Ns / 16) break;
+    float zk[16];
+    const bool mine = cg < w.Ns / 16;
+    if (mine) {
+      const int j = cg;
       float az[8], bz[8], ar[8], br[8], x[16];
       tmem_ld8_nw(trow + (uint32_t)(dz + 16 * j), az);
       tmem_ld8_nw(trow + (uint32_t)(dz + 16 * j + 8), bz);
@@ -321,42 +388,46 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
       for (int t = 0; t < 16; ++t) {
         const int c = 16 * j + t;
         const bool ok = v >= 0 && c < g.d_s;
-        const float sv = ok ? st.mem[(int64_t)v * g.ld_s + c] : 0.f;
-        const float zp = (t < 8 ? az[t] : bz[t - 8]) + (ok ? bgru[c] : 0.f);
-        const float rp = (t < 8 ? ar[t] : br[t - 8]) + (ok ? bgru[g.d_s + c] : 0.f);
-        zk[jj][t] = m4_sig(zp);
-        x[t] = m4_sig(rp) * sv;
+        const float zp = (t < 8 ? az[t] : bz[t - 8]) + (ok ? s_bgru[c] : 0.f);
+        const float rp = (t < 8 ? ar[t] : br[t - 8]) + (ok ? s_bgru[g.d_s + c] : 0.f);
+        zk[t] = m4_sig(zp);
+        x[t] = m4_sig(rp) * sv[t];
       }
       a4_st16(trow + (uint32_t)(w.Nm / 2 + 8 * j), trow + (uint32_t)(half + w.Nm / 2 + 8 * j), x);
     }
     tmem_st_wait();
     cta_sync_tc();
+    A4_MARK(13);
     // ---- D_H = Ag W_h + (r * s) U_h ----
     if (tid == 0) issue(0, half, dz, false);
     finish();
     if (tid == 0) issue(w.Nm / 2, half + w.Nm / 2, dz, true);
     finish();
-    for (int jj = 0; jj < 2; ++jj) {
-      const int j = cg + 4 * jj;
-      if (j >= w.Ns / 16) break;
+    if (mine) {
+      const int j = cg;
       float a[8], b[8];
       tmem_ld8_nw(trow + (uint32_t)(dz + 16 * j), a);
       tmem_ld8_nw(trow + (uint32_t)(dz + 16 * j + 8), b);
       tmem_ld_wait();
       if (v >= 0) {
-        float* dst = s.mem_new + (int64_t)(d0 + row) * g.ld_s;
+        float out[16];
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
           const int c = 16 * j + t;
-          if (c < g.d_s) {
-            const float cand = tanhf((t < 8 ? a[t] : b[t - 8]) + bgru[2 * g.d_s + c]);
-            const float z = zk[jj][t];
-            dst[c] = (1.f - z) * cand + z * st.mem[(int64_t)v * g.ld_s + c];
-          }
+          const float cand = tanhf((t < 8 ? a[t] : b[t - 8]) + (c < g.d_s ? s_bgru[2 * g.d_s + c] : 0.f));
+          out[t] = (1.f - zk[t]) * cand + zk[t] * sv[t];
         }
+        float* dst = s.mem_new + (int64_t)(d0 + row) * g.ld_s + 16 * j;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+          if (16 * j + 4 * q4 + 4 <= g.ld_s)
+            *reinterpret_cast<float4*>(dst + 4 * q4) =
+                make_float4(out[4 * q4], out[4 * q4 + 1], out[4 * q4 + 2], out[4 * q4 + 3]);
       }
     }
+    A4_MARK(14);
     cta_sync_tc();
+    A4_MARK(15);
   }
   if (warp == 0) tmem_free(tmem, 512);
 }

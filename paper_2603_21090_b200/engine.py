@@ -426,14 +426,12 @@ class _SchedulerView:
         if n == 0:
             return 0.0
         e = self._e
-        acc = e._tab.drift_acc[:n].cpu().numpy()
-        touched = e._tab.drift_touched[:n].cpu().numpy()
-        tau = int(ctl.tau)
-        tot = 0.0
-        for a, t in zip(acc, touched):
-            if a != 0.0:
-                tot += float(a) * e.cfg.gamma ** (tau - int(t))
-        return tot / n
+        torch = e._torch
+        acc = e._tab.drift_acc[:n]
+        dec = torch.pow(torch.tensor(e.cfg.gamma, dtype=torch.float64, device=e.device),
+                        (int(ctl.tau) - e._tab.drift_touched[:n]).to(torch.float64))
+        tot = torch.where(acc != 0.0, acc * dec, torch.zeros_like(acc)).sum()
+        return float(tot.item()) / n  # one reduction on the device (S/drift.py:62-70)
 
 
 class IncrementalEngine:
@@ -632,15 +630,18 @@ class IncrementalEngine:
 
     def _pack_memory_bf16x3(self):
         """Operands of the bf16x3 memory-update kernel (stgn.h t4mem, csrc/mem4.cuh):
-        message weights in K-chunks of 128 columns of X2 = [src-side x | dst-side x],
-        then [w_z; w_r], [u_z; u_r], w_h, u_h, each a K-major bf16 hi/lo block."""
+        message weights in K-chunks of 128 columns of x (w_msg_src chunk j, then
+        w_msg_dst chunk j), then [w_z; w_r], [u_z; u_r], w_h, u_h, each a K-major
+        bf16 hi/lo block."""
         p, dm = self.params, self.dims
         Nm, Ns = _rup(dm.d_m, 16), _rup(dm.d_s, 16)
-        kx = 2 * dm.msg_in
-        nmsg = -(-kx // 128)
-        wm = np.zeros((Nm, nmsg * 128))                     # [n = message unit][k = X2 column]
-        wm[:dm.d_m, :kx] = np.concatenate([p.w_msg_src.T, p.w_msg_dst.T], axis=0).T
-        wm = wm.reshape(Nm, nmsg, 128).transpose(1, 0, 2)  # (nmsg, Nm, 128)
+        nmsg = -(-dm.msg_in // 128)
+        wm = np.zeros((nmsg, 2, Nm, 128))                   # chunk j: [W_src cols, W_dst cols]
+        for side, wsd in enumerate((p.w_msg_src, p.w_msg_dst)):   # (d_m, msg_in)
+            full = np.zeros((Nm, nmsg * 128))
+            full[:dm.d_m, :dm.msg_in] = wsd
+            wm[:, side] = full.reshape(Nm, nmsg, 128).transpose(1, 0, 2)
+        wm = wm.reshape(2 * nmsg, Nm, 128)
         zr0 = np.zeros((2 * Ns, Nm))
         zr0[:dm.d_s, :dm.d_m], zr0[Ns:Ns + dm.d_s, :dm.d_m] = p.w_z, p.w_r
         zr1 = np.zeros((2 * Ns, Ns))
@@ -908,11 +909,15 @@ class IncrementalEngine:
                            max_v=float(mv[i]), z_dev=float(zd[i])) for i in range(n)]
 
     def _after_batch(self, B, t_last, top):
-        r = self._rep
-        dm = self.dims
         self._m += B
         self._t_now = t_last
         self._store_n = max(self._store_n, top)
+        self._account(self._rep, B, t_last, self.batch_index)
+
+    def _account(self, r, B, t_last, index):
+        """Counters, last_report and the last batch's set sizes from a report
+        (synchronous calls, or a pipelined caller collecting batch `index`)."""
+        dm = self.dims
         self._last_nD, self._last_nA = int(r.direct), int(r.affected)
         nD, nA = self._last_nD, self._last_nA
         c = self.counters
@@ -946,7 +951,7 @@ class IncrementalEngine:
         c.add("direct", nD)
         c.add("affected", nA)
         self.last_global_drift = float(r.global_drift)
-        self.last_report = BatchReport(index=self.batch_index, edges=B, t_batch=t_last,
+        self.last_report = BatchReport(index=index, edges=B, t_batch=t_last,
                                        direct=nD, affected=nA, rebuild=kind, rebuild_nodes=rb)
 
     def _mac_attn(self, n, e):

@@ -169,6 +169,12 @@ class StreamingEngine:
         self._d = [dict(src=devb(B, dt=torch.int32), dst=devb(B, dt=torch.int32),
                         t=devb(B, dt=torch.float64), feat=devb(B, max(d_e, 1), dt=torch.float32))
                    for _ in range(self.depth)]
+        # per-slot copy of the batch's result block (counters): device copy on the engine
+        # stream right behind the batch, read back with the scores
+        nres = int(engine._L.stgn_batch_result_bytes())
+        self._res_d = [devb(nres, dt=torch.uint8) for _ in range(self.depth)]
+        self._res_h = [host(nres, dt=torch.uint8) for _ in range(self.depth)]
+        self._meta = [None] * self.depth     # (edges, t_last, batch index) of the slot's batch
         self._used = [None] * self.depth   # event on the engine stream: slot's graph enqueued
         self._done = [None] * self.depth   # event on the download stream: scores in pinned memory
         self._pending = []                 # (batch number, slot, n), submission order
@@ -214,12 +220,19 @@ class StreamingEngine:
         preds = eng.process_batch_device(
             d["src"][:n], d["dst"][:n], d["t"][:n], d["feat"][:n, :self.d_e] if has_feat else None,
             max_id=int(max(src.max(), dst.max())), t_first=float(t[0]), t_last=float(t[-1]))
+        import ctypes as C
+        from . import _lib
+        _lib.check(eng._L.stgn_engine_result_copy(
+            eng._handle, C.c_void_p(self._res_d[k].data_ptr()), 1,
+            C.c_void_p(main.cuda_stream)), "result_copy")
+        self._meta[k] = (n, float(t[-1]), eng.batch_index)
         used = torch.cuda.Event()
         used.record(main)
         self._used[k] = used
         self.down.wait_event(used)
         with torch.cuda.stream(self.down):
             h["preds"][:n].copy_(preds, non_blocking=True)
+            self._res_h[k].copy_(self._res_d[k], non_blocking=True)
             done = torch.cuda.Event()
             done.record(self.down)
         preds.record_stream(self.down)
@@ -230,10 +243,22 @@ class StreamingEngine:
         return self.submitted - 1
 
     def _pop(self):
+        import ctypes as C
+        from . import _lib
         num, slot, n = self._pending.pop(0)
         self._done[slot].synchronize()
         self._ready.append((num, self._h[slot]["preds"][:n].numpy().copy()))
         self._done[slot] = None
+        # the batch's counters and report (S/runner.py:73-77), in submission order
+        eng = self.eng
+        rep = _lib.Report()
+        _lib.check(eng._L.stgn_report_from_result(C.c_void_p(self._res_h[slot].data_ptr()),
+                                                  C.byref(rep)), "report")
+        edges, t_last, index = self._meta[slot]
+        eng.counters.start_batch()
+        eng._account(rep, edges, t_last, index)
+        if num != self.submitted - 1:  # the device-side lists belong to a later batch
+            eng._last_nD = eng._last_nA = None
         return slot
 
     def _collect(self, until_slot):

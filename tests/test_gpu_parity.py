@@ -362,6 +362,10 @@ def test_streaming_engine_matches_synchronous(cuda):
     n = int(z["node_count"])
     np.testing.assert_array_equal(eng.memory.states[:n], sync.memory.states[:n])
     np.testing.assert_array_equal(eng.cache.h[:n], sync.cache.h[:n])
+    # the pipelined path delivers the per-batch surface too: counter totals and the
+    # last batch's report, read back with the scores (stgn_engine_result_copy)
+    assert eng.counters.totals == sync.counters.totals
+    assert eng.last_report == sync.last_report
 
 
 @pytest.mark.parametrize("name,layers,seed", [("k1", 1, 3), ("k2", 2, 5)])
