@@ -101,8 +101,11 @@ def config_json(args, n_gpus):
 
 
 def make_stream(args, n_edges, rank):
+    """The C4 stream. Every rank replays the same stream (replicas of one serving
+    engine, weak scaling): the sharded full-rebuild leg all-gathers rows across
+    ranks and needs identical replicas (`rank` is kept for the call sites)."""
     from paper_2603_21090_b200.streamio import generate_stream
-    return generate_stream(args.seed + rank, args.nodes, n_edges, attachment="preferential",
+    return generate_stream(args.seed, args.nodes, n_edges, attachment="preferential",
                            d_e=0)
 
 

@@ -190,6 +190,10 @@ typedef struct {
   int32_t  *ev_node, *ev_dpos, *ev_dn, *ev_nv;  /* [ev_cap] node, direct index or -1, |dN|, |N| */
   double   *ev_bound, *ev_maxv, *ev_zdev;        /* [ev_cap] */
   int64_t  ev_cap;
+  /* optional payload log for historical snapshots (OracleEngine.full_recompute(t_now),
+   * S/oracle.py:40-65): the frozen payload stack of every store entry, indexed like
+   * e_prev (2*eid + side); NULL = not kept */
+  float    *e_pay;          /* [2*cap_edges][K][ld_d] */
 } stgn_state;
 
 /* Per-batch report written by process_batch (host memory). Counter
@@ -303,6 +307,14 @@ const char* stgn_stage_name(int i);
  * memory-update smem bytes, split-TF32 tensor-core kernel active, its tile
  * rows, bf16x3 128-row kernel active, its smem bytes]. */
 int stgn_engine_info(stgn_engine* eng, int64_t* info, int n);
+
+/* Pure full recompute (OracleEngine.full_recompute, S/oracle.py:47-65): every
+ * node's K layers into layers_out_dev [node_count][K][ld_d] (device memory); no
+ * state is touched. t_now = +inf: the current lists (the store's top-L, cached
+ * or not); a finite t_now: each node's L newest store entries with t <= t_now,
+ * rebuilt from the store chains and the payload log (needs stgn_state.e_pay). */
+int stgn_engine_snapshot(stgn_engine* eng, int64_t node_count, double t_now,
+                         float* layers_out_dev, void* stream);
 
 /* Per-batch result block (counters of the last enqueued batch), for pipelined
  * callers that do not block on a report: stgn_engine_result_copy copies it

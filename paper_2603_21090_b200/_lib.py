@@ -29,7 +29,7 @@ EXPORTS = (
     "stgn_engine_info", "stgn_debug_tc_gemm", "stgn_generate_stream",
     "stgn_debug_a4_prof", "stgn_engine_set_scope", "stgn_read_stream",
     "stgn_engine_set_skip_recompute", "stgn_engine_delta_events", "stgn_batch_result_bytes",
-    "stgn_engine_result_copy", "stgn_report_from_result",
+    "stgn_engine_result_copy", "stgn_report_from_result", "stgn_engine_snapshot",
 )
 
 
@@ -73,7 +73,8 @@ DELTA_PTRS = ("attn_logz", "ev_node", "ev_dpos", "ev_dn", "ev_nv", "ev_bound", "
 
 class State(C.Structure):
     _fields_ = [("cap_nodes", C.c_int64), ("cap_edges", C.c_int64), ("gpow_len", C.c_int64)] + \
-               [(n, C.c_void_p) for n in STATE_PTRS + DELTA_PTRS] + [("ev_cap", C.c_int64)]
+               [(n, C.c_void_p) for n in STATE_PTRS + DELTA_PTRS] + [("ev_cap", C.c_int64),
+                                                                    ("e_pay", C.c_void_p)]
 
 
 class Report(C.Structure):
@@ -113,6 +114,7 @@ def lib():
                                                 P(Report), vp]
     L.stgn_engine_rebuild.argtypes = [vp, vp, i64, i64, dbl, P(i64), vp]
     L.stgn_engine_full_reference.argtypes = [vp, i64, vp, vp]
+    L.stgn_engine_snapshot.argtypes = [vp, i64, dbl, vp, vp]
     L.stgn_engine_affected.argtypes = [vp, vp, vp, i64, P(i64), P(i64), vp, vp]
     L.stgn_engine_pred_embeddings.argtypes = [vp, vp, i64, vp]
     L.stgn_pipeline_many.argtypes = [P(Dims), i64, i64] + [vp] * 18

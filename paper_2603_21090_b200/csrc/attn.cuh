@@ -48,6 +48,8 @@ struct RingSrc {
   double valid_at_const;
   int write_valid;
   float* final_out;             // nullable: write last layer to final_out[idx] instead of h
+  float* layers_out;            // nullable: write every layer l to layers_out[idx][l] instead of h
+                                // (pure snapshot recompute, full_recompute)
   float* dpred;                 // nullable: copy last layer of idx < *dpred_count into dpred[idx]
   const int32_t* dpred_count;
   unsigned long long* e_count;  // nullable: sum of entry counts
@@ -356,7 +358,9 @@ attn_kernel(Geo g, AttnWeights w, RingSrc rs, FlatSrc fs, int T) {
         } else {
           const int64_t idx = base + i;
           const bool last = (l == g.K - 1);
-          if (rs.final_out) {  // read-only recompute (full_reference)
+          if (rs.layers_out) {
+            rs.layers_out[(idx * g.K + l) * g.ld_d + j] = v;
+          } else if (rs.final_out) {  // read-only recompute (full_reference)
             if (last) rs.final_out[idx * g.ld_d + j] = v;
           } else {
             rs.h[((int64_t)node * g.K + l) * g.ld_d + j] = v;

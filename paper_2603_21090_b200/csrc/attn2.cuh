@@ -290,6 +290,8 @@ attn2_kernel(Geo g, EngW w, RingSrc rs, int tmax, int wsm_floats) {
         const int mode = s_mode[i];
         if (mode == 1) {  // direct node, pre-batch memory: prediction embedding only
           if (last) rs.dpred[idx * g.ld_d + j] = v;
+        } else if (rs.layers_out) {
+          rs.layers_out[(idx * g.K + l) * g.ld_d + j] = v;
         } else if (rs.final_out) {
           if (last) rs.final_out[idx * g.ld_d + j] = v;
         } else {

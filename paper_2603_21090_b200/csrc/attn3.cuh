@@ -557,6 +557,8 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
             if (node >= 0 && j < g.d) {
               if (mode == 1) {
                 if (last) rs.dpred[idx * g.ld_d + j] = x;
+              } else if (rs.layers_out) {
+                rs.layers_out[(idx * g.K + l) * g.ld_d + j] = x;
               } else if (rs.final_out) {
                 if (last) rs.final_out[idx * g.ld_d + j] = x;
               } else {

@@ -1315,6 +1315,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
         float* dst = nullptr;
         if (node >= 0) {
           if (mode == 1) dst = last ? rs.dpred + idx * g.ld_d : nullptr;
+          else if (rs.layers_out) dst = rs.layers_out + (idx * g.K + l) * g.ld_d;
           else if (rs.final_out) dst = last ? rs.final_out + idx * g.ld_d : nullptr;
           else dst = rs.h + ((int64_t)node * g.K + l) * g.ld_d;
         }

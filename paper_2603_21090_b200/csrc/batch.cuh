@@ -41,6 +41,7 @@ struct StateView {
   int32_t *ev_node, *ev_dpos, *ev_dn, *ev_nv;
   double *ev_bound, *ev_maxv, *ev_zdev;
   int64_t ev_cap;
+  float* e_pay;       // nullable: [2 cap_edges][K][ld_d] frozen payload of every store entry
   int32_t *e_src, *e_dst;
   double* e_t;
   float* e_feat;
@@ -238,6 +239,14 @@ __global__ void k_ring(Geo g, StateView st, Scratch s, const double* __restrict_
     if (lane == 0) {
       const int p = s.rec_prev[r];
       st.e_prev[entry_index(hd->m0, r)] = p >= 0 ? entry_index(hd->m0, p) : st.adj_head[v];
+    }
+    if (st.e_pay) {  // the payload log of every store entry (historical snapshots)
+      float* ep = st.e_pay + entry_index(hd->m0, r) * g.K * g.ld_d;
+      for (int l = 0; l < g.K; ++l) {
+        const float* src = l == 0 ? st.mem + (int64_t)u * g.ld_s
+                                  : st.h + ((int64_t)u * g.K + (l - 1)) * g.ld_d;
+        for (int j = lane; j < g.d; j += 32) ep[l * g.ld_d + j] = (l > 0 || j < g.d_s) ? src[j] : 0.f;
+      }
     }
     const int kadj = st.nodeadj[v];
     const int kk = kadj < g.L ? kadj : g.L;

@@ -15,6 +15,7 @@
 #include "attn4.cuh"
 #include "mem4.cuh"
 #include "delta.cuh"
+#include "snapshot.cuh"
 
 #ifndef STGN_VERSION
 #define STGN_VERSION "stgn 0.1.0 sm_100a"
@@ -396,6 +397,7 @@ int stgn_engine_bind(stgn_engine* e, const stgn_state* s) {
   v.attn_logz = s->attn_logz; v.ev_node = s->ev_node; v.ev_dpos = s->ev_dpos; v.ev_dn = s->ev_dn;
   v.ev_nv = s->ev_nv; v.ev_bound = s->ev_bound; v.ev_maxv = s->ev_maxv; v.ev_zdev = s->ev_zdev;
   v.ev_cap = s->attn_logz ? s->ev_cap : 0;
+  v.e_pay = s->e_pay;
   v.e_src = s->e_src; v.e_dst = s->e_dst; v.e_t = s->e_t; v.e_feat = s->e_feat;
   v.e_prev = s->e_prev; v.adj_head = s->adj_head; v.adj_deg = s->adj_deg;
   v.gpow = s->gpow; v.gpow_len = s->gpow_len; v.ctl = s->ctl;
@@ -969,6 +971,45 @@ extern "C" int stgn_engine_delta_events(stgn_engine* e, int64_t max, int32_t* no
     if (emb) memcpy(emb + k * e->g.d, he.data() + i * e->g.d, sizeof(float) * e->g.d);
   }
   return (int)n;
+}
+
+extern "C" int stgn_engine_snapshot(stgn_engine* e, int64_t node_count, double t_now,
+                                    float* layers_out_dev, void* stream) {
+  if (!e || !e->bound || !e->have_w || !layers_out_dev) return STGN_ERR_INVALID;
+  if (node_count > e->st.cap_nodes) return STGN_ERR_CAPACITY;
+  if (node_count <= 0) return STGN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  RingSrc r = ring_src(e);
+  r.list = nullptr;
+  r.count_const = node_count;
+  r.use_store = 1;
+  r.ring_ccnt = e->sv.ring_cnt;  // the store's top-L lists (S/oracle.py:40-45), not the window's
+  r.layers_out = layers_out_dev;
+  uint8_t* tmp = nullptr;
+  if (std::isfinite(t_now)) {  // historical lists from the store chains + payload log
+    if (!e->sv.e_pay) return STGN_ERR_INVALID;
+    const size_t bytes = hist_rings_bytes(e->g, node_count);
+    CUDA_TRY(cudaMallocAsync((void**)&tmp, bytes, st));
+    CUDA_TRY(cudaMemsetAsync(tmp, 0, bytes, st));
+    HistRings hr = hist_rings_carve(e->g, node_count, tmp);
+    k_hist_rings<<<8 * e->num_sms, 256, 0, st>>>(e->g, e->sv, hr, node_count, t_now, e->w.omega);
+    r.ring_cnt = hr.cnt;
+    r.ring_ccnt = hr.cnt;
+    r.ring_head = hr.head;
+    r.ring_t = hr.t;
+    r.ring_pay = hr.pay;
+    r.ring_feat = hr.feat;
+    r.ring_tb = hr.tb;
+  }
+  launch_attn(e, r, st);
+  cudaError_t ce = cudaGetLastError();
+  if (tmp) cudaFreeAsync(tmp, st);
+  if (ce != cudaSuccess) {
+    stgn_set_error(__FILE__, __LINE__, ce);
+    return STGN_ERR_CUDA;
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return STGN_OK;
 }
 
 extern "C" int stgn_engine_full_reference(stgn_engine* e, int64_t node_count, float* out_dev,

@@ -186,7 +186,8 @@ class _Tables:
 
     def _alloc_edges(self, E):
         torch, g = self.eng._torch, self.eng
-        old = {k: getattr(self, k) for k in self.EDGE} if self.cap_edges else {}
+        names = self.EDGE + (("e_pay",) if g.edge_payloads else ())
+        old = {k: getattr(self, k) for k in names} if self.cap_edges else {}
         e0 = self.cap_edges
         z = self._z
         self.e_src = z(E, dt=torch.int32)
@@ -194,8 +195,10 @@ class _Tables:
         self.e_t = z(E, dt=torch.float64)
         self.e_feat = z(E, g.ld_e)
         self.e_prev = z(2 * E, dt=torch.int64, fill=-1)
+        # payload log (stgn.h e_pay): every store entry's frozen stack, for snapshots
+        self.e_pay = z(2 * E, g.K, g.ld_d) if g.edge_payloads else None
         for k, t in old.items():
-            lim = 2 * e0 if k == "e_prev" else e0
+            lim = 2 * e0 if k in ("e_prev", "e_pay") else e0
             getattr(self, k)[:lim].copy_(t[:lim])
         self.cap_edges = E
 
@@ -234,6 +237,7 @@ class _Tables:
         for name in _lib.STATE_PTRS + _lib.DELTA_PTRS:
             setattr(s, name, getattr(self, name).data_ptr())
         s.ev_cap = self.ev_cap
+        s.e_pay = self.e_pay.data_ptr() if self.e_pay is not None else None
         return s
 
 
@@ -454,8 +458,9 @@ class IncrementalEngine:
 
     def __init__(self, cfg: RunConfig, params: ModelParameters, *, recompute: str = "affected",
                  max_batch: int | None = None, device: int | None = None,
-                 tensor_cores: bool | str = True):
+                 tensor_cores: bool | str = True, edge_payloads: bool = False):
         cfg.validate()
+        self.edge_payloads = bool(edge_payloads)  # keep every entry's payload (snapshots)
         if cfg.mode == "delta":
             if recompute not in ("affected", "delta"):
                 raise ConfigError("delta mode recomputes by its own classification")
@@ -1028,6 +1033,24 @@ class IncrementalEngine:
                                                           self._stream()), "full_reference")
         return out[:n, :self.dims.d].double().cpu().numpy()
 
+    def snapshot_layers(self, t_now: float | None = None) -> np.ndarray:
+        """Pure K-layer recompute of every node (OracleEngine.full_recompute,
+        S/oracle.py:47-65): (n, K, d) float64; nothing is mutated. t_now earlier
+        than the newest edge uses each node's L newest entries with t <= t_now
+        (S/graph_store.py:158-173) and needs edge_payloads=True."""
+        torch = self._torch
+        n = self.node_count
+        self._ensure_nodes(n)
+        hist = t_now is not None and self._m > 0 and t_now < self._t_now
+        if hist and not self.edge_payloads:
+            raise ConfigError("historical snapshots need IncrementalEngine(edge_payloads=True)")
+        out = torch.zeros((max(n, 1), self.K, self.ld_d), dtype=torch.float32, device=self.device)
+        if n:
+            _lib.check(self._L.stgn_engine_snapshot(self._handle, n,
+                                                    float(t_now) if hist else math.inf,
+                                                    out.data_ptr(), self._stream()), "snapshot")
+        return out[:n, :, :self.dims.d].double().cpu().numpy()
+
     def rebuild_range(self, lo: int, hi: int):
         """Exact recompute of node ids [lo, hi); returns their layer-cache rows
         (device tensor [hi-lo, K, d])."""
@@ -1061,9 +1084,16 @@ class IncrementalEngine:
             tref = tab.ring_t[:n].gather(1, head.unsqueeze(1)).squeeze(1)
             tab.attn_tref[:n] = torch.where(tab.ring_ccnt[:n] > 0, tref, torch.zeros_like(tref))
         # rebuild_range counted this rank's shard; a single-device rebuild counts all n
-        from .dist import shard_range
+        from .dist import gather_rows, shard_range
         import torch.distributed as dist
         lo, hi = shard_range(n, dist.get_world_size(group), dist.get_rank(group))
+        if self.recompute == "delta" and self.K == 1:
+            # the rebuilt states' log Z (csrc/delta.cuh) from every shard, and the
+            # running max value norm over all of them
+            tab.attn_logz[:n] = gather_rows(tab.attn_logz[lo:hi].clone(), n, group)
+            mvn = tab.ctl[4:5].view(self._torch.float64).clone()
+            dist.all_reduce(mvn, op=dist.ReduceOp.MAX, group=group)
+            tab.ctl[4:5] = mvn.view(self._torch.int64)
         self.counters.add("rebuild_pipelines", n - (hi - lo))
         return n
 

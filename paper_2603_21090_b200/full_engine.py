@@ -9,11 +9,13 @@ over all node ids). Predictions equal IncrementalEngine's in exact mode (the
 reference pins incremental == oracle bitwise, T/test_engine.py:262-273), so
 the batch step reuses it and adds the O(n) refresh.
 
-Differences from the reference, by design: the snapshot refresh also writes
-the layer cache (the reference's apply_batch_full does the same; its
-stand-alone full_recompute is pure); historical snapshots (t_now earlier than
-the store's newest edge) and finite neighbour-cache windows (the oracle lists
-ignore the window) are not supported and raise.
+full_recompute(t_now) is pure, as the reference's (stgn_engine_snapshot: every
+layer of every node into a fresh buffer). A t_now earlier than the newest edge
+rebuilds each node's list from the append-only store (the L newest entries with
+t <= t_now) and the engine's payload log of every entry's frozen stack, which
+this engine keeps (edge_payloads=True). apply_batch_full refreshes the layer
+cache like the reference's. A finite neighbour-cache window is refused: the
+reference's oracle lists ignore it, the incremental batch path does not.
 """
 
 from __future__ import annotations
@@ -53,6 +55,7 @@ class OracleEngine:
             raise ConfigError("the full-recompute engine reads the store's top-L lists; "
                               "a finite neighbour-cache window is not supported")
         # drift-aware rebuilds are moot when every batch rebuilds everything
+        kw.setdefault("edge_payloads", True)
         self._eng = IncrementalEngine(dataclasses.replace(cfg, rebuild="never"), params, **kw)
         self.cfg, self.params = cfg, params
         self.last_pred_embeddings: dict[int, np.ndarray] = {}
@@ -83,17 +86,19 @@ class OracleEngine:
         return self._eng.batch_index
 
     def full_recompute(self, t_now: float | None = None) -> EngineSnapshot:
-        """K-layer attention for every node (S/oracle.py:49-65)."""
-        eng = self._eng
-        if t_now is not None and t_now < eng.store.t_now:
-            raise NotImplementedError("historical snapshots are not supported on the GPU path")
-        eng.rebuild_nodes(None)
-        return self._snapshot(t_now)
+        """K-layer attention for every node; pure (S/oracle.py:47-65)."""
+        return self._snapshot(t_now, self._eng.snapshot_layers(t_now))
 
-    def _snapshot(self, t_now=None) -> EngineSnapshot:
+    def _refresh(self) -> EngineSnapshot:
+        """apply_batch_full's snapshot: the full recompute written to the layer cache."""
+        self._eng.rebuild_nodes(None)
+        return self._snapshot()
+
+    def _snapshot(self, t_now=None, layers=None) -> EngineSnapshot:
         eng = self._eng
         n = eng.node_count
-        layers = eng.cache.h[:n].copy()
+        if layers is None:
+            layers = eng.cache.h[:n].copy()
         ts = t_now if t_now is not None else (eng.store.t_now if eng.store.m else 0.0)
         return EngineSnapshot(embeddings=layers[:, -1, :].copy(), layers=layers,
                               memory=eng.memory.states[:n].copy(),
@@ -108,7 +113,7 @@ class OracleEngine:
             return [], self._snapshot()
         if not snapshot:
             return preds, self._snapshot()
-        return preds, self.full_recompute()
+        return preds, self._refresh()
 
     def apply_batch_arrays(self, src, dst, t, feat=None, snapshot: bool = True):
         """Array form of apply_batch_full (no TemporalEdge objects)."""
@@ -116,4 +121,4 @@ class OracleEngine:
         self.last_pred_embeddings = dict(self._eng.last_pred_embeddings)
         if not snapshot or len(preds) == 0:
             return preds, self._snapshot()
-        return preds, self.full_recompute()
+        return preds, self._refresh()

@@ -38,9 +38,15 @@ def main(cases=("k2_last_adaptive", "k1_fixed_de0")):
         for i in range(0, len(stream), B):
             p, snap = eng.apply_batch_full(stream[i:i + B])
             preds.extend(p)
+        # pure historical snapshots (full_recompute(t_now), S/oracle.py:40-65) at a
+        # few times inside the stream, plus the current-state one
+        ts = np.array([e.t for e in stream])
+        t_hist = np.array([ts[len(ts) // 7], ts[len(ts) // 2], ts[-B - 1], ts[-1] + 1.0])
+        hist = [eng.full_recompute(float(t)).layers for t in t_hist]
         np.savez_compressed(os.path.join(HERE, f"oracle_engine_{name}.npz"),
                             preds=np.array(preds), layers=snap.layers, memory=snap.memory,
-                            last=snap.last_interaction, timestamp=np.array([snap.timestamp]))
+                            last=snap.last_interaction, timestamp=np.array([snap.timestamp]),
+                            t_hist=t_hist, hist_layers=np.stack(hist))
         print(name, len(preds), snap.layers.shape)
 
 

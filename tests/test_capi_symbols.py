@@ -46,13 +46,13 @@ def test_struct_layouts_match_header():
     assert C.sizeof(_lib.Config) == 4 * 4 + 4 * 8 + 2 * 4
     assert C.sizeof(_lib.Ctl) == 8 + 8 + 4 + 4 + 6 * 8
     assert C.sizeof(_lib.Report) == 12 * 8 + 8 + 4 * 8 + 3 * 8
-    assert C.sizeof(_lib.State) == 3 * 8 + (len(_lib.STATE_PTRS) + len(_lib.DELTA_PTRS)) * 8 + 8
+    assert C.sizeof(_lib.State) == 3 * 8 + (len(_lib.STATE_PTRS) + len(_lib.DELTA_PTRS)) * 8 + 8 + 8
     hdr = _header()
     state_block = hdr[hdr.index("typedef struct {\n  int64_t cap_nodes"):]
     state_block = state_block[:state_block.index("} stgn_state;")]
     state_block = re.sub(r"/\*.*?\*/", "", state_block, flags=re.S)
     names = re.findall(r"\*\s*([a-z_0-9]+)", state_block)
-    assert tuple(names) == _lib.STATE_PTRS + _lib.DELTA_PTRS
+    assert tuple(names) == _lib.STATE_PTRS + _lib.DELTA_PTRS + ("e_pay",)
 
 
 def test_engine_refuses_without_gpu():

@@ -330,6 +330,17 @@ def test_full_recompute_engine_matches_reference_oracle(cuda, name):
     assert_rows_close(snap.memory[:n], zo["memory"], "memory")
     np.testing.assert_array_equal(snap.last_interaction[:n], zo["last"])
     assert snap.timestamp == float(zo["timestamp"][0])
+    # pure historical snapshots: full_recompute(t_now) rebuilds each node's list from the
+    # store (L newest entries with t <= t_now) and the payload log; nothing is mutated
+    h_before = eng.cache.h.copy()
+    mem_before = eng.memory.states.copy()
+    for t_now, ref in zip(zo["t_hist"], zo["hist_layers"]):
+        hs = eng.full_recompute(float(t_now))
+        assert hs.timestamp == float(t_now)
+        assert_rows_close(hs.layers[:n].reshape(n, -1), ref.reshape(n, -1),
+                          f"snapshot layers t={t_now}")
+    np.testing.assert_array_equal(eng.cache.h, h_before)
+    np.testing.assert_array_equal(eng.memory.states, mem_before)
 
 
 def test_streaming_engine_matches_synchronous(cuda):
