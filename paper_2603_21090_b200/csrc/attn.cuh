@@ -66,12 +66,17 @@ struct RingSrc {
     if (fused) return (int64_t)pre_n[0] + post_n[0];
     return count_ptr ? (int64_t)count_ptr[0] : count_const;
   }
+  int own_lo, own_hi;            // node-id shard (own_hi <= own_lo: all): other rows are skipped
   __device__ int node(int64_t idx) const {
+    int v;
     if (fused) {
       const int p = pre_n[0];
-      return list[idx < p ? idx : idx - p];
+      v = list[idx < p ? idx : idx - p];
+    } else {
+      v = list ? list[idx] : (int)idx;
     }
-    return list ? list[idx] : (int)idx;
+    if (own_hi > own_lo && (v < own_lo || v >= own_hi)) return -1;
+    return v;
   }
 };
 
@@ -187,11 +192,13 @@ attn_kernel(Geo g, AttnWeights w, RingSrc rs, FlatSrc fs, int T) {
           E = (int)(fs.offsets[idx + 1] - lo);
         } else {
           node = rs.node(idx);
-          const int cc = rs.ring_ccnt[node];
-          E = cc >= 0 ? cc : (rs.use_store ? rs.ring_cnt[node] : 0);
-          head = rs.ring_head[node];
-          if (E > 0) tref = rs.ring_t[(int64_t)node * g.L + head];
-          if (rs.e_count && E) atomicAdd(rs.e_count, (unsigned long long)E);
+          if (node >= 0) {
+            const int cc = rs.ring_ccnt[node];
+            E = cc >= 0 ? cc : (rs.use_store ? rs.ring_cnt[node] : 0);
+            head = rs.ring_head[node];
+            if (E > 0) tref = rs.ring_t[(int64_t)node * g.L + head];
+            if (rs.e_count && E) atomicAdd(rs.e_count, (unsigned long long)E);
+          }
         }
       }
       s_node[i] = node;

@@ -87,9 +87,9 @@ attn2_kernel(Geo g, EngW w, RingSrc rs, int tmax, int wsm_floats) {
       if (i < T && idx < N) {
         node = rs.node(idx);
         if (rs.fused) mode = idx >= pre_rows ? 2 : (idx < d_rows ? 1 : 0);
-        const int cc = rs.ring_ccnt[node];
-        E = cc >= 0 ? cc : (rs.use_store ? rs.ring_cnt[node] : 0);
-        head = rs.ring_head[node];
+        const int cc = node >= 0 ? rs.ring_ccnt[node] : 0;
+        E = node < 0 ? 0 : (cc >= 0 ? cc : (rs.use_store ? rs.ring_cnt[node] : 0));
+        head = node >= 0 ? rs.ring_head[node] : 0;
         if (E > 0) tref = rs.ring_t[(int64_t)node * g.L + head];
       }
       s_node[i] = node;

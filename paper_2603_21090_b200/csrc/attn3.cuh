@@ -233,9 +233,9 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
       if (i < T && idx < N) {
         node = rs.node(idx);
         if (rs.fused) mode = idx >= pre_rows ? 2 : (idx < d_rows ? 1 : 0);
-        const int cc = rs.ring_ccnt[node];
-        E = cc >= 0 ? cc : (rs.use_store ? rs.ring_cnt[node] : 0);
-        head = rs.ring_head[node];
+        const int cc = node >= 0 ? rs.ring_ccnt[node] : 0;
+        E = node < 0 ? 0 : (cc >= 0 ? cc : (rs.use_store ? rs.ring_cnt[node] : 0));
+        head = node >= 0 ? rs.ring_head[node] : 0;
         if (E > 0) tref = rs.ring_t[(int64_t)node * g.L + head];
       }
       s_node[i] = node; s_E[i] = E; s_head[i] = head; s_tref[i] = tref; s_mode[i] = mode;
@@ -256,9 +256,9 @@ attn3_kernel(Geo g, TcW w, RingSrc rs, int tmax) {
       int node = -1, E = 0, head = 0;
       if (has_next && i < T && idx < N) {
         node = rs.node(idx);
-        const int cc = rs.ring_ccnt[node];
-        E = cc >= 0 ? cc : (rs.use_store ? rs.ring_cnt[node] : 0);
-        head = rs.ring_head[node];
+        const int cc = node >= 0 ? rs.ring_ccnt[node] : 0;
+        E = node < 0 ? 0 : (cc >= 0 ? cc : (rs.use_store ? rs.ring_cnt[node] : 0));
+        head = node >= 0 ? rs.ring_head[node] : 0;
       }
       s_nnode[i] = node; s_nE[i] = E; s_nhead[i] = head;
     }

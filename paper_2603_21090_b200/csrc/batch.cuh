@@ -240,6 +240,21 @@ __global__ void k_ring(Geo g, StateView st, Scratch s, const double* __restrict_
       const int p = s.rec_prev[r];
       st.e_prev[entry_index(hd->m0, r)] = p >= 0 ? entry_index(hd->m0, p) : st.adj_head[v];
     }
+    if (!geo_owns(g, v)) {  // sharded engine: another rank keeps this node's payload rows
+      if (lane == 0) {
+        const int kadj = st.nodeadj[v];
+        const int kk = kadj < g.L ? kadj : g.L;
+        if (a < kk) {
+          int slot = (st.ring_head[v] - kk + a) % g.L;
+          if (slot < 0) slot += g.L;
+          const int64_t rs = (int64_t)v * g.L + slot;
+          st.ring_nbr[rs] = u;
+          st.ring_eid[rs] = hd->m0 + i;
+          st.ring_t[rs] = s.in_t[i];
+        }
+      }
+      continue;
+    }
     if (st.e_pay) {  // the payload log of every store entry (historical snapshots)
       float* ep = st.e_pay + entry_index(hd->m0, r) * g.K * g.ld_d;
       for (int l = 0; l < g.K; ++l) {

@@ -21,7 +21,12 @@ struct Geo {
   int half;             // d_t / 2
   float inv_sqrt_dk;
   float phi_amp;        // sqrt(1/d_t)
+  int own_lo, own_hi;   // node-id shard of this engine (own_hi <= own_lo: every node);
+                        // frozen payload rows are kept and recomputed for owned nodes only
 };
+__host__ __device__ inline bool geo_owns(const Geo& g, int v) {
+  return g.own_hi <= g.own_lo || (v >= g.own_lo && v < g.own_hi);
+}
 
 static inline Geo make_geo(const stgn_dims& dm, int L) {
   Geo g;
@@ -40,6 +45,7 @@ static inline Geo make_geo(const stgn_dims& dm, int L) {
   g.half = dm.d_t / 2;
   g.inv_sqrt_dk = (float)(1.0 / sqrt((double)dm.d_k));
   g.phi_amp = (float)sqrt(1.0 / (double)dm.d_t);
+  g.own_lo = g.own_hi = 0;
   return g;
 }
 

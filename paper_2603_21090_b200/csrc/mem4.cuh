@@ -161,16 +161,22 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
     mbar_wait(&wbar[Gi & 1], (uint32_t)((Gi >> 1) & 1));
     m4_mma(tmem, a_hi, a_lo, (Gi & 1) ? Wb1 : Wb0, w.np[j], w.kp[j], dcol, acc, &mbar);
   };
-  auto finish = [&]() {  // every thread: the MMA of block G is done; refill its buffer
-    mbar_wait(&mbar, (uint32_t)(G & 1));
-    tc_fence_after();
-    if (tid == 0 && G + 2 < total_blocks) stage(G + 2);
-    ++G;
-  };
   auto cta_sync_tc = [&]() {
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+  };
+  // The MMAs of the next n blocks are done (their buffers refilled two blocks ahead),
+  // then a CTA barrier. tid 0 is the only waiter on the commit barrier, in phase
+  // order, so no waiter can fall two parity phases behind the commits.
+  auto wait_mma = [&](int n) {
+    if (tid == 0)
+      for (int k = 0; k < n; ++k) {
+        mbar_wait(&mbar, (uint32_t)((G + k) & 1));
+        if (G + k + 2 < total_blocks) stage(G + k + 2);
+      }
+    G += n;
+    cta_sync_tc();
   };
   const bool last_agg = aggregator == STGN_AGG_LAST;
   const int phi0 = 2 * g.d_s + g.d_e;
@@ -285,9 +291,7 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
           issue(ab, ab + 64, ddst, j > 0, 1);
         }
         if (j + 1 < w.nmsg) build(j + 1, (j + 1) & 1, -1);  // the other buffer, beside the MMAs
-        finish();
-        finish();
-        cta_sync_tc();
+        wait_mma(2);
       }
     } else {  // per-side sums: A0 = src side, A1 = dst side
       A4_MARK(9);
@@ -295,11 +299,11 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
         build(j, 0, 0);
         build(j, 1, 1);
         cta_sync_tc();
-        if (tid == 0) issue(0, 64, dsrc, j > 0);
-        finish();
-        if (tid == 0) issue(128, 128 + 64, ddst, j > 0);
-        finish();
-        cta_sync_tc();
+        if (tid == 0) {
+          issue(0, 64, dsrc, j > 0);
+          issue(128, 128 + 64, ddst, j > 0, 1);
+        }
+        wait_mma(2);
       }
     }
     A4_MARK(10);
@@ -368,10 +372,11 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
     cta_sync_tc();
     A4_MARK(11);
     // ---- D_ZR = Ag [W_z W_r] + s [U_z U_r] ----
-    if (tid == 0) issue(0, half, dz, false);
-    finish();
-    if (tid == 0) issue(w.Nm / 2, half + w.Nm / 2, dz, true);
-    finish();
+    if (tid == 0) {
+      issue(0, half, dz, false);
+      issue(w.Nm / 2, half + w.Nm / 2, dz, true, 1);
+    }
+    wait_mma(2);
     A4_MARK(12);
     // ---- z (registers), A3 = r * s over A2's s half ----
     float zk[16];
@@ -399,10 +404,11 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
     cta_sync_tc();
     A4_MARK(13);
     // ---- D_H = Ag W_h + (r * s) U_h ----
-    if (tid == 0) issue(0, half, dz, false);
-    finish();
-    if (tid == 0) issue(w.Nm / 2, half + w.Nm / 2, dz, true);
-    finish();
+    if (tid == 0) {
+      issue(0, half, dz, false);
+      issue(w.Nm / 2, half + w.Nm / 2, dz, true, 1);
+    }
+    wait_mma(2);
     if (mine) {
       const int j = cg;
       float a[8], b[8];
