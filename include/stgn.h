@@ -316,6 +316,24 @@ int stgn_engine_info(stgn_engine* eng, int64_t* info, int n);
 int stgn_engine_snapshot(stgn_engine* eng, int64_t node_count, double t_now,
                          float* layers_out_dev, void* stream);
 
+/* Node-id-range sharding (multi-GPU, paper_2603_21090_b200/shard.py). The engine
+ * keeps and recomputes the frozen payload rows of nodes [lo, hi) only (hi <= lo:
+ * every node; ring_pay / ring_tb / ring_feat may then be bound with a base
+ * offset so that only rows lo..hi-1 are backed); the topology is replicated.
+ * A sharded batch runs in two phases: phase 1 (inputs staged, everything up to
+ * the recompute), the exchange of the direct nodes' prediction rows
+ * (stgn_engine_dpred_export on every rank, stgn_engine_dpred_import of the
+ * others' rows), then phase 2 (scores, memory commit, drift, rebuild). */
+int stgn_engine_set_ownership(stgn_engine* eng, int32_t lo, int32_t hi);
+int stgn_engine_batch_phase(stgn_engine* eng, int32_t phase, int32_t B, const int32_t* src_dev,
+                            const int32_t* dst_dev, const double* t_dev, const float* feat_dev,
+                            int64_t m0, int64_t batch_index, int64_t node_count,
+                            double* preds_dev, stgn_report* rep, void* stream);
+int stgn_engine_dpred_export(stgn_engine* eng, int32_t* nodes_dev, float* rows_dev,
+                             int64_t* count, void* stream);
+int stgn_engine_dpred_import(stgn_engine* eng, const int32_t* nodes_dev, const float* rows_dev,
+                             int64_t n, void* stream);
+
 /* Per-batch result block (counters of the last enqueued batch), for pipelined
  * callers that do not block on a report: stgn_engine_result_copy copies it
  * (stream-ordered) to device memory (to_device != 0) or pinned host memory;

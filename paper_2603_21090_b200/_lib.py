@@ -30,6 +30,8 @@ EXPORTS = (
     "stgn_debug_a4_prof", "stgn_engine_set_scope", "stgn_read_stream",
     "stgn_engine_set_skip_recompute", "stgn_engine_delta_events", "stgn_batch_result_bytes",
     "stgn_engine_result_copy", "stgn_report_from_result", "stgn_engine_snapshot",
+    "stgn_engine_set_ownership", "stgn_engine_batch_phase", "stgn_engine_dpred_export",
+    "stgn_engine_dpred_import",
 )
 
 
@@ -115,6 +117,10 @@ def lib():
     L.stgn_engine_rebuild.argtypes = [vp, vp, i64, i64, dbl, P(i64), vp]
     L.stgn_engine_full_reference.argtypes = [vp, i64, vp, vp]
     L.stgn_engine_snapshot.argtypes = [vp, i64, dbl, vp, vp]
+    L.stgn_engine_set_ownership.argtypes = [vp, i32, i32]
+    L.stgn_engine_batch_phase.argtypes = [vp, i32, i32, vp, vp, vp, vp, i64, i64, i64, vp, vp, vp]
+    L.stgn_engine_dpred_export.argtypes = [vp, vp, vp, vp, vp]
+    L.stgn_engine_dpred_import.argtypes = [vp, vp, vp, i64, vp]
     L.stgn_engine_affected.argtypes = [vp, vp, vp, i64, P(i64), P(i64), vp, vp]
     L.stgn_engine_pred_embeddings.argtypes = [vp, vp, i64, vp]
     L.stgn_pipeline_many.argtypes = [P(Dims), i64, i64] + [vp] * 18

@@ -484,7 +484,11 @@ static void launch_drift(const stgn_engine* e, cudaStream_t st, cudaGraphConditi
 
 // The whole per-batch sequence; every size is read on the device. With
 // profiling on, an event is recorded after every stage (no graph).
-static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalHandle cond) {
+// part 0: the whole batch. Sharded engines (shard.py) run it eagerly in two
+// parts around the exchange of the direct nodes' prediction rows: part 1 up to
+// and including the recompute, part 2 from the scores on (no graph, no fork).
+static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalHandle cond,
+                          int part = 0) {
   const Geo& g = e->g;
   const StateView& v = e->sv;
   const Scratch& s = e->sc;
@@ -496,10 +500,12 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   int n = 0;  // kernel launches
   int stage = 0;
   auto mark = [&]() {
-    if (e->profiling) cudaEventRecord(e->ev[stage], st);
+    if (e->profiling && part == 0) cudaEventRecord(e->ev[stage], st);
     ++stage;
   };
   mark();
+  cudaStream_t dst_ = st;  // drift branch (graph mode)
+  if (part != 2) {
   if (e->cfg.scope == STGN_SCOPE_DELTA && g.K == 1 && v.attn_logz)
     cudaMemsetAsync(&v.ctl->reserved[0], 0, sizeof(int64_t), st);  // this batch's bound records
   // ingest: direct set, per-node record order, ring insert with payload freeze, store append
@@ -555,7 +561,6 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   // Branch 1 (graph mode): the drift estimators and the rebuild decision read
   // the change records only, so they overlap the recompute; joined before the
   // (conditional) rebuild block.
-  cudaStream_t dst_ = st;
   if (fork && !e->profiling) {
     cudaEventRecord(e->ev_fork[1], st);
     cudaStreamWaitEvent(e->side[1], e->ev_fork[1], 0);
@@ -593,6 +598,11 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
     n += 1;
   }
   mark();
+  }  // part 1
+  if (part == 1) {
+    e->launches = n;
+    return;
+  }
   chain_launch(k_predict_commit, g_warp, T, 0, st, g, v, s, e->w.wpred, e->w.bpred);
   n += 1;
   mark();
@@ -893,6 +903,113 @@ extern "C" int stgn_engine_process_batch_dev(stgn_engine* e, int32_t B, const in
     CUDA_TRY(cudaStreamSynchronize(st));
     fill_report(*e->h_res, nullptr, rep);
   }
+  return STGN_OK;
+}
+
+// ---- node-id-range sharding (paper_2603_21090_b200/shard.py) ----
+extern "C" int stgn_engine_set_ownership(stgn_engine* e, int32_t lo, int32_t hi) {
+  if (!e || lo < 0 || (hi > 0 && hi < lo)) return STGN_ERR_INVALID;
+  e->g.own_lo = lo;
+  e->g.own_hi = hi;
+  drop_graph(e);
+  return STGN_OK;
+}
+
+// One batch in two eager parts around the prediction-row exchange: phase 1
+// stages the inputs and runs everything through the recompute; phase 2 the
+// scores, the memory commit, drift and rebuild (and returns the report).
+extern "C" int stgn_engine_batch_phase(stgn_engine* e, int32_t phase, int32_t B,
+                                       const int32_t* src_dev, const int32_t* dst_dev,
+                                       const double* t_dev, const float* feat_dev, int64_t m0,
+                                       int64_t batch_index, int64_t node_count, double* preds_dev,
+                                       stgn_report* rep, void* stream) {
+  if (!e || (phase != 1 && phase != 2)) return STGN_ERR_INVALID;
+  int rc = check_batch(e, B, m0, batch_index, node_count);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Scratch& s = e->sc;
+  if (phase == 1) {
+    BatchHdr hdr;
+    fill_hdr(e, &hdr, B, 0.0, m0, batch_index, node_count);
+    k_set_hdr<<<1, 1, 0, st>>>(s.hdr, hdr);
+    CUDA_TRY(cudaMemcpyAsync(s.in_src, src_dev, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(s.in_dst, dst_dev, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(s.in_t, t_dev, sizeof(double) * B, cudaMemcpyDeviceToDevice, st));
+    if (e->g.d_e > 0 && feat_dev)
+      k_pack_feat<<<(int)std::min<int64_t>(cdiv((int64_t)B * e->g.d_e, 256), 1024), 256, 0, st>>>(
+          feat_dev, s.in_feat, B, e->g.d_e, e->g.ld_e);
+    else if (e->g.d_e > 0)
+      CUDA_TRY(cudaMemsetAsync(s.in_feat, 0, sizeof(float) * (size_t)B * e->g.ld_e, st));
+    enqueue_batch(e, st, 0, 1);
+    CUDA_TRY(cudaGetLastError());
+    return STGN_OK;
+  }
+  enqueue_batch(e, st, 0, 2);
+  CUDA_TRY(cudaGetLastError());
+  if (preds_dev)
+    CUDA_TRY(cudaMemcpyAsync(preds_dev, s.preds, sizeof(double) * B, cudaMemcpyDeviceToDevice, st));
+  if (rep) {
+    CUDA_TRY(cudaMemcpyAsync(e->h_res, s.res, sizeof(BatchRes), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    fill_report(*e->h_res, nullptr, rep);
+  }
+  return STGN_OK;
+}
+
+__global__ void k_dpred_export(Geo g, Scratch s, int32_t* nodes, float* rows, int* count) {
+  const int nD = s.res->nD;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t d = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; d < nD; d += warps) {
+    const int v = s.alist[d];
+    if (!geo_owns(g, v)) continue;
+    int pos = 0;
+    if (lane == 0) pos = atomicAdd(count, 1);
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (lane == 0) nodes[pos] = v;
+    for (int j = lane; j < g.ld_d; j += 32) rows[(int64_t)pos * g.ld_d + j] = s.dpred[d * g.ld_d + j];
+  }
+}
+
+__global__ void k_dpred_import(Geo g, Scratch s, const int32_t* nodes, const float* rows, int n) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+    const int v = nodes[i];
+    if (geo_owns(g, v)) continue;  // computed here
+    const int64_t d = s.dmap[v];
+    for (int j = lane; j < g.ld_d; j += 32) s.dpred[d * g.ld_d + j] = rows[i * g.ld_d + j];
+  }
+}
+
+// The batch's prediction rows (final layer, pre-batch memory) of the direct
+// nodes this engine owns: node ids and [ld_d] rows into caller device buffers
+// of capacity 2*max_batch; *count on the host (synchronises the stream).
+extern "C" int stgn_engine_dpred_export(stgn_engine* e, int32_t* nodes_dev, float* rows_dev,
+                                        int64_t* count, void* stream) {
+  if (!e || !e->bound || !nodes_dev || !rows_dev || !count) return STGN_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  int* dcount = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&dcount, sizeof(int), st));
+  CUDA_TRY(cudaMemsetAsync(dcount, 0, sizeof(int), st));
+  k_dpred_export<<<4 * e->num_sms, 256, 0, st>>>(e->g, e->sc, nodes_dev, rows_dev, dcount);
+  int h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h, dcount, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaFreeAsync(dcount, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *count = h;
+  return STGN_OK;
+}
+
+// The other owners' rows (node ids + [ld_d] rows, device) into this batch's
+// prediction rows, before phase 2.
+extern "C" int stgn_engine_dpred_import(stgn_engine* e, const int32_t* nodes_dev,
+                                        const float* rows_dev, int64_t n, void* stream) {
+  if (!e || !e->bound) return STGN_ERR_INVALID;
+  if (n <= 0) return STGN_OK;
+  k_dpred_import<<<4 * e->num_sms, 256, 0, (cudaStream_t)stream>>>(e->g, e->sc, nodes_dev,
+                                                                     rows_dev, (int)n);
+  CUDA_TRY(cudaGetLastError());
   return STGN_OK;
 }
 

@@ -157,9 +157,11 @@ class _Tables:
         self.ring_nbr = z(N, g.L, dt=torch.int32)
         self.ring_eid = z(N, g.L, dt=torch.int64)
         self.ring_t = z(N, g.L, dt=torch.float64)
-        self.ring_pay = z(N, g.K, g.L, g.ld_d)
-        self.ring_feat = z(N, g.L, g.ld_e)
-        self.ring_tb = z(N, g.L, g.ld_t)
+        # frozen payload rows: every node, or only the shard's (bound with a base offset)
+        NP = N if g.shard is None else g.shard[1] - g.shard[0]
+        self.ring_pay = z(NP, g.K, g.L, g.ld_d)
+        self.ring_feat = z(NP, g.L, g.ld_e)
+        self.ring_tb = z(NP, g.L, g.ld_t)
         self.drift_acc = z(N, dt=torch.float64)
         self.drift_touched = z(N, dt=torch.int64)
         self.attn_ver = z(N, dt=torch.int64, fill=-1)
@@ -176,6 +178,9 @@ class _Tables:
         self.adj_head = z(N, dt=torch.int64, fill=-1)
         self.adj_deg = z(N, dt=torch.int64)
         for k, t in old.items():
+            if g.shard is not None and k in ("ring_pay", "ring_feat", "ring_tb"):
+                getattr(self, k).copy_(t)
+                continue
             getattr(self, k)[:n0].copy_(t[:n0])
         self.cap_nodes = N
 
@@ -236,6 +241,12 @@ class _Tables:
         s.cap_nodes, s.cap_edges, s.gpow_len = self.cap_nodes, self.cap_edges, self.gpow.numel()
         for name in _lib.STATE_PTRS + _lib.DELTA_PTRS:
             setattr(s, name, getattr(self, name).data_ptr())
+        if self.eng.shard is not None:  # payload rows of nodes lo..hi-1 only: base offset
+            lo = self.eng.shard[0]
+            for name in ("ring_pay", "ring_feat", "ring_tb"):
+                t = getattr(self, name)
+                row = t[0].numel() * t.element_size()
+                setattr(s, name, t.data_ptr() - lo * row)
         s.ev_cap = self.ev_cap
         s.e_pay = self.e_pay.data_ptr() if self.e_pay is not None else None
         return s
@@ -458,9 +469,20 @@ class IncrementalEngine:
 
     def __init__(self, cfg: RunConfig, params: ModelParameters, *, recompute: str = "affected",
                  max_batch: int | None = None, device: int | None = None,
-                 tensor_cores: bool | str = True, edge_payloads: bool = False):
+                 tensor_cores: bool | str = True, edge_payloads: bool = False,
+                 shard: tuple | None = None):
         cfg.validate()
         self.edge_payloads = bool(edge_payloads)  # keep every entry's payload (snapshots)
+        # node-id range [lo, hi) whose payload rows this engine keeps and recomputes
+        # (shard.py); None = every node
+        self.shard = None
+        if shard is not None:
+            lo, hi = int(shard[0]), int(shard[1])
+            if cfg.nodes <= 0 or not 0 <= lo < hi <= cfg.nodes:
+                raise ConfigError("shard=(lo, hi) needs 0 <= lo < hi <= cfg.nodes")
+            if edge_payloads:
+                raise ConfigError("the payload log is single-engine only")
+            self.shard = (lo, hi)
         if cfg.mode == "delta":
             if recompute not in ("affected", "delta"):
                 raise ConfigError("delta mode recomputes by its own classification")
@@ -536,6 +558,8 @@ class IncrementalEngine:
         self._handle = h
         if getattr(self, "_state_only", False):
             self._L.stgn_engine_set_skip_recompute(h, 1)
+        if self.shard is not None:
+            _lib.check(self._L.stgn_engine_set_ownership(self._handle, *self.shard), "ownership")
 
     def _upload_weights(self):
         torch = self._torch
@@ -703,6 +727,9 @@ class IncrementalEngine:
 
     def _grow(self, need_nodes=0, need_edges=0, need_batch=0, need_gpow=0):
         tab = self._tab
+        if self.shard is not None and need_nodes > self.cfg.nodes:
+            raise ValueError(f"node id {need_nodes - 1} outside the sharded id range "
+                             f"[0, {self.cfg.nodes})")
         rebuild_handle = need_batch > self._max_batch
         if rebuild_handle:
             self._max_batch = max(need_batch, 2 * self._max_batch)
@@ -792,6 +819,99 @@ class IncrementalEngine:
             _lib.check(rc, "process_batch")
         self._after_batch(B, float(t[-1]), top)
         return self._preds[:B].copy()
+
+    # -- sharded batches (shard.py): two device phases around the exchange --------
+    @property
+    def stack_width(self) -> int:
+        """Floats per node stack row [s (ld_s) | h_0 .. h_{K-2} (ld_d each)]."""
+        return self.ld_s + (self.K - 1) * self.ld_d
+
+    def gather_stacks(self, idx):
+        """Pre-batch stacks of node ids `idx` (device int64 tensor): [n, stack_width]."""
+        tab, torch = self._tab, self._torch
+        parts = [tab.mem[idx]]
+        if self.K > 1:
+            parts.append(tab.h[idx, :self.K - 1].reshape(idx.shape[0], -1))
+        return torch.cat(parts, 1).contiguous()
+
+    def scatter_stacks(self, idx, rows):
+        """Write stacks (from gather_stacks on their owner) into rows `idx`."""
+        tab = self._tab
+        tab.mem[idx] = rows[:, :self.ld_s]
+        if self.K > 1:
+            tab.h[idx, :self.K - 1] = rows[:, self.ld_s:].reshape(idx.shape[0], self.K - 1,
+                                                                   self.ld_d)
+
+    def batch_phase1(self, src, dst, t, feat=None):
+        """Stage one batch and run it through the recompute (stgn_engine_batch_phase 1)."""
+        torch = self._torch
+        self.counters.start_batch()
+        self._affected_cache = None
+        self._pred_cache = None
+        src = np.ascontiguousarray(src, dtype=np.int64)
+        dst = np.ascontiguousarray(dst, dtype=np.int64)
+        t = np.ascontiguousarray(t, dtype=np.float64)
+        B = int(src.shape[0])
+        if B == 0 or dst.shape[0] != B or t.shape[0] != B:
+            raise ValueError("a sharded batch needs B >= 1 edges with matching src/dst/t")
+        if (src < 0).any() or (dst < 0).any():
+            raise ValueError("node ids must be non-negative")
+        prev = np.concatenate([[self._t_now], t[:-1]])
+        if (t < prev).any():
+            j = int(np.nonzero(t < prev)[0][0])
+            raise MonotonicityError(f"batch edge at t={t[j]} precedes committed history t={prev[j]}")
+        top = int(max(src.max(), dst.max())) + 1
+        self._grow(need_nodes=max(self._n_mem, top, self.cfg.nodes, self._store_n),
+                   need_edges=self._m + B, need_batch=B, need_gpow=self.batch_index + 3)
+        self._n_mem = max(self._n_mem, top)
+        self.batch_index += 1
+        dev = self.device
+        self._ph = dict(
+            B=B, top=top, t_last=float(t[-1]),
+            src=torch.from_numpy(src.astype(np.int32)).to(dev),
+            dst=torch.from_numpy(dst.astype(np.int32)).to(dev),
+            t=torch.from_numpy(t).to(dev),
+            feat=(torch.from_numpy(np.ascontiguousarray(feat, dtype=np.float32)).to(dev)
+                  if (feat is not None and self.dims.d_e) else None))
+        ph = self._ph
+        rc = self._L.stgn_engine_batch_phase(
+            self._handle, 1, B, ph["src"].data_ptr(), ph["dst"].data_ptr(), ph["t"].data_ptr(),
+            ph["feat"].data_ptr() if ph["feat"] is not None else None, self._m, self.batch_index,
+            self.node_count, None, None, self._stream())
+        if rc:
+            self.batch_index -= 1
+            _lib.check(rc, "batch_phase(1)")
+
+    def dpred_export(self):
+        """(node ids int32, [n, ld_d] rows) of this engine's owned direct nodes."""
+        torch = self._torch
+        cap = 2 * self._max_batch
+        nodes = torch.empty(cap, dtype=torch.int32, device=self.device)
+        rows = torch.empty((cap, self.ld_d), dtype=torch.float32, device=self.device)
+        cnt = C.c_int64()
+        _lib.check(self._L.stgn_engine_dpred_export(self._handle, nodes.data_ptr(), rows.data_ptr(),
+                                                    C.byref(cnt), self._stream()), "dpred_export")
+        n = int(cnt.value)
+        return nodes[:n], rows[:n]
+
+    def dpred_import(self, gathered):
+        nodes, rows = gathered
+        nodes = nodes.to(self.device, dtype=self._torch.int32).contiguous()
+        rows = rows.to(self.device, dtype=self._torch.float32).contiguous()
+        _lib.check(self._L.stgn_engine_dpred_import(self._handle, nodes.data_ptr(), rows.data_ptr(),
+                                                    int(nodes.shape[0]), self._stream()),
+                   "dpred_import")
+
+    def batch_phase2(self) -> np.ndarray:
+        """Scores, memory commit, drift and rebuild; returns the batch's scores."""
+        ph = self._ph
+        preds = self._torch.empty(ph["B"], dtype=self._torch.float64, device=self.device)
+        _lib.check(self._L.stgn_engine_batch_phase(
+            self._handle, 2, ph["B"], None, None, None, None, self._m, self.batch_index,
+            self.node_count, preds.data_ptr(), C.byref(self._rep), self._stream()), "batch_phase(2)")
+        self._after_batch(ph["B"], ph["t_last"], ph["top"])
+        self._ph = None
+        return preds.cpu().numpy()
 
     def process_batch_device(self, src, dst, t, feat=None, *, max_id: int, t_last: float,
                              t_first: float, report: bool = False):
