@@ -2,6 +2,7 @@
 // as a CUDA graph), rebuild / full_reference entry points and the
 // operator-level pipeline_many. See include/stgn.h for the contract.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -367,7 +368,10 @@ int stgn_engine_set_weights(stgn_engine* e, const stgn_weights* w) {
 #ifdef STGN_NO_MEM4  // experiments: the FFMA memory update
   e->use_m4 = false;
 #else
-  e->use_m4 = e->m4_ok && w->t4mem;
+  {
+    const char* env = getenv("STGN_MEM4");  // "0": the FFMA memory update
+    e->use_m4 = e->m4_ok && w->t4mem && !(env && env[0] == '0');
+  }
 #endif
   if (e->use_m4) e->m4w.wblk = w->t4mem;
   e->aw.wq = w->wq;

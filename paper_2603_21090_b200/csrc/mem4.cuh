@@ -286,12 +286,11 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
       A4_MARK(9);
       for (int j = 0; j < w.nmsg; ++j) {
         const int ab = (j & 1) ? 128 : 0;
-        if (tid == 0) {  // both weight sides (two staged buffers) back to back
-          issue(ab, ab + 64, dsrc, j > 0);
-          issue(ab, ab + 64, ddst, j > 0, 1);
-        }
-        if (j + 1 < w.nmsg) build(j + 1, (j + 1) & 1, -1);  // the other buffer, beside the MMAs
-        wait_mma(2);
+        if (tid == 0) issue(ab, ab + 64, dsrc, j > 0);
+        if (j + 1 < w.nmsg) build(j + 1, (j + 1) & 1, -1);  // the other buffer, beside the MMA
+        wait_mma(1);
+        if (tid == 0) issue(ab, ab + 64, ddst, j > 0);
+        wait_mma(1);
       }
     } else {  // per-side sums: A0 = src side, A1 = dst side
       A4_MARK(9);
@@ -299,11 +298,10 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
         build(j, 0, 0);
         build(j, 1, 1);
         cta_sync_tc();
-        if (tid == 0) {
-          issue(0, 64, dsrc, j > 0);
-          issue(128, 128 + 64, ddst, j > 0, 1);
-        }
-        wait_mma(2);
+        if (tid == 0) issue(0, 64, dsrc, j > 0);
+        wait_mma(1);
+        if (tid == 0) issue(128, 128 + 64, ddst, j > 0);
+        wait_mma(1);
       }
     }
     A4_MARK(10);
@@ -372,11 +370,10 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
     cta_sync_tc();
     A4_MARK(11);
     // ---- D_ZR = Ag [W_z W_r] + s [U_z U_r] ----
-    if (tid == 0) {
-      issue(0, half, dz, false);
-      issue(w.Nm / 2, half + w.Nm / 2, dz, true, 1);
-    }
-    wait_mma(2);
+    if (tid == 0) issue(0, half, dz, false);
+    wait_mma(1);
+    if (tid == 0) issue(w.Nm / 2, half + w.Nm / 2, dz, true);
+    wait_mma(1);
     A4_MARK(12);
     // ---- z (registers), A3 = r * s over A2's s half ----
     float zk[16];
@@ -404,11 +401,10 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
     cta_sync_tc();
     A4_MARK(13);
     // ---- D_H = Ag W_h + (r * s) U_h ----
-    if (tid == 0) {
-      issue(0, half, dz, false);
-      issue(w.Nm / 2, half + w.Nm / 2, dz, true, 1);
-    }
-    wait_mma(2);
+    if (tid == 0) issue(0, half, dz, false);
+    wait_mma(1);
+    if (tid == 0) issue(w.Nm / 2, half + w.Nm / 2, dz, true);
+    wait_mma(1);
     if (mine) {
       const int j = cg;
       float a[8], b[8];
