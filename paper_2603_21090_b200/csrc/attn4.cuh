@@ -1273,6 +1273,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
 #endif
       A4_MARK(3);
       cta_sync_tc();
+      A4_MARK(6);
       if (tid == 0) {  // the walk is done with the weight buffers: stage V_0, V_1
         fence_async_smem();
         stage(G);
@@ -1280,6 +1281,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
       }
       // ---- c_h = ubar_h W_V,h ----
       gemm(w.qt0, w.Nv, w.Ku, 0);
+      A4_MARK(7);
       // every thread must observe the V_0 commit phase before V_1 can complete the
       // next one (a parity wait cannot tell phase G from phase G + 2)
       cta_sync_tc();

@@ -443,6 +443,8 @@ static RingSrc ring_src(const stgn_engine* e) {
   r.ring_cnt = v.ring_cnt; r.ring_head = v.ring_head; r.ring_ccnt = v.ring_ccnt;
   r.ring_t = v.ring_t; r.ring_pay = v.ring_pay; r.ring_feat = v.ring_feat;
   r.ring_tb = v.ring_tb;
+  r.own_lo = e->g.own_lo;  // sharded engine: rows of other ranks' nodes are skipped
+  r.own_hi = e->g.own_hi;
   return r;
 }
 

@@ -235,24 +235,45 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
           const float* po = st.mem + (int64_t)s_loth[row] * g.ld_s;
           const float* pf = s.in_feat + (int64_t)s_le[row] * g.ld_e;
           const int c0 = j * M4_KC + 16 * b;  // x column of t = 0
+          // a block inside one row segment at a 4-aligned offset: four 16-byte loads
+          const float* seg = nullptr;
+          if (c0 + 16 <= g.d_s) seg = pv + c0;
+          else if (c0 >= g.d_s && c0 + 16 <= 2 * g.d_s && ((c0 - g.d_s) & 3) == 0) seg = po + (c0 - g.d_s);
+          else if (c0 >= 2 * g.d_s && c0 + 16 <= phi0 && ((c0 - 2 * g.d_s) & 3) == 0)
+            seg = pf + (c0 - 2 * g.d_s);
+          if (seg) {
 #pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            const int cs = c0 + t;
-            if (cs >= 0 && cs < phi0) {
-              const float* p = cs < g.d_s ? pv + cs : (cs < 2 * g.d_s ? po + (cs - g.d_s)
-                                                                      : pf + (cs - 2 * g.d_s));
-              x[t] = __ldg(p);
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const float4 f = __ldg(reinterpret_cast<const float4*>(seg) + q4);
+              x[4 * q4] = f.x; x[4 * q4 + 1] = f.y; x[4 * q4 + 2] = f.z; x[4 * q4 + 3] = f.w;
+            }
+          } else if (c0 < phi0) {
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              const int cs = c0 + t;
+              if (cs < phi0) {
+                const float* p = cs < g.d_s ? pv + cs : (cs < 2 * g.d_s ? po + (cs - g.d_s)
+                                                                        : pf + (cs - 2 * g.d_s));
+                x[t] = __ldg(p);
+              }
             }
           }
-          const double dt = s_ldt[row];
+          if (c0 + 16 > phi0 && c0 < g.msg_in) {  // time encoding: one sincos per frequency
+            const double dt = s_ldt[row];
 #pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            const int cs = c0 + t;
-            if (cs >= phi0 && cs < g.msg_in) {
+            for (int t = 0; t < 16; ++t) {
+              const int cs = c0 + t;
               const int p = cs - phi0;
-              float sv, cv;
-              phase_sincos(omega[p >> 1], dt, &sv, &cv);
-              x[t] = ((p & 1) ? sv : cv) * g.phi_amp;
+              if (p >= 0 && cs < g.msg_in && (t == 0 || !(p & 1))) {
+                float sv, cv;
+                phase_sincos(omega[p >> 1], dt, &sv, &cv);
+                if (p & 1) {
+                  x[t] = sv * g.phi_amp;
+                } else {
+                  x[t] = cv * g.phi_amp;
+                  if (t + 1 < 16 && cs + 1 < g.msg_in) x[t + 1] = sv * g.phi_amp;
+                }
+              }
             }
           }
         } else if (v >= 0) {

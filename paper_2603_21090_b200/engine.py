@@ -831,7 +831,7 @@ class IncrementalEngine:
         tab, torch = self._tab, self._torch
         parts = [tab.mem[idx]]
         if self.K > 1:
-            parts.append(tab.h[idx, :self.K - 1].reshape(idx.shape[0], -1))
+            parts.append(tab.h[idx, :self.K - 1].reshape(idx.shape[0], (self.K - 1) * self.ld_d))
         return torch.cat(parts, 1).contiguous()
 
     def scatter_stacks(self, idx, rows):

@@ -37,8 +37,12 @@ a = np.array(buf[:n], dtype=np.uint64)
 t = (a >> 4).astype(np.int64)
 tag = (a & 15).astype(np.int64)
 print("marks", n, "rows", eng._rep.affected, "span_us", (t[-1] - t[0]) / 1e3 if n else 0)
-names = {0: "Q+q", 1: "K0/K1", 2: "walk", 3: "V+c", 4: "O+out", 5: "->next"}
+names = {0: "Q+q", 1: "K0/K1", 2: "walk (thread 0)", 3: "walk tail (CTA barrier)",
+         6: "V weights staged + V_0", 7: "V_1 + c", 4: "O+out", 5: "->next"}
 acc = {}
+keep = tag < 8  # attn4 marks only (mem4 uses 8..15)
+t, tag = t[keep], tag[keep]
+n = len(t)
 for i in range(n - 1):
     acc.setdefault(int(tag[i]), []).append((t[i + 1] - t[i]) / 1e3)
 tot = sum(sum(v) for v in acc.values())
