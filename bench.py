@@ -575,7 +575,7 @@ def run_ours(args, world, rank, local_rank):
         "fallback (B200_PROFILING.md)"
     info = eng.info()
     traffic = None  # DRAM bytes per launch of the same kernel from the committed ncu capture
-    tr_path = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    tr_path = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
     if os.path.exists(tr_path) and info.get("bf16x3"):
         with open(tr_path) as fh:
             traffic = json.load(fh).get("traffic_bytes_per_launch")
@@ -688,7 +688,7 @@ def run_ours(args, world, rank, local_rank):
                     "sync_call_p99_ms": float(np.percentile(e2e_lat, 99) * 1e3)},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak,
                          "unit": "GB/s", "frac": achieved_gbs / hbm_peak, "traffic": traffic,
-                         "traffic_source": "profiles/r01_ncu_traffic.json (ncu --set full)",
+                         "traffic_source": "profiles/r02_ncu_traffic.json (ncu --set full)",
                          "kernel": kname + ": recompute of A (pre-batch memory) + V_direct "
                                            "(post-batch memory), one launch",
                          "avg_launch_ms": a_ms, "algorithmic_bytes": float(np.mean(attn_bytes)),

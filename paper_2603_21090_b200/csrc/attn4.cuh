@@ -91,6 +91,9 @@ __device__ int g_a4_prof_n;
 #ifndef A4_EVQ
 #define A4_EVQ 1  // quadrant fill/pack duties as an event loop (see the walk phase)
 #endif
+#ifndef A4_NXH
+#define A4_NXH 1  // the next tile's row headers loaded during this tile's first walk (warp A4_WARPS-1)
+#endif
 #ifndef A4_LPT
 #define A4_LPT 0  // rows of a tile sorted by descending entry count (see the tile header)
 #endif
@@ -885,6 +888,10 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
   float* Ub0 = reinterpret_cast<float*>(sbase + (size_t)w.region_bytes);
   float* Ub1 = A4_NUB > 1 ? Ub0 + 32 * w.ldu : Ub0;
   __shared__ int s_node[A4_TMAX], s_E[A4_TMAX], s_head[A4_TMAX], s_mode[A4_TMAX];
+#if A4_NXH
+  __shared__ int nx_node[A4_TMAX], nx_E[A4_TMAX], nx_head[A4_TMAX], nx_mode[A4_TMAX];
+  __shared__ double nx_tref[A4_TMAX];
+#endif
 #if A4_LPT
   __shared__ int s_idx[A4_TMAX], t_node[A4_TMAX], t_E[A4_TMAX], t_head[A4_TMAX], t_mode[A4_TMAX];
   __shared__ double t_tref[A4_TMAX];
@@ -974,21 +981,34 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
     tc_fence_after();
   };
 
+  // row i of tile `tl`: node (-1 if none / another rank's), ring entry count, head, t_ref, mode
+  auto row_header = [&](int64_t tl, int i, int& node, int& E, int& head, int& mode, double& tref) {
+    const int64_t idx = tl * T + i;
+    node = -1; E = 0; head = 0; mode = 0; tref = 0.0;
+    if (i < T && idx < N) {
+      node = rs.node(idx);
+      if (rs.fused) mode = idx >= pre_rows ? 2 : (idx < d_rows ? 1 : 0);
+      const int cc = node >= 0 ? rs.ring_ccnt[node] : 0;
+      E = node < 0 ? 0 : (cc >= 0 ? cc : (rs.use_store ? rs.ring_cnt[node] : 0));
+      head = node >= 0 ? rs.ring_head[node] : 0;
+      if (E > 0) tref = rs.ring_t[(int64_t)node * g.L + head];
+    }
+  };
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += grid) {
     const int64_t base = tile * T;
     if (tid < A4_TMAX) {
       const int i = tid;
-      const int64_t idx = base + i;
-      int node = -1, E = 0, head = 0, mode = 0;
-      double tref = 0.0;
-      if (i < T && idx < N) {
-        node = rs.node(idx);
-        if (rs.fused) mode = idx >= pre_rows ? 2 : (idx < d_rows ? 1 : 0);
-        const int cc = node >= 0 ? rs.ring_ccnt[node] : 0;
-        E = node < 0 ? 0 : (cc >= 0 ? cc : (rs.use_store ? rs.ring_cnt[node] : 0));
-        head = node >= 0 ? rs.ring_head[node] : 0;
-        if (E > 0) tref = rs.ring_t[(int64_t)node * g.L + head];
+      int node, E, head, mode;
+      double tref;
+#if A4_NXH
+      if (tile != blockIdx.x) {  // loaded during the previous tile's first walk
+        node = nx_node[i]; E = nx_E[i]; head = nx_head[i]; mode = nx_mode[i]; tref = nx_tref[i];
+      } else {
+        row_header(tile, i, node, E, head, mode, tref);
       }
+#else
+      row_header(tile, i, node, E, head, mode, tref);
+#endif
 #if A4_LPT
       t_node[i] = node; t_E[i] = E; t_head[i] = head; t_tref[i] = tref; t_mode[i] = mode;
 #else
@@ -1101,6 +1121,23 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
         // ---- q~_h = (W_K,h / sqrt(d_k)) q_h -> QT_h ----
         gemm(0, w.Nk, w.Kq, h == 0 ? w.qt0 : w.qt1);
       }
+#if A4_NXH
+      // the next tile's row headers (dependent global loads) and an L2 prefetch of its
+      // query rows, by the last warp before it joins this tile's first walk
+      if (l == 0 && warp == A4_WARPS - 1 && tile + grid < ntiles) {
+        for (int i = lane; i < A4_TMAX; i += 32) {
+          int node, E, head, mode;
+          double tref;
+          row_header(tile + grid, i, node, E, head, mode, tref);
+          nx_node[i] = node; nx_E[i] = E; nx_head[i] = head; nx_mode[i] = mode; nx_tref[i] = tref;
+          if (node >= 0) {
+            const float* xr = mode == 2 ? rs.mem_post + ((tile + grid) * T + i - pre_rows) * g.ld_s
+                                        : rs.mem + (int64_t)node * g.ld_s;
+            bulk_prefetch_l2(xr, (uint32_t)(g.ld_s * 4));
+          }
+        }
+      }
+#endif
       // ---- walk, one 32-row quadrant at a time ----
       A4_MARK(2);
       fence_async_smem();
