@@ -382,6 +382,70 @@ def config_legs(args, torch, dev):
     return out
 
 
+def operator_leg(torch, dev, N=10_000, E_per=10, reps=20):
+    """The operator-level drop-in (kernels.pipeline_many, S/kernels/__init__.py:42-44) at the
+    C4 widths (K = 2, d = 100, d_e = 0, H = 2, d_k = 50): node-pipelines/s through the C ABI
+    with device-resident inputs (CUDA events around `reps` calls) and through the numpy API
+    (host arrays in and out, host clock). BASELINE.md §2 measured the reference's numba kernel
+    at 1,735 node-pipelines/s (K = 2, d_e = 0, L = 10)."""
+    import ctypes as C
+    from paper_2603_21090_b200 import _lib, kernels
+    from paper_2603_21090_b200.config import Dims
+    from paper_2603_21090_b200.params import init_params
+    dims = Dims(d_s=100, d_e=0, d_t=100, d_x=0, d_m=100, d_k=50, heads=2, layers=2)
+    p = init_params(0, dims)
+    rng = np.random.default_rng(0)
+    E = N * E_per
+    qbase = rng.standard_normal((N, 100))
+    offsets = np.arange(0, E + 1, E_per, dtype=np.int64)
+    payload = rng.standard_normal((E, 2, 100))
+    feat = np.zeros((E, 0))
+    dt = rng.uniform(0, 1e4, E)
+    phi0 = np.empty(100)
+    phi0[0::2], phi0[1::2] = 1.0, 0.0
+    phi0 *= np.sqrt(1.0 / 100)
+    kernels.pipeline_many(qbase[:8], offsets[:9], payload[:80], feat[:80], dt[:80], p.omega, phi0,
+                          p.w_q, p.w_k, p.w_v, p.w_o)  # warm-up
+    t0 = time.perf_counter()
+    for _ in range(3):
+        kernels.pipeline_many(qbase, offsets, payload, feat, dt, p.omega, phi0, p.w_q, p.w_k,
+                              p.w_v, p.w_o)
+    host_s = (time.perf_counter() - t0) / 3
+    f32 = lambda a: torch.tensor(np.ascontiguousarray(a, dtype=np.float32), device=dev)  # noqa: E731
+    t = dict(q=f32(qbase), off=torch.tensor(offsets, device=dev), pay=f32(payload),
+             feat=f32(np.zeros((E, 1))), dt=torch.tensor(dt, device=dev),
+             om=torch.tensor(p.omega, device=dev), phi0=f32(phi0), wq=f32(p.w_q), wk=f32(p.w_k),
+             wv=f32(p.w_v), wo=f32(p.w_o))
+    outs = [torch.zeros(sh, dtype=torch.float32, device=dev) for sh in
+            ((N, 2, 100), (E, 2, 2), (E, 2, 2, 50), (N, 2, 2), (N, 2, 2), (N, 2, 2, 50))]
+    ds = _lib.dims_struct(dims)
+    L = _lib.lib()
+    stream = torch.cuda.current_stream(dev)
+    ptr = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+
+    def call():
+        _lib.check(L.stgn_pipeline_many(
+            C.byref(ds), N, E, ptr(t["q"]), ptr(t["off"]), ptr(t["pay"]), ptr(t["feat"]),
+            ptr(t["dt"]), ptr(t["om"]), ptr(t["phi0"]), ptr(t["wq"]), ptr(t["wk"]), ptr(t["wv"]),
+            ptr(t["wo"]), *[ptr(o) for o in outs], C.c_void_p(stream.cuda_stream)), "pipeline_many")
+    call()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    for _ in range(reps):
+        call()
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    dev_ms = ev[0].elapsed_time(ev[1]) / reps
+    return {"nodes": N, "entries_per_node": E_per, "widths": "K=2, d=100, d_e=0, H=2, d_k=50",
+            "device_ms_per_call": dev_ms, "node_pipelines_per_s": N / (dev_ms / 1e3),
+            "numpy_api_ms_per_call": host_s * 1e3, "numpy_api_node_pipelines_per_s": N / host_s,
+            "cpu_reference_node_pipelines_per_s": 1735,
+            "note": "stgn_pipeline_many returns every per-entry intermediate of the reference "
+                    "operator (scores, values, maxlog, zsum, qvecs): FFMA kernel with per-entry "
+                    "K/V projections"}
+
+
 def _timed_batches(torch, stream, feed, k0, K):
     """Feed batches k0..k0+K-1 of a DeviceStream, one CUDA event after each;
     returns (total ms, per-batch ms)."""
@@ -664,6 +728,7 @@ def run_ours(args, world, rank, local_rank):
 
     # 5) the other configs of BASELINE.json (C1, C2 full streams; C3 TGAT at the C4 scale)
     cfg_legs = config_legs(args, torch, dev) if (args.config_legs and rank == 0) else None
+    op_leg = operator_leg(torch, dev) if (args.config_legs and rank == 0) else None
 
     line = None
     if rank == 0:
@@ -705,6 +770,7 @@ def run_ours(args, world, rank, local_rank):
             "latency": lat,
             "sweep": sweep_out,
             "configs": cfg_legs,
+            "operator_pipeline_many": op_leg,
             "full_rebuild": rb,
             # the paper's "index refresh" comparison: one full recompute of
             # every node (the TGL-style / OracleEngine baseline) vs one incremental batch
