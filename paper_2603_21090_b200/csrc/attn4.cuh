@@ -91,6 +91,9 @@ __device__ int g_a4_prof_n;
 #ifndef A4_EVQ
 #define A4_EVQ 1  // quadrant fill/pack duties as an event loop (see the walk phase)
 #endif
+#ifndef A4_RUNPTR
+#define A4_RUNPTR 1  // walk 1: running source pointers for the cp.async issue
+#endif
 #ifndef A4_NXH
 #define A4_NXH 1  // the next tile's row headers loaded during this tile's first walk (warp A4_WARPS-1)
 #endif
@@ -486,6 +489,15 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
 #endif
   const int nch = (E + EC - 1) / EC;
   int iss_slot = 0, con_slot = 0;  // stage slots of the next issue / the next consumed chunk
+#if A4_RUNPTR
+  // running per-lane source rows of the next entry to issue (chunks are issued in
+  // order): one pointer bump per entry instead of slot arithmetic and 64-bit
+  // multiplies per copy; the ring wraps once at most
+  int r_slot = hd;
+  const float* r_pay = payb + (int64_t)hd * g.ld_d;
+  const float* r_tb = tbb + (int64_t)hd * g.ld_t;
+  const float* r_ft = ftb + (int64_t)hd * g.ld_e;
+#endif
   auto issue = [&](int c) {
     if (c < nch) {
       float4* sb = stg + iss_slot * (EC * NSEG * 32) + lane;
@@ -493,6 +505,28 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
       for (int u = 0; u < EC; ++u) {
         const int e = c * EC + u;
         const bool ev = e < E;
+#if A4_RUNPTR
+        const int pay_bytes = (ev && lp) ? 16 : 0, tb_bytes = (ev && lt) ? 16 : 0;
+#if A4_HINTS
+        cp_async16_pol(sb + (u * NSEG) * 32, r_pay, pay_bytes, pol_pay);
+        if (!A4_TRIG) cp_async16_pol(sb + (u * NSEG + 1) * 32, r_tb, tb_bytes, pol_tb);
+#else
+        cp_async16(sb + (u * NSEG) * 32, r_pay, pay_bytes);
+        if (!A4_TRIG) cp_async16(sb + (u * NSEG + 1) * 32, r_tb, tb_bytes);
+#endif
+        if (KF) cp_async16(sb + (u * NSEG + 2) * 32, r_ft, (ev && lf) ? 16 : 0);
+        if (++r_slot == g.L) {
+          r_slot = 0;
+          r_pay = payb;
+          r_tb = tbb;
+          r_ft = ftb;
+        } else {
+          r_pay += g.ld_d;
+          r_tb += g.ld_t;
+          r_ft += g.ld_e;
+        }
+        continue;
+#endif
         int slot = hd + e;
         if (slot >= g.L) slot -= g.L;
         if (EC > 2 && !ev) slot = 0;  // EC = 2: hd + e < 2L, one wrap keeps it in the ring
