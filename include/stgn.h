@@ -128,6 +128,12 @@ typedef struct {
    *   1 block                    N = Ns,   K = Nm    w_h
    *   1 block                    N = Ns,   K = Ns    u_h */
   const uint16_t *t4mem;
+  /* folded output operands of the bf16x3 recompute kernel, per layer:
+   *   P_h = w_v[l,h] (time rows * sqrt(1/d_t)) @ w_o[l, h*d_k:(h+1)*d_k, :]   (k_in x d)
+   * as B operands [n = output column][k = key feature, 4-padded layout of t4k], split at
+   * output column Na = min(round_up(d,16), 64): Pa_0, Pa_1 (N = Na), Pb_0, Pb_1
+   * (N = round_up(d,16) - Na, absent when 0), K = round_up(k_in padded, 16) */
+  const uint16_t *t4p;
 } stgn_weights;
 
 /* Persistent control block (device). */

@@ -52,7 +52,7 @@ class Weights(C.Structure):
                 ("wq", "bq", "wkt", "wv", "wo", "wmsg", "bmsg", "wgru", "ugru", "bgru", "wpred",
                  "omega", "phi0")] + [("bpred", C.c_double)] + \
                [(n, C.c_void_p) for n in ("tcq", "tck", "tcv", "tco", "t4q", "t4k", "t4v", "t4o",
-                                          "t4bq", "t4mem")]
+                                          "t4bq", "t4mem", "t4p")]
 
 
 class Ctl(C.Structure):

@@ -91,6 +91,10 @@ __device__ int g_a4_prof_n;
 #ifndef A4_EVQ
 #define A4_EVQ 1  // quadrant fill/pack duties as an event loop (see the walk phase)
 #endif
+#ifndef A4_VOF
+#define A4_VOF 1  // out = sum_h ubar_h (W_V,h W_O,h): the V GEMMs, the c pack and the O GEMM fold
+                  // into two passes of two MMA blocks over the TMEM ubar operands
+#endif
 #ifndef A4_RUNPTR
 #define A4_RUNPTR 1  // walk 1: running source pointers for the cp.async issue
 #endif
@@ -114,6 +118,8 @@ __device__ int g_a4_prof_n;
 
 struct A4W {
   const uint16_t *wq, *wk, *wv, *wo;  // packed bf16 B operands, hi block then lo block
+  const uint16_t* wp;                 // folded P_h = W_V,h W_O,h (A4_VOF): [K][Pa_0 Pa_1 Pb_0 Pb_1]
+  int Npa, Npb, nbl;                  // out columns of the two P passes; weight blocks per layer
   const float* bq;                    // [K][H*Kq]
   const double* omega;
   int Kx, Kq, Ku, Kc, Nq, Nk, Nv, No;
@@ -146,7 +152,11 @@ static inline bool a4_plan(const Geo& g, A4W* w) {
   int ldu = g.H * w->kpad;
   while (ldu % 8 != 4) ++ldu;  // 8 consecutive rows hit distinct 16-byte bank groups
   w->ldu = ldu;
+  w->Npa = std::min(w->No, 64);
+  w->Npb = w->No - w->Npa;
+  w->nbl = A4_VOF ? (w->Npb > 0 ? 7 : 5) : 6;
   int mb = std::max(std::max(w->Nq * w->Kx, w->Nk * w->Kq), std::max(w->Nv * w->Ku, w->No * w->Kc));
+  mb = std::max(mb, w->Npa * w->Ku);
   w->wblk_bytes = (mb * 2 * 2 + 1023) & ~1023;
 #if A4_WALK == 2
   // two chunk stages per warp: [A4_EC2][ld_d] payload, [A4_EC2][ld_t] basis, [A4_EC2][ld_e] features
@@ -228,7 +238,8 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
 // one thread: bf16x3 MMAs of one block, A = TMEM [a, a+Kp) (hi then lo), B = smem
 // K-major bf16 [Np][Kp] (8x8 core matrices, hi block then lo block), then commit
 __device__ __forceinline__ void a4_mma(uint32_t tmem, int a, const uint16_t* Wb, int Np, int Kp,
-                                       int dcol, uint64_t* bar) {
+                                       int dcol, uint64_t* bar, bool acc0 = false,
+                                       bool commit = true) {
   tc_fence_after();
   const uint32_t idesc = umma_idesc_bf16(128, Np);
   const uint32_t sbo = (uint32_t)(Kp / 8) * 128u;
@@ -238,11 +249,11 @@ __device__ __forceinline__ void a4_mma(uint32_t tmem, int a, const uint16_t* Wb,
     const uint32_t off = (uint32_t)s * 256u;
     const uint64_t dh = umma_desc(bh + off, 128, sbo), dl = umma_desc(bl + off, 128, sbo);
     const uint32_t ah = ah0 + 8u * s, al = al0 + 8u * s;
-    umma_bf16_ts(tmem + (uint32_t)dcol, ah, dh, idesc, s > 0 ? 1u : 0u);
+    umma_bf16_ts(tmem + (uint32_t)dcol, ah, dh, idesc, (acc0 || s > 0) ? 1u : 0u);
     umma_bf16_ts(tmem + (uint32_t)dcol, ah, dl, idesc, 1u);
     umma_bf16_ts(tmem + (uint32_t)dcol, al, dh, idesc, 1u);
   }
-  umma_commit(bar);
+  if (commit) umma_commit(bar);
 }
 
 // weight block j (Q, K_0, K_1, V_0, V_1, O) of layer l: source and element count
@@ -256,12 +267,24 @@ __device__ __forceinline__ const uint16_t* a4_block(const Geo& g, const A4W& w, 
     *elems = a4_blk_elems(w.Nk, w.Kq);
     return w.wk + ((int64_t)l * 2 + (j - 1)) * *elems;
   }
+#if A4_VOF
+  // layer l: Pa_0, Pa_1 ([Npa][Ku]), then Pb_0, Pb_1 ([Npb][Ku])
+  const int64_t ea = a4_blk_elems(w.Npa, w.Ku), eb = a4_blk_elems(w.Npb, w.Ku);
+  const uint16_t* base = w.wp + (int64_t)l * 2 * (ea + eb);
+  if (j <= 4) {
+    *elems = ea;
+    return base + (int64_t)(j - 3) * ea;
+  }
+  *elems = eb;
+  return base + 2 * ea + (int64_t)(j - 5) * eb;
+#else
   if (j <= 4) {
     *elems = a4_blk_elems(w.Nv, w.Ku);
     return w.wv + ((int64_t)l * 2 + (j - 3)) * *elems;
   }
   *elems = a4_blk_elems(w.No, w.Kc);
   return w.wo + (int64_t)l * *elems;
+#endif
 }
 
 // L2 prefetch of layer l's ring rows of tile rows [r0, r1): the valid slots
@@ -949,7 +972,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
   const int64_t ntiles = cdiv(N, T);
   if ((int64_t)blockIdx.x >= ntiles) return;
   const int64_t my_tiles = cdiv(ntiles - blockIdx.x, grid);
-  const int64_t total_blocks = my_tiles * g.K * 6;
+  const int64_t total_blocks = my_tiles * g.K * w.nbl;
   const int64_t pre_rows = rs.fused ? (int64_t)rs.pre_n[0] : N;
   const int64_t d_rows = rs.fused ? (int64_t)rs.post_n[0] : 0;
 
@@ -976,7 +999,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
   const int row = 32 * quad + lane;
   auto stage = [&](int64_t G) {  // one thread
     int64_t el;
-    const uint16_t* src = a4_block(g, w, (int)((G / 6) % g.K), (int)(G % 6), &el);
+    const uint16_t* src = a4_block(g, w, (int)((G / w.nbl) % g.K), (int)(G % w.nbl), &el);
     bulk_stage((G & 1) ? (void*)Wb1 : (void*)Wb0, src, (uint32_t)(el * 2), &wbar[G & 1]);
   };
   if (tid == 0) {
@@ -993,21 +1016,40 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
   S2.bar = sbar2 + 2 * warp;
   S2.n_iss = S2.n_con = 0;
 #endif
-  auto deferred = [&](int64_t Gb) { const int j = (int)(Gb % 6); return j == 3 || j == 4; };
+  auto deferred = [&](int64_t Gb) { const int j = (int)(Gb % w.nbl); return j == 3 || j == 4; };
   int64_t G = 0;  // weight blocks consumed by this CTA
   int ub_use[2] = {0, 0};  // uses of each quadrant row buffer so far (mbarrier phases)
   // one GEMM: wait for its weights, MMA, wait for the MMA, refill the buffer.
   // Callers put a CTA barrier before every gemm: mbarrier waits are by phase
   // parity, so no thread may fall two commit phases behind.
+  uint32_t mph = 0;  // commits of the MMA barrier so far (its phase parity)
   auto gemm = [&](int a, int Np, int Kp, int dcol) {
     if (tid == 0) {  // only the issuing thread waits for the weights
       mbar_wait(&wbar[G & 1], (uint32_t)((G >> 1) & 1));
       a4_mma(tmem, a, (G & 1) ? Wb1 : Wb0, Np, Kp, dcol, &mbar);
     }
-    mbar_wait(&mbar, (uint32_t)(G & 1));
+    mbar_wait(&mbar, mph & 1u);
+    ++mph;
     tc_fence_after();
     if (tid == 0 && G + 2 < total_blocks && !deferred(G + 2)) stage(G + 2);
     ++G;
+  };
+  // two blocks (both weight buffers) accumulated into one D, one commit
+  auto gemm_pair = [&](int a0, int a1, int Np, int Kp, int dcol) {
+    if (tid == 0) {
+      mbar_wait(&wbar[G & 1], (uint32_t)((G >> 1) & 1));
+      a4_mma(tmem, a0, (G & 1) ? Wb1 : Wb0, Np, Kp, dcol, &mbar, false, false);
+      mbar_wait(&wbar[(G + 1) & 1], (uint32_t)(((G + 1) >> 1) & 1));
+      a4_mma(tmem, a1, ((G + 1) & 1) ? Wb1 : Wb0, Np, Kp, dcol, &mbar, true, true);
+    }
+    mbar_wait(&mbar, mph & 1u);
+    ++mph;
+    tc_fence_after();
+    if (tid == 0) {
+      if (G + 2 < total_blocks && !deferred(G + 2)) stage(G + 2);
+      if (G + 3 < total_blocks && !deferred(G + 3)) stage(G + 3);
+    }
+    G += 2;
   };
   auto cta_sync_tc = [&]() {
     tc_fence_before();
@@ -1350,6 +1392,79 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
         stage(G);
         stage(G + 1);
       }
+#if A4_VOF
+      // ---- out_l = sum_h ubar_h P_h (P_h = W_V,h W_O,h), columns [0, Npa) then [Npa, No),
+      //      accumulated in TMEM [0, 64) (free: QA is dead, ubar_1 starts at Kq) ----
+      float va[16], vb[16];
+      int64_t o_idx = 0;
+      float* dst = nullptr;
+      if (quad_live) {
+        const int node = row < T ? s_node[row] : -1;
+        const int mode = row < T ? s_mode[row] : 0;
+        o_idx = A4_ROWIDX(row);
+        if (node >= 0) {
+          if (mode == 1) dst = last ? rs.dpred + o_idx * g.ld_d : nullptr;
+          else if (rs.layers_out) dst = rs.layers_out + (o_idx * g.K + l) * g.ld_d;
+          else if (rs.final_out) dst = last ? rs.final_out + o_idx * g.ld_d : nullptr;
+          else dst = rs.h + ((int64_t)node * g.K + l) * g.ld_d;
+        }
+      }
+      auto out_block = [&](int jj, float (&v)[16]) {  // TMEM [16*i, +16) -> output columns 16*jj..
+        float a[8], b[8];
+        const int col = 16 * (jj - (jj >= w.Npa / 16 ? w.Npa / 16 : 0));
+        tmem_ld8_nw(tmem + lane_base + (uint32_t)col, a);
+        tmem_ld8_nw(tmem + lane_base + (uint32_t)(col + 8), b);
+        tmem_ld_wait();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          v[k] = (16 * jj + k < g.d) ? a[k] : 0.f;
+          v[8 + k] = (16 * jj + 8 + k < g.d) ? b[k] : 0.f;
+        }
+        if (dst) {
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int c = 16 * jj + 4 * k4;
+            if (c < g.d)
+              *reinterpret_cast<float4*>(dst + c) =
+                  make_float4(v[4 * k4], v[4 * k4 + 1], v[4 * k4 + 2], v[4 * k4 + 3]);
+          }
+        }
+      };
+      gemm_pair(w.qt0, w.qt1, w.Npa, w.Ku, 0);
+      A4_MARK(7);
+      const int ja = cg, jb = w.Npa / 16 + cg;
+      // part a's x_{l+1} block waits in the (idle) row buffers, not in registers
+      float4* stash = reinterpret_cast<float4*>(Ub0) + (size_t)tid * 4;
+      if (quad_live && ja < w.Npa / 16) {
+        out_block(ja, va);
+        if (!last)
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4)
+            stash[q4] = make_float4(va[4 * q4], va[4 * q4 + 1], va[4 * q4 + 2], va[4 * q4 + 3]);
+      }
+      if (w.Npb > 0) {
+        cta_sync_tc();  // every part-a read is done before part b overwrites the columns
+        gemm_pair(w.qt0, w.qt1, w.Npb, w.Ku, 0);
+        if (quad_live && jb < w.No / 16) out_block(jb, vb);
+      }
+      A4_MARK(4);
+      if (!last) {  // x_{l+1} -> X_A (bf16 hi|lo); X_A overlaps the part-b columns and ubar_1
+        cta_sync_tc();
+        if (quad_live) {
+          if (ja < w.Npa / 16) {
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const float4 f = stash[q4];
+              va[4 * q4] = f.x; va[4 * q4 + 1] = f.y; va[4 * q4 + 2] = f.z; va[4 * q4 + 3] = f.w;
+            }
+            a4_st16(tmem + lane_base + (uint32_t)(8 * ja), tmem + lane_base + (uint32_t)(w.Kx / 2 + 8 * ja), va);
+          }
+          if (w.Npb > 0 && jb < w.No / 16)
+            a4_st16(tmem + lane_base + (uint32_t)(8 * jb), tmem + lane_base + (uint32_t)(w.Kx / 2 + 8 * jb), vb);
+          tmem_st_wait();
+        }
+      }
+#else
       // ---- c_h = ubar_h W_V,h ----
       gemm(w.qt0, w.Nv, w.Ku, 0);
       A4_MARK(7);
@@ -1416,6 +1531,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
         }
         if (!last) tmem_st_wait();
       }
+#endif
       A4_MARK(5);
       if (last && rs.write_valid && tid < T) {
         const int node = s_node[tid];

@@ -356,13 +356,14 @@ int stgn_engine_set_weights(stgn_engine* e, const stgn_weights* w) {
     e->tcw.bq = w->bq;
     e->tcw.omega = w->omega;
   }
-  e->use_a4 = e->a4_ok && w->t4q && w->t4k && w->t4v && w->t4o && w->t4bq;
+  e->use_a4 = e->a4_ok && w->t4q && w->t4k && w->t4v && w->t4o && w->t4bq && (!A4_VOF || w->t4p);
   if (e->use_a4) {
     e->a4w.wq = w->t4q;
     e->a4w.wk = w->t4k;
     e->a4w.wv = w->t4v;
     e->a4w.wo = w->t4o;
     e->a4w.bq = w->t4bq;
+    e->a4w.wp = w->t4p;
     e->a4w.omega = w->omega;
   }
 #ifdef STGN_NO_MEM4  // experiments: the FFMA memory update

@@ -653,8 +653,20 @@ class IncrementalEngine:
         wv = np.zeros((K, H, d_k, kpad))      # [n][k]
         wv[:, :, :, kmap] = np.transpose(p.w_v, (0, 1, 3, 2))
         wv[:, :, :, kmap[t0:]] *= amp
+        # folded output operands: P_h = wv_h^T (kpad x d_k) @ w_o[l, h] (d_k x d), as B
+        # operands [n = output column][k = key feature], split at column Na (stgn.h t4p)
+        No = _rup(d, 16)
+        Na = min(No, 64)
+        pk = []
+        for l in range(K):
+            P = [np.zeros((No, kpad)) for _ in range(H)]
+            for h in range(H):
+                P[h][:d, :] = (wv[l, h].T @ p.w_o[l, h * d_k:(h + 1) * d_k, :]).T
+            blocks = [P[h][:Na] for h in range(H)] + ([P[h][Na:] for h in range(H)] if No > Na else [])
+            pk += [self._pack_kmajor_bf16(b).reshape(-1) for b in blocks]
+        t4p = self._torch.cat(pk)
         return {"t4q": self._pack_kmajor_bf16(wq), "t4k": self._pack_kmajor_bf16(wk),
-                "t4v": self._pack_kmajor_bf16(wv), "t4o": self._pack_kmajor_bf16(wo),
+                "t4v": self._pack_kmajor_bf16(wv), "t4o": self._pack_kmajor_bf16(wo), "t4p": t4p,
                 "t4bq": self._torch.tensor(bq.astype(np.float32), device=self.device)}
 
     def _pack_memory_bf16x3(self):
