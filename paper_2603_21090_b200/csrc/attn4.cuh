@@ -92,7 +92,7 @@ __device__ int g_a4_prof_n;
 #define A4_EVQ 1  // quadrant fill/pack duties as an event loop (see the walk phase)
 #endif
 #ifndef A4_VOF
-#define A4_VOF 1  // out = sum_h ubar_h (W_V,h W_O,h): the V GEMMs, the c pack and the O GEMM fold
+#define A4_VOF 0  // out = sum_h ubar_h (W_V,h W_O,h): the V GEMMs, the c pack and the O GEMM fold
                   // into two passes of two MMA blocks over the TMEM ubar operands
 #endif
 #ifndef A4_RUNPTR
