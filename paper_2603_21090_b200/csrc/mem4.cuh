@@ -89,7 +89,8 @@ static inline size_t mem4_smem_bytes(const M4W& w) { return 1024 + 2 * (size_t)w
 // one thread: bf16x3 MMAs of one weight block; A = TMEM hi columns [a_hi, +Kp/2)
 // and lo columns [a_lo, +Kp/2); B = smem [Np][Kp] K-major (hi block, lo block)
 __device__ __forceinline__ void m4_mma(uint32_t tmem, int a_hi, int a_lo, const uint16_t* Wb,
-                                       int Np, int Kp, int dcol, bool acc, uint64_t* bar) {
+                                       int Np, int Kp, int dcol, bool acc, uint64_t* bar,
+                                       bool commit = true) {
   tc_fence_after();
   const uint32_t idesc = umma_idesc_bf16(128, Np);
   const uint32_t sbo = (uint32_t)(Kp / 8) * 128u;
@@ -102,7 +103,7 @@ __device__ __forceinline__ void m4_mma(uint32_t tmem, int a_hi, int a_lo, const 
     umma_bf16_ts(tmem + (uint32_t)dcol, ah, dl, idesc, 1u);
     umma_bf16_ts(tmem + (uint32_t)dcol, al, dh, idesc, 1u);
   }
-  umma_commit(bar);
+  if (commit) umma_commit(bar);
 }
 
 __device__ __forceinline__ float m4_sig(float x) { return 1.f / (1.f + __expf(-x)); }
@@ -155,11 +156,12 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
     if (total_blocks > 1) stage(1);
   }
   int64_t G = 0;
-  auto issue = [&](int a_hi, int a_lo, int dcol, bool acc, int off = 0) {  // tid 0: block G + off
+  auto issue = [&](int a_hi, int a_lo, int dcol, bool acc, int off = 0,
+                   bool commit = true) {  // tid 0: block G + off
     const int64_t Gi = G + off;
     const int j = (int)(Gi % w.nblk);
     mbar_wait(&wbar[Gi & 1], (uint32_t)((Gi >> 1) & 1));
-    m4_mma(tmem, a_hi, a_lo, (Gi & 1) ? Wb1 : Wb0, w.np[j], w.kp[j], dcol, acc, &mbar);
+    m4_mma(tmem, a_hi, a_lo, (Gi & 1) ? Wb1 : Wb0, w.np[j], w.kp[j], dcol, acc, &mbar, commit);
   };
   auto cta_sync_tc = [&]() {
     tc_fence_before();
@@ -169,13 +171,16 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
   // The MMAs of the next n blocks are done (their buffers refilled two blocks ahead),
   // then a CTA barrier. tid 0 is the only waiter on the commit barrier, in phase
   // order, so no waiter can fall two parity phases behind the commits.
-  auto wait_mma = [&](int n) {
-    if (tid == 0)
-      for (int k = 0; k < n; ++k) {
-        mbar_wait(&mbar, (uint32_t)((G + k) & 1));
+  uint32_t mph = 0;  // commits of the MMA barrier so far (its phase parity)
+  // wait for the one commit covering the next nb blocks' MMAs, refill their buffers
+  auto wait_mma = [&](int nb) {
+    if (tid == 0) {
+      mbar_wait(&mbar, mph & 1u);
+      for (int k = 0; k < nb; ++k)
         if (G + k + 2 < total_blocks) stage(G + k + 2);
-      }
-    G += n;
+    }
+    ++mph;
+    G += nb;
     cta_sync_tc();
   };
   const bool last_agg = aggregator == STGN_AGG_LAST;
@@ -307,11 +312,12 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
       A4_MARK(9);
       for (int j = 0; j < w.nmsg; ++j) {
         const int ab = (j & 1) ? 128 : 0;
-        if (tid == 0) issue(ab, ab + 64, dsrc, j > 0);
-        if (j + 1 < w.nmsg) build(j + 1, (j + 1) & 1, -1);  // the other buffer, beside the MMA
-        wait_mma(1);
-        if (tid == 0) issue(ab, ab + 64, ddst, j > 0);
-        wait_mma(1);
+        if (tid == 0) {  // both weight sides, one commit
+          issue(ab, ab + 64, dsrc, j > 0, 0, false);
+          issue(ab, ab + 64, ddst, j > 0, 1, true);
+        }
+        if (j + 1 < w.nmsg) build(j + 1, (j + 1) & 1, -1);  // the other buffer, beside the MMAs
+        wait_mma(2);
       }
     } else {  // per-side sums: A0 = src side, A1 = dst side
       A4_MARK(9);
@@ -319,10 +325,11 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
         build(j, 0, 0);
         build(j, 1, 1);
         cta_sync_tc();
-        if (tid == 0) issue(0, 64, dsrc, j > 0);
-        wait_mma(1);
-        if (tid == 0) issue(128, 128 + 64, ddst, j > 0);
-        wait_mma(1);
+        if (tid == 0) {
+          issue(0, 64, dsrc, j > 0, 0, false);
+          issue(128, 128 + 64, ddst, j > 0, 1, true);
+        }
+        wait_mma(2);
       }
     }
     A4_MARK(10);
@@ -391,10 +398,11 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
     cta_sync_tc();
     A4_MARK(11);
     // ---- D_ZR = Ag [W_z W_r] + s [U_z U_r] ----
-    if (tid == 0) issue(0, half, dz, false);
-    wait_mma(1);
-    if (tid == 0) issue(w.Nm / 2, half + w.Nm / 2, dz, true);
-    wait_mma(1);
+    if (tid == 0) {
+      issue(0, half, dz, false, 0, false);
+      issue(w.Nm / 2, half + w.Nm / 2, dz, true, 1, true);
+    }
+    wait_mma(2);
     A4_MARK(12);
     // ---- z (registers), A3 = r * s over A2's s half ----
     float zk[16];
@@ -422,10 +430,11 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
     cta_sync_tc();
     A4_MARK(13);
     // ---- D_H = Ag W_h + (r * s) U_h ----
-    if (tid == 0) issue(0, half, dz, false);
-    wait_mma(1);
-    if (tid == 0) issue(w.Nm / 2, half + w.Nm / 2, dz, true);
-    wait_mma(1);
+    if (tid == 0) {
+      issue(0, half, dz, false, 0, false);
+      issue(w.Nm / 2, half + w.Nm / 2, dz, true, 1, true);
+    }
+    wait_mma(2);
     if (mine) {
       const int j = cg;
       float a[8], b[8];
