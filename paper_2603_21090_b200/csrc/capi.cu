@@ -18,6 +18,10 @@
 #include "delta.cuh"
 #include "snapshot.cuh"
 
+#ifndef STGN_LATE_RECORDS
+#define STGN_LATE_RECORDS 1
+#endif
+
 #ifndef STGN_VERSION
 #define STGN_VERSION "stgn 0.1.0 sm_100a"
 #endif
@@ -512,6 +516,23 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   };
   mark();
   cudaStream_t dst_ = st;  // drift branch (graph mode)
+  // Change records: with an infinite window and exact scope the recompute does not
+  // need them (every list is the store's top-L: k_dupdate sets the direct nodes'
+  // cached length and the recompute reads ring_cnt for uncached nodes), so they move
+  // to the drift branch, whose estimators are their only consumer.
+  const bool late_records = STGN_LATE_RECORDS && !std::isfinite(e->cfg.window) &&
+                            e->cfg.scope != STGN_SCOPE_DELTA;
+  auto launch_records = [&](cudaStream_t rst, bool chain) {
+    if (g.L <= 32) {
+      if (chain)
+        chain_launch(k_records_warp, 8 * e->num_sms, T, 0, rst, g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
+      else
+        k_records_warp<<<8 * e->num_sms, T, 0, rst>>>(g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
+    } else {
+      k_records<<<g_wide, T, 0, rst>>>(g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
+    }
+    n += 1;
+  };
   if (part != 2) {
   if (e->cfg.scope == STGN_SCOPE_DELTA && g.K == 1 && v.attn_logz)
     cudaMemsetAsync(&v.ctl->reserved[0], 0, sizeof(int64_t), st);  // this batch's bound records
@@ -544,11 +565,7 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
     n += 2;
   }
   mark();
-  if (g.L <= 32)
-    chain_launch(k_records_warp, 8 * e->num_sms, T, 0, st, g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
-  else
-    k_records<<<g_wide, T, 0, st>>>(g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
-  n += 1;
+  if (!late_records) launch_records(st, true);
   if (e->cfg.scope == STGN_SCOPE_DELTA) {
     chain_launch(k_delta_classify, g_rec, T, 0, st, g, v, s);
     chain_launch(k_delta_fin, 1, 32, 0, st, s);
@@ -572,6 +589,7 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
     cudaEventRecord(e->ev_fork[1], st);
     cudaStreamWaitEvent(e->side[1], e->ev_fork[1], 0);
     dst_ = e->side[1];
+    if (late_records) launch_records(dst_, false);
     launch_drift(e, dst_, cond);
     n += 2;
     cudaEventRecord(e->ev_join[1], dst_);
@@ -586,6 +604,7 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
     rs.pre_n = e->cfg.scope == STGN_SCOPE_DIRECT ? &s.res->nD : &s.res->nA;
   }
   rs.post_n = &s.res->nD;
+  if (late_records) rs.use_store = 1;  // uncached lists are the store's top-L (records run later)
   rs.mem_post = s.mem_new;
   rs.valid_at_ptr = &s.hdr->t_batch;
   rs.write_valid = 1;
@@ -615,6 +634,7 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   mark();
   // drift + rebuild policy
   if (dst_ == st) {
+    if (late_records) launch_records(st, false);
     launch_drift(e, st, cond);
     n += 2;
   } else {
