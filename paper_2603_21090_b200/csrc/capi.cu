@@ -18,8 +18,11 @@
 #include "delta.cuh"
 #include "snapshot.cuh"
 
+#ifndef STGN_DRIFT_FORK
+#define STGN_DRIFT_FORK 1  // drift estimators + decision on a branch beside the recompute
+#endif
 #ifndef STGN_LATE_RECORDS
-#define STGN_LATE_RECORDS 1
+#define STGN_LATE_RECORDS 0
 #endif
 
 #ifndef STGN_VERSION
@@ -585,7 +588,7 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   // Branch 1 (graph mode): the drift estimators and the rebuild decision read
   // the change records only, so they overlap the recompute; joined before the
   // (conditional) rebuild block.
-  if (fork && !e->profiling) {
+  if (fork && !e->profiling && STGN_DRIFT_FORK) {
     cudaEventRecord(e->ev_fork[1], st);
     cudaStreamWaitEvent(e->side[1], e->ev_fork[1], 0);
     dst_ = e->side[1];
