@@ -377,6 +377,9 @@ int stgn_generate_stream(const uint64_t* rng_state, int64_t n, int64_t m, int32_
 /* Debug: phase timestamps of CTA 0 of the bf16x3 recompute kernel, returns the
  * count copied (0 unless the library was built with -DA4_PROF); resets. */
 int stgn_debug_a4_prof(uint64_t* out, int cap);
+/* Per-CTA start/end ns, ring entries, tiles of the recompute launches since the
+   last read (-DA4_PROF builds only; 0 otherwise). Debug, no reference analogue. */
+int stgn_debug_a4_cta(uint64_t* out, int cap);
 
 /*
  * Native reader of the edge-stream CSV format (S/streamio.py:15-79). Returns

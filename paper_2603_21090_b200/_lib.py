@@ -27,7 +27,7 @@ EXPORTS = (
     "stgn_engine_affected", "stgn_engine_pred_embeddings", "stgn_pipeline_many",
     "stgn_engine_set_profiling", "stgn_engine_stage_times", "stgn_stage_name",
     "stgn_engine_info", "stgn_debug_tc_gemm", "stgn_generate_stream",
-    "stgn_debug_a4_prof", "stgn_engine_set_scope", "stgn_read_stream",
+    "stgn_debug_a4_prof", "stgn_debug_a4_cta", "stgn_engine_set_scope", "stgn_read_stream",
     "stgn_engine_set_skip_recompute", "stgn_engine_delta_events", "stgn_batch_result_bytes",
     "stgn_engine_result_copy", "stgn_report_from_result", "stgn_engine_snapshot",
     "stgn_engine_set_ownership", "stgn_engine_batch_phase", "stgn_engine_dpred_export",
@@ -132,6 +132,7 @@ def lib():
     L.stgn_engine_info.argtypes = [vp, vp, C.c_int]
     L.stgn_debug_tc_gemm.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, vp, C.c_int, vp]
     L.stgn_debug_a4_prof.argtypes = [vp, C.c_int]
+    L.stgn_debug_a4_cta.argtypes = [vp, C.c_int]
     L.stgn_engine_set_scope.argtypes = [vp, C.c_int]
     L.stgn_engine_set_skip_recompute.argtypes = [vp, C.c_int]
     L.stgn_read_stream.argtypes = [C.c_char_p, i32, i64, P(i64), P(i64), vp, vp, vp, vp, P(i64)]

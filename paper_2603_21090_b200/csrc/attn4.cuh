@@ -48,6 +48,13 @@
 #ifdef A4_PROF
 __device__ unsigned long long g_a4_prof[8192];
 __device__ int g_a4_prof_n;
+// Per CTA: start ns, end ns, summed ring entries of its rows, tiles (all CTAs).
+__device__ unsigned long long g_a4_cta[4 * 1024];
+__device__ __forceinline__ unsigned long long a4_now() {
+  unsigned long long t_;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+  return t_;
+}
 #define A4_MARK(tag)                                                              \
   do {                                                                           \
     if (blockIdx.x == 0 && threadIdx.x == 0 && g_a4_prof_n < 8190) {             \
@@ -976,6 +983,10 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
   const int64_t pre_rows = rs.fused ? (int64_t)rs.pre_n[0] : N;
   const int64_t d_rows = rs.fused ? (int64_t)rs.post_n[0] : 0;
 
+#ifdef A4_PROF
+  if (tid == 0 && blockIdx.x < 1024) g_a4_cta[4 * blockIdx.x] = a4_now();
+  unsigned long long prof_e = 0;
+#endif
   if (warp == 0) tmem_alloc(&tslot, 512);
   if (tid == 0) {
     mbar_init(&mbar, 1);
@@ -1542,6 +1553,20 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
       }
     }
     cta_sync_tc();
+#ifdef A4_PROF
+    if (tid < T) prof_e += (unsigned long long)s_E[tid];
+#endif
   }
+#ifdef A4_PROF
+  if (blockIdx.x < 1024) {
+    if (prof_e) atomicAdd(&g_a4_cta[4 * blockIdx.x + 2], prof_e);
+    if (tid == 0) {
+      g_a4_cta[4 * blockIdx.x + 1] = a4_now();
+      unsigned smid_;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));
+      g_a4_cta[4 * blockIdx.x + 3] = (unsigned long long)my_tiles | ((unsigned long long)smid_ << 16);
+    }
+  }
+#endif
   if (warp == 0) tmem_free(tmem, 512);
 }

@@ -1325,6 +1325,22 @@ extern "C" int stgn_engine_set_scope(stgn_engine* e, int scope) {
   return STGN_OK;
 }
 
+// Per-CTA start/end/entries/tiles of the last recompute launches (-DA4_PROF
+// builds; reading clears them). Returns the entries written (4 per CTA).
+extern "C" int stgn_debug_a4_cta(uint64_t* out, int cap) {
+#ifdef A4_PROF
+  const int n = cap < 4 * 1024 ? cap : 4 * 1024;
+  if (cudaMemcpyFromSymbol(out, g_a4_cta, sizeof(uint64_t) * n) != cudaSuccess) return -1;
+  static uint64_t zeros[4 * 1024];
+  cudaMemcpyToSymbol(g_a4_cta, zeros, sizeof(zeros));
+  return n;
+#else
+  (void)out;
+  (void)cap;
+  return 0;
+#endif
+}
+
 // Phase timestamps of CTA 0 of the 128-row recompute kernel (builds with
 // -DA4_PROF only; otherwise 0 entries). Each entry: globaltimer_ns << 4 | tag.
 extern "C" int stgn_debug_a4_prof(uint64_t* out, int cap) {

@@ -29,6 +29,7 @@ torch.cuda.synchronize()
 L = _lib.lib()
 buf = (C.c_uint64 * 8192)()
 L.stgn_debug_a4_prof(buf, 8192)  # drop the fast-forward marks
+L.stgn_debug_a4_cta((C.c_uint64 * 4096)(), 4096)
 eng.set_profiling(True)
 eng.process_batch_arrays(st.src[edges:edges + 600], st.dst[edges:edges + 600], st.t[edges:edges + 600])
 torch.cuda.synchronize()
@@ -49,3 +50,30 @@ tot = sum(sum(v) for v in acc.values())
 for k in sorted(acc):
     v = acc[k]
     print(f"after tag {k} ({names.get(k)}): n={len(v)} total_us={sum(v):8.1f} share={100 * sum(v) / tot:5.1f}% mean_us={np.mean(v):7.2f}")
+
+# per-CTA balance of the same launch(es): start/end spread, ring entries per CTA
+buf2 = (C.c_uint64 * 4096)()
+L.stgn_debug_a4_cta(buf2, 4096)
+c = np.array(buf2[:4096], dtype=np.uint64).reshape(1024, 4).astype(np.int64)
+c = c[(c[:, 3] & 0xFFFF) > 0]
+if len(c):
+    sm = c[:, 3] >> 16
+    c[:, 3] &= 0xFFFF
+    t0 = c[:, 0].min()
+    st_us, en_us = (c[:, 0] - t0) / 1e3, (c[:, 1] - t0) / 1e3
+    dur = en_us - st_us
+    print(f"CTAs {len(c)} tiles/CTA {np.unique(c[:, 3]).tolist()}")
+    print(f"start us: min {st_us.min():.1f} p50 {np.median(st_us):.1f} max {st_us.max():.1f}")
+    print(f"end   us: min {en_us.min():.1f} p50 {np.median(en_us):.1f} mean {en_us.mean():.1f} max {en_us.max():.1f}")
+    print(f"busy  us: min {dur.min():.1f} p50 {np.median(dur):.1f} max {dur.max():.1f}")
+    e = c[:, 2].astype(np.float64)
+    print(f"entries/CTA: min {e.min():.0f} p50 {np.median(e):.0f} max {e.max():.0f}; corr(entries, busy) {np.corrcoef(e, dur)[0, 1]:.3f}")
+    print(f"us per 1K entries (fit): {1e3 * np.polyfit(e, dur, 1)[0]:.3f}, intercept {np.polyfit(e, dur, 1)[1]:.1f} us")
+    for name, m in (("SM id < 74", sm < 74), ("SM id >= 74", sm >= 74), ("even SM", sm % 2 == 0), ("odd SM", sm % 2 == 1)):
+        if m.any():
+            print(f"  {name}: n {m.sum()} mean end {en_us[m].mean():.1f} max {en_us[m].max():.1f}")
+    # a tile's rows' entries: the slowest CTAs vs the fastest
+    q = np.argsort(dur)
+    print(f"fastest 20 CTAs mean entries {e[q[:20]].mean():.0f}, slowest 20 {e[q[-20:]].mean():.0f}")
+    order = np.argsort(-en_us)[:5]
+    print("latest CTAs (idx, start, end, entries):", [(int(i), round(st_us[i], 1), round(en_us[i], 1), int(e[i])) for i in order])
