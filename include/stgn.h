@@ -322,6 +322,63 @@ int stgn_engine_info(stgn_engine* eng, int64_t* info, int n);
 int stgn_engine_snapshot(stgn_engine* eng, int64_t node_count, double t_now,
                          float* layers_out_dev, void* stream);
 
+/* Stage-level surface (the reference's unit entry points that process_batch runs
+ * fused; csrc/stage.cuh). All pointers are device memory; each call completes
+ * before returning.
+ *
+ * stage_affected replaces IncrementalEngine.detect_affected(pending)
+ * (S/engine.py:196-212): the direct endpoints of the P staged edges (src_dev,
+ * dst_dev, int32, batch order) and their K-hop closure over the post-insertion
+ * truncated lists (staged entries newest first, then the cached list or the
+ * store's top-L; S/engine.py:170-194). Writes the set to out_dev[0 ..
+ * hop_off[K+1]) in discovery order, hop_off_dev[K+2] (int32) the hop
+ * boundaries. stamp: a node-mark value no batch uses (the host takes them
+ * above 2^31). Nothing but the marks is written. STGN_ERR_CAPACITY when the
+ * set exceeds cap. */
+int stgn_engine_stage_affected(stgn_engine* eng, int32_t P, const int32_t* src_dev,
+                               const int32_t* dst_dev, uint32_t stamp, int32_t* out_dev,
+                               int64_t cap, int32_t* hop_off_dev, void* stream);
+
+/* New neighbour entries of nn distinct nodes, CSR by node, newest first. */
+typedef struct {
+  const int32_t* nodes;  /* [nn] */
+  const int32_t* off;    /* [nn + 1] */
+  const int32_t* nbr;    /* [ne] */
+  const double* t;       /* [ne] */
+  const int64_t* eid;    /* [ne] */
+  const float* pay;      /* [ne][K][ld_d] frozen stack of the opposite endpoint */
+  const float* feat;     /* [ne][ld_e] */
+  const int32_t* put;    /* [nn] 1: cache put with a record; 0: store-list refresh only */
+} stgn_stage_entries;
+
+/* Per-node records; node i's expired entries start at off[i] + i * L. */
+typedef struct {
+  int32_t* hit;      /* [nn] 1 when the node was cached */
+  int32_t* exp_n;    /* [nn] */
+  int32_t* exp_nbr;  /* [ne + nn L] */
+  double* exp_t;
+  int64_t* exp_eid;
+  int32_t* upd_n;    /* [nn] */
+  int32_t* upd_nbr;  /* [nn L] */
+} stgn_stage_records;
+
+/* update_neighbor_cache (S/engine.py:216-243) for nn nodes: prepend the new
+ * entries, evict beyond L, expire entries older than t_now - window; with put,
+ * the node's cache becomes the kept list and its record is written (expired;
+ * updated = kept older entries whose neighbour is in direct_dev, sorted, nd).
+ * put = 0 moves only the store's top-L list (commit of an uncached node). */
+int stgn_engine_stage_nbr_update(stgn_engine* eng, int32_t nn, const stgn_stage_entries* entries,
+                                 const int32_t* direct_dev, int32_t nd, double t_now,
+                                 const stgn_stage_records* records, void* stream);
+
+/* commit_pending (S/engine_base.py:108-117): the P staged edges enter the
+ * append-only store as edge ids m0 .. m0+P-1 (edge log, per-node chains, and
+ * the payload log when bound: pay_dev [P][2][K][ld_d], side 0 the src entry's
+ * payload = the dst stack). feat_dev [P][ld_e]. Lists are not touched. */
+int stgn_engine_stage_commit(stgn_engine* eng, int32_t P, const int32_t* src_dev,
+                             const int32_t* dst_dev, const double* t_dev, const float* feat_dev,
+                             const float* pay_dev, int64_t m0, void* stream);
+
 /* Node-id-range sharding (multi-GPU, paper_2603_21090_b200/shard.py). The engine
  * keeps and recomputes the frozen payload rows of nodes [lo, hi) only (hi <= lo:
  * every node; ring_pay / ring_tb / ring_feat may then be bound with a base

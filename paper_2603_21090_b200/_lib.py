@@ -31,7 +31,8 @@ EXPORTS = (
     "stgn_engine_set_skip_recompute", "stgn_engine_delta_events", "stgn_batch_result_bytes",
     "stgn_engine_result_copy", "stgn_report_from_result", "stgn_engine_snapshot",
     "stgn_engine_set_ownership", "stgn_engine_batch_phase", "stgn_engine_dpred_export",
-    "stgn_engine_dpred_import",
+    "stgn_engine_dpred_import", "stgn_engine_stage_affected", "stgn_engine_stage_nbr_update",
+    "stgn_engine_stage_commit",
 )
 
 
@@ -71,6 +72,15 @@ STATE_PTRS = (
 
 DELTA_PTRS = ("attn_logz", "ev_node", "ev_dpos", "ev_dn", "ev_nv", "ev_bound", "ev_maxv",
               "ev_zdev")
+
+
+class StageEntries(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("nodes", "off", "nbr", "t", "eid", "pay", "feat", "put")]
+
+
+class StageRecords(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("hit", "exp_n", "exp_nbr", "exp_t", "exp_eid", "upd_n",
+                                           "upd_nbr")]
 
 
 class State(C.Structure):
@@ -121,6 +131,10 @@ def lib():
     L.stgn_engine_batch_phase.argtypes = [vp, i32, i32, vp, vp, vp, vp, i64, i64, i64, vp, vp, vp]
     L.stgn_engine_dpred_export.argtypes = [vp, vp, vp, vp, vp]
     L.stgn_engine_dpred_import.argtypes = [vp, vp, vp, i64, vp]
+    L.stgn_engine_stage_affected.argtypes = [vp, i32, vp, vp, C.c_uint32, vp, i64, vp, vp]
+    L.stgn_engine_stage_nbr_update.argtypes = [vp, i32, P(StageEntries), vp, i32, dbl,
+                                               P(StageRecords), vp]
+    L.stgn_engine_stage_commit.argtypes = [vp, i32, vp, vp, vp, vp, vp, i64, vp]
     L.stgn_engine_affected.argtypes = [vp, vp, vp, i64, P(i64), P(i64), vp, vp]
     L.stgn_engine_pred_embeddings.argtypes = [vp, vp, i64, vp]
     L.stgn_pipeline_many.argtypes = [P(Dims), i64, i64] + [vp] * 18

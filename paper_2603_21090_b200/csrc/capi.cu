@@ -17,6 +17,7 @@
 #include "mem4.cuh"
 #include "delta.cuh"
 #include "snapshot.cuh"
+#include "stage.cuh"
 
 #ifndef STGN_DRIFT_FORK
 #define STGN_DRIFT_FORK 1  // drift estimators + decision on a branch beside the recompute
@@ -1155,6 +1156,55 @@ extern "C" int stgn_engine_snapshot(stgn_engine* e, int64_t node_count, double t
     stgn_set_error(__FILE__, __LINE__, ce);
     return STGN_ERR_CUDA;
   }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return STGN_OK;
+}
+
+extern "C" int stgn_engine_stage_affected(stgn_engine* e, int32_t P, const int32_t* src_dev,
+                                          const int32_t* dst_dev, uint32_t stamp, int32_t* out_dev,
+                                          int64_t cap, int32_t* hop_off_dev, void* stream) {
+  if (!e || !e->bound || P < 0 || !out_dev || !hop_off_dev || (P > 0 && (!src_dev || !dst_dev)))
+    return STGN_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  k_stage_affected<<<1, 1024, 0, st>>>(e->g, e->sv, src_dev, dst_dev, P, stamp, out_dev, cap,
+                                       hop_off_dev);
+  CUDA_TRY(cudaGetLastError());
+  int32_t n = 0;
+  CUDA_TRY(cudaMemcpyAsync(&n, hop_off_dev + e->g.K + 1, sizeof(n), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return n > cap ? STGN_ERR_CAPACITY : STGN_OK;
+}
+
+extern "C" int stgn_engine_stage_nbr_update(stgn_engine* e, int32_t nn,
+                                            const stgn_stage_entries* entries,
+                                            const int32_t* direct_dev, int32_t nd, double t_now,
+                                            const stgn_stage_records* records, void* stream) {
+  if (!e || !e->bound || !e->have_w || nn < 0 || !entries || !records || nd < 0 ||
+      (nd > 0 && !direct_dev))
+    return STGN_ERR_INVALID;
+  if (nn == 0) return STGN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const double cutoff = std::isfinite(e->cfg.window) ? t_now - e->cfg.window : -INFINITY;
+  const int blocks = (int)std::min<int64_t>(cdiv(nn, 8), 4 * e->num_sms);
+  k_stage_nbr_update<<<blocks, 256, 0, st>>>(e->g, e->sv, *entries, nn, direct_dev, nd, cutoff,
+                                             e->w.omega, *records);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return STGN_OK;
+}
+
+extern "C" int stgn_engine_stage_commit(stgn_engine* e, int32_t P, const int32_t* src_dev,
+                                        const int32_t* dst_dev, const double* t_dev,
+                                        const float* feat_dev, const float* pay_dev, int64_t m0,
+                                        void* stream) {
+  if (!e || !e->bound || P < 0) return STGN_ERR_INVALID;
+  if (P == 0) return STGN_OK;
+  if (!src_dev || !dst_dev || !t_dev || !feat_dev || (e->sv.e_pay && !pay_dev))
+    return STGN_ERR_INVALID;
+  if (m0 < 0 || m0 + P > e->st.cap_edges) return STGN_ERR_CAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  k_stage_commit<<<1, 512, 0, st>>>(e->g, e->sv, src_dev, dst_dev, t_dev, feat_dev, pay_dev, P, m0);
+  CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(st));
   return STGN_OK;
 }

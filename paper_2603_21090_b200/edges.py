@@ -6,11 +6,13 @@ the reference raises on this path.
   InputError        <- engine_base.py:30
   KernelInputError  <- kernels/reference.py:17
   DriftContractError <- drift.py:9
+  PendingEdge       <- engine_base.py:50-58
+  ChangeRecord      <- state.py:131-140
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import NamedTuple
 
 import numpy as np
@@ -54,6 +56,37 @@ class NeighborEntry(NamedTuple):
     nbr: int
     t: float
     edge_id: int
+
+
+@dataclass
+class PendingEdge:
+    """A staged batch edge (S/engine_base.py:50-58): its id, endpoints, time,
+    features and the (K, d) pre-batch stacks frozen for both endpoints."""
+
+    edge_id: int
+    src: int
+    dst: int
+    t: float
+    feat: np.ndarray
+    stack_src: np.ndarray
+    stack_dst: np.ndarray
+
+
+@dataclass
+class ChangeRecord:
+    """Per-node neighbourhood delta of one update (S/state.py:131-140)."""
+
+    added: list = field(default_factory=list)
+    expired: list = field(default_factory=list)
+    updated: set = field(default_factory=set)
+
+    @property
+    def size(self) -> int:
+        return len(self.added) + len(self.expired) + len(self.updated)
+
+    @property
+    def empty(self) -> bool:
+        return self.size == 0
 
 
 def edges_to_arrays(batch, d_e: int):

@@ -4,7 +4,11 @@ Mirrors /root/reference/pkg/src/streamtgn/engine.py:155-453 — same
 constructor (RunConfig, ModelParameters), same `process_batch`,
 `rebuild_nodes`, `full_reference` and the read-side surface the runner and
 tests use (`memory`, `cache`, `nbr_cache`, `store`, `counters`,
-`scheduler`, `last_report`, `last_affected`, `last_pred_embeddings`).
+`scheduler`, `last_report`, `last_affected`, `last_pred_embeddings`), plus the
+stage-level entry points process_batch runs fused (`stage_batch`,
+`detect_affected`, `update_neighbor_cache`, `commit_pending`, and the
+scheduler's `record_batch_changes` / `note_affected` / `decide_rebuild` /
+`execute_rebuild` / `reset`).
 All state lives on the device in PyTorch-allocated tensors; each batch is
 one call into the C ABI (include/stgn.h), which replays a captured CUDA
 graph of the sm_100a kernels. There is no CPU fallback: without a GPU or
@@ -21,8 +25,8 @@ import numpy as np
 
 from . import _lib
 from .config import ConfigError, RunConfig
-from .edges import (DriftContractError, FeatureDimError, MonotonicityError, NeighborEntry,
-                    edges_to_arrays)
+from .edges import (ChangeRecord, DriftContractError, FeatureDimError, InputError,
+                    MonotonicityError, NeighborEntry, PendingEdge, edges_to_arrays)
 from .params import ModelParameters
 
 
@@ -435,18 +439,117 @@ class _SchedulerView:
             return 0.0
         return acc * e.cfg.gamma ** (int(ctl.tau) - int(e._tab.drift_touched[pos]))
 
-    def global_drift(self):
-        ctl = self._ctl()
-        n = int(ctl.cum_count)
-        if n == 0:
-            return 0.0
-        e = self._e
+    def _decayed_all(self):
+        """Decayed estimators of the cumulative set, by position (device)."""
+        e, ctl = self._e, self._ctl()
+        n, tau = int(ctl.cum_count), int(ctl.tau)
         torch = e._torch
         acc = e._tab.drift_acc[:n]
-        dec = torch.pow(torch.tensor(e.cfg.gamma, dtype=torch.float64, device=e.device),
-                        (int(ctl.tau) - e._tab.drift_touched[:n]).to(torch.float64))
-        tot = torch.where(acc != 0.0, acc * dec, torch.zeros_like(acc)).sum()
-        return float(tot.item()) / n  # one reduction on the device (S/drift.py:62-70)
+        age = tau - e._tab.drift_touched[:n]
+        if tau < e._tab.gpow.numel():  # the gamma^k table the batch kernels use
+            dec = e._tab.gpow[age.clamp(0, e._tab.gpow.numel() - 1)]
+        else:
+            dec = torch.pow(torch.tensor(e.cfg.gamma, dtype=torch.float64, device=e.device),
+                            age.to(torch.float64))
+        return torch.where(acc != 0.0, acc * dec, torch.zeros_like(acc))
+
+    def global_drift(self):
+        n = int(self._ctl().cum_count)
+        if n == 0:
+            return 0.0
+        # one reduction on the device (S/drift.py:62-70)
+        return float(self._decayed_all().sum().item()) / n
+
+    @property
+    def delta_max(self):
+        return self._e.cfg.delta_max
+
+    @property
+    def alpha(self):
+        return self._e.cfg.alpha
+
+    def note_affected(self, nodes) -> None:
+        """S/drift.py:59-60: nodes join the cumulative affected set."""
+        e = self._e
+        torch, tab = e._torch, e._tab
+        ids = sorted({int(v) for v in nodes})
+        if not ids:
+            return
+        e._grow(need_nodes=ids[-1] + 1)
+        tab = e._tab
+        ctl = self._ctl()
+        gen = int(ctl.cum_gen) + 1
+        idx = torch.tensor(ids, dtype=torch.int64, device=e.device)
+        new = idx[tab.cum_mark[idx] != gen]
+        k, n0 = int(new.numel()), int(ctl.cum_count)
+        if k == 0:
+            return
+        pos = torch.arange(n0, n0 + k, dtype=torch.int64, device=e.device)
+        tab.cum_mark[new] = gen
+        tab.cum_list[pos] = new.to(torch.int32)
+        tab.cum_pos[new] = pos.to(torch.int32)
+        tab.drift_acc[pos] = 0.0
+        tab.drift_touched[pos] = 0
+        tab.ctl[1] = n0 + k
+
+    def record_batch_changes(self, changes: dict) -> None:
+        """S/drift.py:51-57: tau advances; each v's estimator becomes
+        gamma^elapsed * acc + |dN_v| / |N_v|. Estimators live at the node's
+        position in the cumulative set (csrc/batch.cuh k_drift_record), so a
+        recorded node also joins that set (the engine always notes the nodes it
+        records, S/engine.py:371-372)."""
+        e = self._e
+        tab = e._tab
+        tau = int(self._ctl().tau) + 1
+        tab.ctl[0] = tau
+        items = []
+        for v, (dn, nv) in changes.items():
+            if nv <= 0:
+                raise DriftContractError(f"node {v}: |N_v| must be positive")
+            items.append((int(v), dn, nv))
+        if not items:
+            return
+        self.note_affected([v for v, _, _ in items])
+        tab = e._tab
+        torch = e._torch
+        idx = torch.tensor([v for v, _, _ in items], dtype=torch.int64, device=e.device)
+        pos = tab.cum_pos[idx].to(torch.int64)
+        acc = tab.drift_acc[pos].tolist()
+        tch = tab.drift_touched[pos].tolist()
+        g = e.cfg.gamma
+        new = [(a * g ** (tau - t) if a != 0.0 else 0.0) + dn / nv
+               for a, t, (_, dn, nv) in zip(acc, tch, items)]
+        tab.drift_acc[pos] = torch.tensor(new, dtype=torch.float64, device=e.device)
+        tab.drift_touched[pos] = tau
+
+    def decide_rebuild(self, n: int):
+        """S/drift.py:72-78: None, ("partial", drifted nodes) or ("full", None)."""
+        if self.global_drift() <= self.delta_max:
+            return None
+        e = self._e
+        n_c = int(self._ctl().cum_count)
+        dec = self._decayed_all()
+        drifted = set(e._tab.cum_list[:n_c][dec > self.delta_max].tolist())
+        if len(drifted) < self.alpha * n:
+            return ("partial", drifted)
+        return ("full", None)
+
+    def execute_rebuild(self, decision, engine) -> int:
+        """S/drift.py:80-90: run the rebuild on the engine, then reset."""
+        if decision is None:
+            raise DriftContractError("execute_rebuild needs a non-None decision")
+        kind, nodes = decision
+        count = engine.rebuild_nodes(sorted(nodes) if kind == "partial" else None)
+        self.reset()
+        return count
+
+    def reset(self) -> None:
+        """S/drift.py:92-96 (as k_drift_reset_fin: forgetting the set clears
+        every estimator)."""
+        ctl = self._e._tab.ctl
+        ctl[0] = 0
+        ctl[1] = 0
+        ctl[2] += 1  # cum_gen (low word)
 
 
 class IncrementalEngine:
@@ -539,6 +642,9 @@ class IncrementalEngine:
         self._ev_batch = -1     # batch whose bound records self._events holds
         self._events: list = []
         self._preds = np.zeros(self._max_batch, dtype=np.float64)
+        self._pending: dict = {}       # staged edges by id (stage_batch .. commit_pending)
+        self._stage_put: set = set()   # nodes whose lists update_neighbor_cache moved
+        self._stage_stamp = 0x80000000  # node marks of detect_affected (batches use < 2^31)
 
     # -- plumbing -------------------------------------------------------------
     def _stream(self):
@@ -790,6 +896,8 @@ class IncrementalEngine:
         self.counters.start_batch()
         self._affected_cache = None
         self._pred_cache = None
+        self._pending.clear()  # the fused batch stages and commits its own edges
+        self._stage_put.clear()
         src = np.ascontiguousarray(src, dtype=np.int64)
         dst = np.ascontiguousarray(dst, dtype=np.int64)
         t = np.ascontiguousarray(t, dtype=np.float64)
@@ -1235,6 +1343,203 @@ class IncrementalEngine:
             raise DriftContractError("execute_rebuild needs a non-None decision")
         kind, nodes = decision
         return self.rebuild_nodes(sorted(nodes) if kind == "partial" else None)
+
+    # -- stage-level surface (csrc/stage.cuh) -----------------------------------
+    def _stack_of(self, row) -> np.ndarray:
+        """gather_stacks row -> the reference's (K, d) stack (S/state.py:118-127)."""
+        dm = self.dims
+        st = np.zeros((self.K, dm.d))
+        st[0, :dm.d_s] = row[:dm.d_s]
+        for j in range(1, self.K):
+            o = self.ld_s + (j - 1) * self.ld_d
+            st[j] = row[o:o + dm.d]
+        return st
+
+    def stage_batch(self, batch) -> list:
+        """S/engine_base.py:88-106: edge ids from the store's count, both
+        endpoints' pre-batch stacks frozen (one device gather). Nothing is
+        committed; the edges wait in `_pending` for commit_pending."""
+        torch = self._torch
+        src, dst, t, feat = edges_to_arrays(batch, self.dims.d_e)
+        B = len(batch)
+        if B == 0:
+            return []
+        top = int(max(src.max(), dst.max())) + 1
+        self._grow(need_nodes=max(self._n_mem, top, self.cfg.nodes, self._store_n),
+                   need_edges=self._m + B)
+        self._n_mem = max(self._n_mem, top)
+        ids = torch.from_numpy(np.concatenate([src, dst])).to(self.device)
+        rows = self.gather_stacks(ids).double().cpu().numpy()
+        out = []
+        for i in range(B):
+            pe = PendingEdge(edge_id=self._m + i, src=int(src[i]), dst=int(dst[i]), t=float(t[i]),
+                             feat=feat[i].copy(), stack_src=self._stack_of(rows[i]),
+                             stack_dst=self._stack_of(rows[B + i]))
+            self._pending[pe.edge_id] = pe
+            out.append(pe)
+        return out
+
+    def detect_affected(self, pending) -> AffectedSet:
+        """S/engine.py:196-212 on the device (k_stage_affected): the direct
+        endpoints and their K-hop closure over the post-insertion truncated
+        lists; nothing is mutated. Records start empty, as in the reference."""
+        torch = self._torch
+        pending = list(pending)
+        if not pending:
+            return AffectedSet(set(), set(), {})
+        dev = self.device
+        src = torch.tensor([pe.src for pe in pending], dtype=torch.int32, device=dev)
+        dst = torch.tensor([pe.dst for pe in pending], dtype=torch.int32, device=dev)
+        top = int(max(src.max().item(), dst.max().item())) + 1
+        self._grow(need_nodes=max(top, self.node_count))
+        cap = self._tab.cap_nodes
+        out = torch.empty(cap, dtype=torch.int32, device=dev)
+        hop = torch.zeros(self.K + 2, dtype=torch.int32, device=dev)
+        self._stage_stamp = self._stage_stamp + 1 if self._stage_stamp < 0xFFFFFFFF else 0x80000000
+        _lib.check(self._L.stgn_engine_stage_affected(
+            self._handle, len(pending), src.data_ptr(), dst.data_ptr(), self._stage_stamp,
+            out.data_ptr(), cap, hop.data_ptr(), self._stream()), "stage_affected")
+        h = hop.cpu().numpy()
+        ids = out[:int(h[self.K + 1])].cpu().numpy()
+        allset = set(ids.tolist())
+        return AffectedSet(set(ids[:int(h[1])].tolist()), allset,
+                           {v: ChangeRecord() for v in allset})
+
+    def _entry_payload(self, e, viewer):
+        """(stack (K, d), feat) of entry e seen from `viewer` (S/engine_base.py:119-133)."""
+        pe = self._pending.get(int(e.edge_id))
+        if pe is not None:
+            return (pe.stack_dst if viewer == pe.src else pe.stack_src), pe.feat
+        eid = int(e.edge_id)
+        if eid >= self._m or self._tab.e_pay is None:
+            raise InputError(f"edge {eid} is neither staged nor in the payload log "
+                             "(build the engine with edge_payloads=True)")
+        side = 0 if int(self._tab.e_src[eid]) == viewer else 1
+        row = self._tab.e_pay[2 * eid + side].double().cpu().numpy()
+        st = row.reshape(self.K, self.ld_d)[:, :self.dims.d]
+        return st, self._tab.e_feat[eid, :self.dims.d_e].double().cpu().numpy()
+
+    def _stage_update(self, items, direct, t_now):
+        """items: [(v, [NeighborEntry newest first], put)] with distinct v.
+        Returns per item (hit, expired entries, updated neighbours)."""
+        torch = self._torch
+        if not items:
+            return []
+        dev, K, dm = self.device, self.K, self.dims
+        top = max(v for v, _, _ in items) + 1
+        self._grow(need_nodes=max(top, self.node_count))
+        nodes = [int(v) for v, _, _ in items]
+        off = np.zeros(len(items) + 1, dtype=np.int32)
+        for i, (_, ents, _) in enumerate(items):
+            off[i + 1] = off[i] + len(ents)
+        ne = int(off[-1])
+        pay = np.zeros((max(ne, 1), K, self.ld_d), dtype=np.float32)
+        feat = np.zeros((max(ne, 1), self.ld_e), dtype=np.float32)
+        nbr = np.zeros(max(ne, 1), dtype=np.int32)
+        tt = np.zeros(max(ne, 1), dtype=np.float64)
+        eid = np.zeros(max(ne, 1), dtype=np.int64)
+        q = 0
+        for v, ents, _ in items:
+            for e in ents:
+                st, f = self._entry_payload(e, v)
+                pay[q, :, :dm.d] = st
+                feat[q, :dm.d_e] = f
+                nbr[q], tt[q], eid[q] = int(e.nbr), float(e.t), int(e.edge_id)
+                q += 1
+
+        def up(a):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        d_nodes, d_off, d_nbr, d_t, d_eid = map(up, (np.array(nodes, dtype=np.int32), off, nbr,
+                                                     tt, eid))
+        d_pay, d_feat = up(pay), up(feat)
+        d_put = up(np.array([1 if p else 0 for _, _, p in items], dtype=np.int32))
+        d_dir = up(np.array(sorted(int(x) for x in direct) or [0], dtype=np.int32))
+        nn, L = len(items), self.L
+        z = torch.zeros
+        hit, exp_n, upd_n = (z(nn, dtype=torch.int32, device=dev) for _ in range(3))
+        exp_nbr = z(ne + nn * L, dtype=torch.int32, device=dev)
+        exp_t = z(ne + nn * L, dtype=torch.float64, device=dev)
+        exp_eid = z(ne + nn * L, dtype=torch.int64, device=dev)
+        upd_nbr = z(nn * L, dtype=torch.int32, device=dev)
+        ent = _lib.StageEntries(*[x.data_ptr() for x in (d_nodes, d_off, d_nbr, d_t, d_eid, d_pay,
+                                                         d_feat, d_put)])
+        rec = _lib.StageRecords(*[x.data_ptr() for x in (hit, exp_n, exp_nbr, exp_t, exp_eid,
+                                                         upd_n, upd_nbr)])
+        _lib.check(self._L.stgn_engine_stage_nbr_update(
+            self._handle, nn, C.byref(ent), d_dir.data_ptr(), len(direct), float(t_now),
+            C.byref(rec), self._stream()), "stage_nbr_update")
+        hit, exp_n, upd_n = hit.tolist(), exp_n.tolist(), upd_n.tolist()
+        exp_nbr, exp_t, exp_eid = exp_nbr.tolist(), exp_t.tolist(), exp_eid.tolist()
+        upd_nbr = upd_nbr.tolist()
+        out = []
+        for i in range(nn):
+            xo = int(off[i]) + i * L
+            expired = [NeighborEntry(exp_nbr[xo + k], exp_t[xo + k], exp_eid[xo + k])
+                       for k in range(exp_n[i])]
+            out.append((bool(hit[i]), expired, set(upd_nbr[i * L:i * L + upd_n[i]])))
+        return out
+
+    def update_neighbor_cache(self, v: int, new_entries, direct, t_now: float) -> ChangeRecord:
+        """S/engine.py:216-243 on the device (k_stage_nbr_update): prepend,
+        evict beyond L, expire outside the window; returns the ChangeRecord.
+        New entries must be staged (stage_batch) or in the payload log."""
+        new_entries = list(new_entries)
+        hit, expired, updated = self._stage_update([(int(v), new_entries, True)], set(direct),
+                                                   t_now)[0]
+        self.counters.add("nbr_hit" if hit else "nbr_miss")
+        self._stage_put.add(int(v))
+        return ChangeRecord(added=new_entries, expired=expired, updated=updated)
+
+    def commit_pending(self) -> None:
+        """S/engine_base.py:108-117: the staged edges enter the store in id
+        order (k_stage_commit). The store's top-L lists of their endpoints move
+        with them; a cached endpoint whose list update_neighbor_cache did not
+        move gets the post-insertion list (the cache and the store's top-L share
+        one ring per node here, csrc/stage.cuh)."""
+        if not self._pending:
+            return
+        torch = self._torch
+        eids = sorted(self._pending)
+        if eids != list(range(self._m, self._m + len(eids))):
+            raise InputError(f"staged edge ids {eids[0]}..{eids[-1]} do not follow the store "
+                             f"count {self._m}")
+        pes = [self._pending[i] for i in eids]
+        prev = self._t_now
+        for pe in pes:
+            if pe.t < prev:
+                raise MonotonicityError(
+                    f"batch edge at t={pe.t} precedes committed history t={prev}")
+            prev = pe.t
+        P, dev, dm = len(pes), self.device, self.dims
+        by_node: dict = {}
+        for pe in reversed(pes):  # S/engine.py:170-180
+            by_node.setdefault(pe.src, []).append(NeighborEntry(pe.dst, pe.t, pe.edge_id))
+            if pe.dst != pe.src:
+                by_node.setdefault(pe.dst, []).append(NeighborEntry(pe.src, pe.t, pe.edge_id))
+        todo = [v for v in by_node if v not in self._stage_put]
+        if todo:
+            cached = self._tab.ring_ccnt[torch.tensor(todo, dtype=torch.int64, device=dev)]
+            items = [(v, by_node[v], c >= 0) for v, c in zip(todo, cached.tolist())]
+            self._stage_update(items, set(by_node), pes[-1].t)
+        src = torch.tensor([pe.src for pe in pes], dtype=torch.int32, device=dev)
+        dst = torch.tensor([pe.dst for pe in pes], dtype=torch.int32, device=dev)
+        tt = torch.tensor([pe.t for pe in pes], dtype=torch.float64, device=dev)
+        feat = np.zeros((P, self.ld_e), dtype=np.float32)
+        pay = np.zeros((P, 2, self.K, self.ld_d), dtype=np.float32)
+        for i, pe in enumerate(pes):
+            feat[i, :dm.d_e] = pe.feat
+            pay[i, 0, :, :dm.d] = pe.stack_dst
+            pay[i, 1, :, :dm.d] = pe.stack_src
+        d_feat = torch.from_numpy(feat).to(dev)
+        d_pay = torch.from_numpy(pay).to(dev)
+        _lib.check(self._L.stgn_engine_stage_commit(
+            self._handle, P, src.data_ptr(), dst.data_ptr(), tt.data_ptr(), d_feat.data_ptr(),
+            d_pay.data_ptr(), self._m, self._stream()), "stage_commit")
+        self._m += P
+        self._t_now = pes[-1].t
+        self._store_n = max(self._store_n, max(max(pe.src, pe.dst) for pe in pes) + 1)
+        self._pending.clear()
+        self._stage_put.clear()
 
     def sync(self):
         self._torch.cuda.current_stream(self.device).synchronize()
