@@ -46,7 +46,22 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-template <int KF, int MAXH>
+// Key input element a of one ring entry: [payload_l || feat || phi(dt)] (the
+// reference's kin_row, S/engine_base.py:135-137).
+__device__ __forceinline__ float a2_key(const Geo& g, const EngW& w, const float* pay,
+                                        const float* ft, double dt, int a) {
+  if (a < g.d) return pay[a];
+  if (a < g.d + g.d_e) return ft[a - g.d];
+  const int p = a - g.d - g.d_e;
+  float sv, cv;
+  phase_sincos(w.omega[p >> 1], dt, &sv, &cv);
+  return ((p & 1) ? sv : cv) * g.phi_amp;
+}
+
+// GEN = 1: any widths (d, d_e, d_t, H): the walk keeps no per-lane register
+// arrays; one head at a time, the query is read from shared memory and the
+// value accumulator lives in a per-warp row of the (then idle) weight stage.
+template <int KF, int MAXH, int GEN = 0>
 __global__ void __launch_bounds__(A2_THREADS, 1)
 attn2_kernel(Geo g, EngW w, RingSrc rs, int tmax, int wsm_floats) {
   constexpr int KP = 4;  // payload elements per lane (d <= 128)
@@ -159,6 +174,38 @@ attn2_kernel(Geo g, EngW w, RingSrc rs, int tmax, int wsm_floats) {
                            g.k_in, g.H, U, UK, g.k_in, g.inv_sqrt_dk, nullptr, 0, false, Wsm,
                            wsm_floats);
       // per-node online softmax over the ring entries, ubar into U
+      if constexpr (GEN) {
+        float* ub = Wsm + warp * round_up(g.k_in, 4);
+        for (int i = warp; i < T; i += A2_WARPS) {
+          const int node = s_node[i];
+          const int E = s_E[i];
+          for (int hh = 0; hh < g.H; ++hh) {
+            const int hb = hh * g.k_in;
+            for (int a = lane; a < g.k_in; a += 32) ub[a] = 0.f;
+            float mx = -INFINITY, zs = 0.f;
+            for (int e = 0; e < E; ++e) {
+              int slot = s_head[i] + e;
+              if (slot >= g.L) slot -= g.L;
+              const float* pay = rs.ring_pay + (((int64_t)node * g.K + l) * g.L + slot) * g.ld_d;
+              const float* ft = rs.ring_feat + ((int64_t)node * g.L + slot) * g.ld_e;
+              const double dt = s_tref[i] - rs.ring_t[(int64_t)node * g.L + slot];
+              float part = 0.f;
+              for (int a = lane; a < g.k_in; a += 32)
+                part = fmaf(U[r4(i, hb + a, UK)], a2_key(g, w, pay, ft, dt, a), part);
+              const float logit = warp_sum(part);
+              const float nm = fmaxf(mx, logit);
+              const float sc = __expf(mx - nm);
+              const float p = __expf(logit - nm);
+              zs = fmaf(zs, sc, p);
+              for (int a = lane; a < g.k_in; a += 32)
+                ub[a] = fmaf(p, a2_key(g, w, pay, ft, dt, a), ub[a] * sc);
+              mx = nm;
+            }
+            const float inv = E > 0 ? 1.f / zs : 0.f;
+            for (int a = lane; a < g.k_in; a += 32) U[r4(i, hb + a, UK)] = ub[a] * inv;
+          }
+        }
+      } else
       for (int i = warp; i < T; i += A2_WARPS) {
         const int node = s_node[i];
         const int E = s_E[i];

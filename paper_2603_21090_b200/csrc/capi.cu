@@ -117,6 +117,7 @@ struct stgn_engine {
   M4W m4w;                      // bf16x3 tcgen05 memory update (when the plan fits)
   size_t mem4_smem = 0;
   bool m4_ok = false, use_m4 = false;
+  bool ds_ok = false;           // k_delta_state's shared-memory plan fits (delta mode)
   bool skip_recompute = false;  // state-only fast-forward (tests): no attention launches
   EngW ew;
   size_t mem_smem = 0;
@@ -151,15 +152,18 @@ static void drop_graph(stgn_engine* e) {
   }
 }
 
-static int validate_dims(const stgn_dims* d, const stgn_config* c) {
+// operator = true: the flat pipeline_many kernel's register budget (attn.cuh:
+// H <= 4, k_in <= 512). The engine takes any widths its shared-memory plans fit
+// (the width-generic attn2 walk covers what the register-resident walks do not).
+static int validate_dims(const stgn_dims* d, const stgn_config* c, bool op = false) {
   if (!d || !c) return STGN_ERR_INVALID;
   if (d->d_s <= 0 || d->d_t <= 0 || d->d_m <= 0 || d->d_k <= 0 || d->heads <= 0 ||
       d->layers <= 0 || d->d_e < 0 || d->d_x < 0 || (d->d_t & 1))
     return STGN_ERR_INVALID;
-  if (d->layers > STGN_MAX_LAYERS || d->heads > 4) return STGN_ERR_INVALID;
+  if (d->layers > STGN_MAX_LAYERS || d->heads > (op ? 4 : 64)) return STGN_ERR_INVALID;
   if (c->fanout < 1 || c->max_batch < 1) return STGN_ERR_INVALID;
   const int k_in = d->d_s + d->d_x + d->d_e + d->d_t;
-  if (k_in > 16 * 32) return STGN_ERR_INVALID;
+  if (k_in > (op ? 16 * 32 : 8192)) return STGN_ERR_INVALID;
   return STGN_OK;
 }
 
@@ -201,28 +205,31 @@ int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engin
     delete e;
     return STGN_ERR_CUDA;
   }
-  if (e->g.d > 128 || e->g.d_e > 192 || e->g.half > 64) {  // attn2 register budget
-    delete e;
-    return STGN_ERR_INVALID;
-  }
-  e->attn2 = e->g.d_e > 0 ? (e->g.H > 2 ? attn2_kernel<6, 4> : attn2_kernel<6, 2>)
-                          : (e->g.H > 2 ? attn2_kernel<0, 4> : attn2_kernel<0, 2>);
+  // register-resident walk within its budget, else the width-generic walk
+  const bool a2_gen = e->g.d > 128 || e->g.d_e > 192 || e->g.half > 64 || e->g.H > 4;
+  e->attn2 = a2_gen ? attn2_kernel<0, 1, 1>
+                    : e->g.d_e > 0 ? (e->g.H > 2 ? attn2_kernel<6, 4> : attn2_kernel<6, 2>)
+                                   : (e->g.H > 2 ? attn2_kernel<0, 4> : attn2_kernel<0, 2>);
   {  // tile rows vs staged-weight space within ~220 KB of shared memory
     const int64_t budget = 220 * 1024 / 4;
-    const int64_t row = attn2_row_floats(e->g), full = attn2_wsm_full(e->g);
+    // the generic walk keeps one k_in row per warp in the weight stage
+    const int64_t gen_ws = a2_gen ? A2_WARPS * round_up(e->g.k_in, 4) : 0;
+    const int64_t row = attn2_row_floats(e->g),
+                  full = std::max<int64_t>(attn2_wsm_full(e->g), gen_ws);
     int64_t tmax = (budget - full) / row / 4 * 4;
     int64_t wsm;
     if (tmax >= 8) {
       if (tmax > A2_TMAX) tmax = A2_TMAX;
       wsm = budget - tmax * row;
     } else {  // stage weights in chunks
-      wsm = 16 * 1024;
+      wsm = std::max<int64_t>(16 * 1024, gen_ws);
       tmax = (budget - wsm) / row / 4 * 4;
       if (tmax > A2_TMAX) tmax = A2_TMAX;
       wsm = budget - tmax * row;
     }
     const int64_t ldmax = round_up(e->g.k_in > e->g.HD ? e->g.k_in : e->g.HD, 4);
-    if (tmax < 4 || wsm < (int64_t)e->g.H * ldmax) {
+    const int64_t need = std::max<int64_t>((int64_t)e->g.H * ldmax, gen_ws);
+    if (tmax < 4 || wsm < need) {
       delete e;
       return STGN_ERR_INVALID;
     }
@@ -282,6 +289,15 @@ int stgn_engine_create(const stgn_dims* dims, const stgn_config* cfg, stgn_engin
       return STGN_ERR_INVALID;
     }
     e->mem_smem = (size_t)(act + e->mem_wsm) * sizeof(float);
+  }
+  e->ds_ok = delta_state_smem(e->g) <= 227 * 1024 &&
+             cudaFuncSetAttribute((const void*)k_delta_state,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)delta_state_smem(e->g)) == cudaSuccess;
+  cudaGetLastError();
+  if (e->cfg.scope == STGN_SCOPE_DELTA && e->g.K == 1 && (e->g.H > 4 || !e->ds_ok)) {
+    delete e;
+    return STGN_ERR_INVALID;
   }
   ce = cudaFuncSetAttribute((const void*)k_memory, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)e->mem_smem);
@@ -1296,7 +1312,7 @@ extern "C" int stgn_pipeline_many(const stgn_dims* dims, int64_t N, int64_t E, c
   memset(&c, 0, sizeof(c));
   c.fanout = 1;
   c.max_batch = 1;
-  int rc = validate_dims(dims, &c);
+  int rc = validate_dims(dims, &c, true);
   if (rc) return rc;
   if (N < 0 || E < 0) return STGN_ERR_INVALID;
   if (N == 0) return STGN_OK;
@@ -1370,6 +1386,8 @@ extern "C" int stgn_engine_set_scope(stgn_engine* e, int scope) {
              scope != STGN_SCOPE_DELTA))
     return STGN_ERR_INVALID;
   if (scope == STGN_SCOPE_DIRECT && std::isfinite(e->cfg.window)) return STGN_ERR_INVALID;
+  if (scope == STGN_SCOPE_DELTA && e->g.K == 1 && (e->g.H > 4 || !e->ds_ok))
+    return STGN_ERR_INVALID;  // attn_logz keeps 4 heads; the state kernel's smem plan
   e->cfg.scope = scope;
   drop_graph(e);
   return STGN_OK;

@@ -182,6 +182,40 @@ def test_engine_vs_oracle_fresh_stream(cuda):
     assert_rows_close(eng.cache.h[:n].reshape(n, -1), orc.h[:n].reshape(n, -1), "h")
 
 
+@pytest.mark.parametrize("wide", ["d160_de200_dt160_h6_k2", "d40_de0_dt140_h5_k1"])
+@pytest.mark.parametrize("tc", [True, False])
+def test_widths_beyond_register_walks(cuda, wide, tc):
+    """Widths the register-resident walks do not cover (d > 128, d_e > 192,
+    d_t > 128, H > 4; the reference accepts any valid Dims, S/config.py:47-51):
+    the width-generic attn2 walk (or split-TF32 where its plan fits) against
+    the oracle, sets exact."""
+    from oracle.stgn_oracle import Oracle
+    from paper_2603_21090_b200.config import Dims, RunConfig
+    from paper_2603_21090_b200.engine import IncrementalEngine
+    from paper_2603_21090_b200.streamio import generate_stream
+    from golden_util import random_params
+    if wide.startswith("d160"):
+        dims = Dims(d_s=160, d_e=200, d_t=160, d_m=64, d_k=24, heads=6, layers=2)
+    else:
+        dims = Dims(d_s=40, d_e=0, d_t=140, d_m=32, d_k=12, heads=5, layers=1)
+    cfg = RunConfig(dims=dims, batch_size=100, fanout=6, nodes=300, rebuild="adaptive")
+    params = random_params(3, dims)
+    stream = generate_stream(5, 300, 1500, attachment="preferential", d_e=dims.d_e)
+    eng = IncrementalEngine(cfg, params, tensor_cores=tc)
+    orc = Oracle(cfg, params)
+    worst = 0.0
+    for b in batches(stream, 100):
+        p = eng.process_batch_arrays(b.src, b.dst, b.t, b.feat)
+        q = orc.process_batch(b.src, b.dst, b.t, b.feat)
+        assert eng.last_affected.all == orc.last_all
+        assert eng.last_affected.direct == orc.last_direct
+        worst = max(worst, float(np.max(np.abs(p - np.array(q)))))
+    assert worst <= PRED_ATOL
+    n = orc.node_count
+    assert_rows_close(eng.memory.states[:n], orc.mem[:n], "memory")
+    assert_rows_close(eng.cache.h[:n].reshape(n, -1), orc.h[:n].reshape(n, -1), "h")
+
+
 def test_distributed_full_rebuild_nccl_world1(cuda):
     """The sharded-rebuild path over NCCL (one rank here) equals rebuild_nodes(None)."""
     import os
