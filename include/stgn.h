@@ -379,6 +379,44 @@ int stgn_engine_stage_commit(stgn_engine* eng, int32_t P, const int32_t* src_dev
                              const int32_t* dst_dev, const double* t_dev, const float* feat_dev,
                              const float* pay_dev, int64_t m0, void* stream);
 
+/* DySAT streaming inference (paper_2603_21090_b200/dysat.py states the model;
+ * the reference reports DySAT results only, and ships no
+ * code). All pointers are device memory bound by the caller; row widths padded
+ * to ld (a multiple of 4). */
+typedef struct {
+  int32_t d_in, d, heads_s, heads_t, window, fanout, ld, max_batch;
+  int64_t n, snapshot, pos_len, chunk;
+  const float* P;        /* [n][ld]  X W_s */
+  const float* ss;       /* [n][heads_s]  a_self,h . P_v,h */
+  const float* sn;       /* [n][heads_s]  a_nbr,h . P_v,h */
+  int32_t* lst_nbr;      /* [n][fanout]  current-snapshot lists (rings, newest at head) */
+  int32_t* lst_head;     /* [n] */
+  int32_t* lst_cnt;      /* [n] */
+  float* hist_k;         /* [n][window][ld]  temporal key rows by snapshot mod window */
+  float* hist_v;         /* [n][window][ld] */
+  float* emb;            /* [n][ld]  current embeddings */
+  int32_t* mark;         /* [n] node stamps */
+  int32_t* work;         /* [2 max_batch + 8]: affected list, count at [2 max_batch] */
+  float* rows;           /* [max(chunk, 2 max_batch)][ld] structural rows */
+  const float* pos;      /* [pos_len][ld] */
+  const float *wq, *wk, *wv, *wo;  /* [d][ld] */
+  const double* wpred;   /* [2 d] */
+  double bpred;
+} stgn_dysat;
+
+/* One snapshot segment of B edges (device int32 ids, all of snapshot
+ * s->snapshot): scores from the pre-batch embeddings into preds_dev, then the
+ * endpoints' lists, structural and temporal rows. *n_affected (host, nullable:
+ * no synchronisation) = the endpoints' count; the list is s->work[0 .. n). */
+int stgn_dysat_batch(const stgn_dysat* s, int32_t B, const int32_t* src_dev,
+                     const int32_t* dst_dev, uint32_t stamp, double* preds_dev,
+                     int32_t* n_affected, void* stream);
+/* Every node at the current snapshot (the full-recompute baseline). */
+int stgn_dysat_recompute_all(const stgn_dysat* s, void* stream);
+/* Snapshot boundary (the caller has advanced s->snapshot): clear the lists,
+ * recompute every node. */
+int stgn_dysat_roll(const stgn_dysat* s, void* stream);
+
 /* Node-id-range sharding (multi-GPU, paper_2603_21090_b200/shard.py). The engine
  * keeps and recomputes the frozen payload rows of nodes [lo, hi) only (hi <= lo:
  * every node; ring_pay / ring_tb / ring_feat may then be bound with a base

@@ -32,7 +32,7 @@ EXPORTS = (
     "stgn_engine_result_copy", "stgn_report_from_result", "stgn_engine_snapshot",
     "stgn_engine_set_ownership", "stgn_engine_batch_phase", "stgn_engine_dpred_export",
     "stgn_engine_dpred_import", "stgn_engine_stage_affected", "stgn_engine_stage_nbr_update",
-    "stgn_engine_stage_commit",
+    "stgn_engine_stage_commit", "stgn_dysat_batch", "stgn_dysat_recompute_all", "stgn_dysat_roll",
 )
 
 
@@ -81,6 +81,16 @@ class StageEntries(C.Structure):
 class StageRecords(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("hit", "exp_n", "exp_nbr", "exp_t", "exp_eid", "upd_n",
                                            "upd_nbr")]
+
+
+class DySAT(C.Structure):
+    _fields_ = ([(n, C.c_int32) for n in ("d_in", "d", "heads_s", "heads_t", "window", "fanout",
+                                          "ld", "max_batch")] +
+                [(n, C.c_int64) for n in ("n", "snapshot", "pos_len", "chunk")] +
+                [(n, C.c_void_p) for n in ("P", "ss", "sn", "lst_nbr", "lst_head", "lst_cnt",
+                                           "hist_k", "hist_v", "emb", "mark", "work", "rows",
+                                           "pos", "wq", "wk", "wv", "wo", "wpred")] +
+                [("bpred", C.c_double)])
 
 
 class State(C.Structure):
@@ -135,6 +145,9 @@ def lib():
     L.stgn_engine_stage_nbr_update.argtypes = [vp, i32, P(StageEntries), vp, i32, dbl,
                                                P(StageRecords), vp]
     L.stgn_engine_stage_commit.argtypes = [vp, i32, vp, vp, vp, vp, vp, i64, vp]
+    L.stgn_dysat_batch.argtypes = [P(DySAT), i32, vp, vp, C.c_uint32, vp, vp, vp]
+    L.stgn_dysat_recompute_all.argtypes = [P(DySAT), vp]
+    L.stgn_dysat_roll.argtypes = [P(DySAT), vp]
     L.stgn_engine_affected.argtypes = [vp, vp, vp, i64, P(i64), P(i64), vp, vp]
     L.stgn_engine_pred_embeddings.argtypes = [vp, vp, i64, vp]
     L.stgn_pipeline_many.argtypes = [P(Dims), i64, i64] + [vp] * 18

@@ -18,6 +18,7 @@
 #include "delta.cuh"
 #include "snapshot.cuh"
 #include "stage.cuh"
+#include "dysat.cuh"
 
 #ifndef STGN_DRIFT_FORK
 #define STGN_DRIFT_FORK 1  // drift estimators + decision on a branch beside the recompute
@@ -1223,6 +1224,80 @@ extern "C" int stgn_engine_stage_commit(stgn_engine* e, int32_t P, const int32_t
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(st));
   return STGN_OK;
+}
+
+// ---- DySAT (csrc/dysat.cuh) -------------------------------------------------
+static bool dy_valid(const stgn_dysat* s) {
+  return s && s->n > 0 && s->d > 0 && s->heads_s > 0 && s->heads_s <= 32 && s->heads_t > 0 &&
+         s->d % s->heads_s == 0 && s->d % s->heads_t == 0 && s->window >= 1 && s->window <= 32 &&
+         s->fanout >= 1 && s->fanout <= 31 && s->ld >= s->d && s->ld % 4 == 0 &&
+         s->snapshot >= 0 && s->snapshot < s->pos_len && s->chunk > 0 && s->max_batch > 0 &&
+         s->P && s->ss && s->sn && s->lst_nbr && s->lst_head && s->lst_cnt && s->hist_k &&
+         s->hist_v && s->emb && s->mark && s->work && s->rows && s->pos && s->wq && s->wk &&
+         s->wv && s->wo && s->wpred;
+}
+
+static int dy_temporal(const stgn_dysat* s, const int32_t* list, const int32_t* count_ptr,
+                       int64_t count_const, int64_t base, int64_t max_rows, cudaStream_t st) {
+  const int wsm = 8192;
+  const int T = dy_tile_rows(s->d, wsm);
+  if (T < 4) return STGN_ERR_INVALID;
+  const size_t smem = (size_t)(5 * T * s->d + wsm) * sizeof(float);
+  CUDA_TRY(cudaFuncSetAttribute((const void*)k_dy_temporal,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 148;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(cdiv(max_rows, T), 4 * sms));
+  k_dy_temporal<<<(int)grid, DY_THREADS, smem, st>>>(*s, list, count_ptr, count_const, base, T, wsm);
+  CUDA_TRY(cudaGetLastError());
+  return STGN_OK;
+}
+
+extern "C" int stgn_dysat_batch(const stgn_dysat* s, int32_t B, const int32_t* src_dev,
+                                const int32_t* dst_dev, uint32_t stamp, double* preds_dev,
+                                int32_t* n_affected, void* stream) {
+  if (!dy_valid(s) || B < 0 || (B > 0 && (!src_dev || !dst_dev || !preds_dev)))
+    return STGN_ERR_INVALID;
+  if (B > s->max_batch) return STGN_ERR_CAPACITY;
+  if (n_affected) *n_affected = 0;
+  if (B == 0) return STGN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t* cnt = s->work + 2 * s->max_batch;
+  k_dy_predict<<<(int)cdiv(B, 8), 256, 0, st>>>(*s, B, src_dev, dst_dev, preds_dev);
+  CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int32_t), st));
+  k_dy_claim<<<(int)cdiv(2 * B, 256), 256, 0, st>>>(*s, B, src_dev, dst_dev, stamp);
+  k_dy_lists<<<(int)cdiv(2 * B, 8), 256, 0, st>>>(*s, B, src_dev, dst_dev);
+  k_dy_struct<<<(int)cdiv(2 * B, DY_THREADS / 32), DY_THREADS, 0, st>>>(*s, s->work, cnt, 0, 0);
+  CUDA_TRY(cudaGetLastError());
+  int rc = dy_temporal(s, s->work, cnt, 0, 0, 2 * (int64_t)B, st);
+  if (rc) return rc;
+  if (n_affected) {
+    CUDA_TRY(cudaMemcpyAsync(n_affected, cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  return STGN_OK;
+}
+
+extern "C" int stgn_dysat_recompute_all(const stgn_dysat* s, void* stream) {
+  if (!dy_valid(s)) return STGN_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int64_t lo = 0; lo < s->n; lo += s->chunk) {
+    const int64_t c = std::min<int64_t>(s->chunk, s->n - lo);
+    k_dy_struct<<<(int)cdiv(c, DY_THREADS / 32), DY_THREADS, 0, st>>>(*s, nullptr, nullptr, c, lo);
+    CUDA_TRY(cudaGetLastError());
+    int rc = dy_temporal(s, nullptr, nullptr, c, lo, c, st);
+    if (rc) return rc;
+  }
+  return STGN_OK;
+}
+
+extern "C" int stgn_dysat_roll(const stgn_dysat* s, void* stream) {
+  if (!dy_valid(s)) return STGN_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(s->lst_cnt, 0, sizeof(int32_t) * s->n, st));
+  CUDA_TRY(cudaMemsetAsync(s->lst_head, 0, sizeof(int32_t) * s->n, st));
+  return stgn_dysat_recompute_all(s, stream);
 }
 
 extern "C" int stgn_engine_full_reference(stgn_engine* e, int64_t node_count, float* out_dev,
