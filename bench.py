@@ -67,7 +67,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-batches", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--config-legs", default="C1,C2,C3",
+    ap.add_argument("--config-legs", default="C1,C2,C3,C5",
                     help="other BASELINE.json configs to run after the C4 legs ('' = none)")
     ap.add_argument("--c3-edges", type=int, default=30_000_000)
     ap.add_argument("--latency-steps", type=int, default=1000,
@@ -311,7 +311,7 @@ def config_legs(args, torch, dev):
     from paper_2603_21090_b200.params import init_params, memoryless
     from paper_2603_21090_b200.streamio import generate_stream
     out = {}
-    for name in [c for c in args.config_legs.split(",") if c]:
+    for name in [c for c in args.config_legs.split(",") if c and c != "C5"]:
         c = CONFIGS[name]
         m = c["edges"] or args.c3_edges
         dims = Dims(d_s=100, d_e=c["d_e"], d_t=100, d_x=0, d_m=100, d_k=50, heads=2,
@@ -380,6 +380,78 @@ def config_legs(args, torch, dev):
         del feed, eng, st
         torch.cuda.empty_cache()
     return out
+
+
+def dysat_leg(torch, dev, n=1_000_000, m=3_000_000, B=600, snapshots=10):
+    """configs[4]: DySAT incremental inference on a 1M-node synthetic snapshot stream vs full
+    recompute (paper_2603_21090_b200/dysat.py; the reference has no DySAT code, so there is no
+    reference number and parity is pinned only to oracle/dysat_oracle.py). The whole stream is
+    fed from HBM in B-edge batches split at snapshot boundaries, one CUDA event per batch; a
+    batch that crosses a boundary includes the O(|V|) roll (every node recomputed)."""
+    from paper_2603_21090_b200.dysat import DySATConfig, DySATEngine, init_dysat_params
+    from paper_2603_21090_b200.streamio import generate_stream
+    st = generate_stream(5, n, m, attachment="preferential", d_e=0)
+    span = float(st.t[-1]) + 1.0
+    cfg = DySATConfig(n=n, d_in=64, d=128, heads_s=16, heads_t=16, window=8, fanout=20,
+                      snapshot_len=span / snapshots, max_snapshots=snapshots + 2, batch_size=B)
+    eng = DySATEngine(cfg, init_dysat_params(0, cfg))
+    src = torch.from_numpy(st.src.astype(np.int32)).to(dev)
+    dst = torch.from_numpy(st.dst.astype(np.int32)).to(dev)
+    snap = np.floor(st.t / cfg.snapshot_len).astype(np.int64)
+    segs = []   # (lo, hi, snapshot) batches of at most B edges inside one snapshot
+    lo = 0
+    while lo < m:
+        hi = min(lo + B, m)
+        k = int(snap[lo])
+        hi = lo + int(np.searchsorted(snap[lo:hi], k, side="right"))
+        segs.append((lo, hi, k))
+        lo = hi
+    stream = torch.cuda.current_stream(dev)
+    for lo, hi, k in segs[:3]:   # warm-up (snapshot 0 batches; re-run below from a fresh engine)
+        eng.process_batch_device(src[lo:hi], dst[lo:hi], float(st.t[hi - 1]), k)
+    torch.cuda.synchronize()
+    del eng
+    eng = DySATEngine(cfg, init_dysat_params(0, cfg))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(segs) + 1)]
+    rolls = []
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    for q, (lo, hi, k) in enumerate(segs):
+        if k > eng.snapshot:
+            rolls.append(q)
+        eng.process_batch_device(src[lo:hi], dst[lo:hi], float(st.t[hi - 1]), k)
+        ev[q + 1].record(stream)
+    torch.cuda.synchronize()
+    per = np.array([ev[q].elapsed_time(ev[q + 1]) for q in range(len(segs))])
+    total = float(ev[0].elapsed_time(ev[-1]))
+    plain = np.delete(per, rolls)
+    full = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.full_recompute()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        full.append(e0.elapsed_time(e1))
+    full_ms = float(np.median(full))
+    p50 = float(np.percentile(plain, 50))
+    # HBM bytes of one full recompute (dysat.cuh header): per node, L list ids + the gathered
+    # P rows of its list (the snapshot's lists are empty after the last roll: self only),
+    # 2 (W-1) history rows read, 2 history rows + 1 embedding row written, + its own P row
+    d4 = 4 * eng.ld
+    fb = n * (d4 + 2 * (cfg.window - 1) * d4 + 3 * d4 + 4 * cfg.fanout)
+    return {"workload": "DySAT (1 structural layer, 16 heads; 1 temporal layer, 16 heads, window "
+                        "8; d = 128, node features 64, L = 20) on a synthetic preferential "
+                        f"stream, {n:,} nodes, {m:,} edges, {snapshots} snapshots, B = {B}",
+            "value": m / (total / 1e3), "unit": UNIT, "batches": len(segs),
+            "p50_ms": p50, "p99_ms": float(np.percentile(plain, 99)),
+            "roll_ms_mean": float(np.mean(per[rolls])) if rolls else None, "rolls": len(rolls),
+            "full_recompute_ms": full_ms, "full_recompute_hbm_gbs": fb / (full_ms / 1e3) / 1e9,
+            "speedup_vs_full_recompute": full_ms / p50,
+            "affected_per_batch": "the batch endpoints (one structural layer on static features)",
+            "parity": "oracle/dysat_oracle.py (tests/test_gpu_dysat.py); unpinned vs the "
+                      "reference, which ships no DySAT code",
+            "cpu_reference": None}
 
 
 def operator_leg(torch, dev, N=10_000, E_per=10, reps=20):
@@ -729,6 +801,8 @@ def run_ours(args, world, rank, local_rank):
     # 5) the other configs of BASELINE.json (C1, C2 full streams; C3 TGAT at the C4 scale)
     cfg_legs = config_legs(args, torch, dev) if (args.config_legs and rank == 0) else None
     op_leg = operator_leg(torch, dev) if (args.config_legs and rank == 0) else None
+    dy_leg = (dysat_leg(torch, dev) if (rank == 0 and "C5" in args.config_legs.split(","))
+              else None)
 
     line = None
     if rank == 0:
@@ -771,6 +845,7 @@ def run_ours(args, world, rank, local_rank):
             "sweep": sweep_out,
             "configs": cfg_legs,
             "operator_pipeline_many": op_leg,
+            "dysat": dy_leg,
             "full_rebuild": rb,
             # the paper's "index refresh" comparison: one full recompute of
             # every node (the TGL-style / OracleEngine baseline) vs one incremental batch

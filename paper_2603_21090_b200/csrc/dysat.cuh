@@ -103,14 +103,25 @@ k_dy_struct(stgn_dysat s, const int32_t* list, const int32_t* count_ptr, int64_t
     const bool live = lane <= E;
     const int u = lane == 0 ? v : (live ? s.lst_nbr[(int64_t)v * L + (s.lst_head[v] + lane - 1) % L] : v);
     s_u[w][lane] = u;
-    for (int h = 0; h < Hs; ++h) {
-      float e = s.ss[(int64_t)v * Hs + h] + s.sn[(int64_t)u * Hs + h];
-      e = e > 0.f ? e : 0.2f * e;
-      float mx = live ? e : -INFINITY;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      const float p = live ? __expf(e - mx) : 0.f;
-      s_alpha[w][h * 32 + lane] = p / warp_sum(p);
+    __syncwarp();
+    // lane = head: softmax over [self] + list sequentially in the lane (no shuffles)
+    for (int h = lane; h < Hs; h += 32) {
+      const float sv = s.ss[(int64_t)v * Hs + h];
+      float mx = -INFINITY;
+      for (int j = 0; j <= E; ++j) {
+        float e = sv + s.sn[(int64_t)s_u[w][j] * Hs + h];
+        e = e > 0.f ? e : 0.2f * e;
+        s_alpha[w][h * 32 + j] = e;
+        mx = fmaxf(mx, e);
+      }
+      float z = 0.f;
+      for (int j = 0; j <= E; ++j) {
+        const float p = __expf(s_alpha[w][h * 32 + j] - mx);
+        s_alpha[w][h * 32 + j] = p;
+        z += p;
+      }
+      const float inv = 1.f / z;
+      for (int j = 0; j <= E; ++j) s_alpha[w][h * 32 + j] *= inv;
     }
     __syncwarp();
     float* out = s.rows + i * s.ld;
@@ -175,6 +186,50 @@ k_dy_temporal(stgn_dysat s, const int32_t* list, const int32_t* count_ptr, int64
       s.hist_k[hr] = Kc[r4(i, c, d)];
       s.hist_v[hr] = Vc[r4(i, c, d)];
     }
+    // fast path: lane owns CH = d / 32 consecutive elements; a head spans
+    // dt / CH lanes (a power of two), so a logit is a segmented shuffle sum
+    const int CH = d >> 5;
+    const int lph = (d % 32 == 0 && CH <= 8 && dt % CH == 0) ? dt / CH : 0;
+    const bool fast = lph > 0 && lph <= 32 && (lph & (lph - 1)) == 0;
+    if (fast) {
+      for (int i = warp; i < T; i += blockDim.x >> 5) {
+        const int v = s_node[i];
+        if (v < 0) continue;
+        const int c0 = lane * CH;
+        float q[8], o[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          q[x] = x < CH ? Q[r4(i, c0 + x, d)] * scale : 0.f;
+          o[x] = 0.f;
+        }
+        float mx = -INFINITY, z = 0.f;
+        for (int p = 0; p < np; ++p) {  // online softmax over the window
+          const int64_t j = j0 + p;
+          const float* kr = s.hist_k + ((int64_t)v * W + (int)(j % W)) * s.ld + c0;
+          const float* vr = s.hist_v + ((int64_t)v * W + (int)(j % W)) * s.ld + c0;
+          float part = 0.f, vv[8];
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {
+            if (x < CH) {
+              const float kx = j == k ? Kc[r4(i, c0 + x, d)] : kr[x];
+              vv[x] = j == k ? Vc[r4(i, c0 + x, d)] : vr[x];
+              part = fmaf(q[x], kx, part);
+            }
+          }
+          for (int m = 1; m < lph; m <<= 1) part += __shfl_xor_sync(0xffffffffu, part, m);
+          const float nm = fmaxf(mx, part);
+          const float sc = __expf(mx - nm), pe = __expf(part - nm);
+          z = fmaf(z, sc, pe);
+#pragma unroll
+          for (int x = 0; x < 8; ++x) o[x] = fmaf(pe, vv[x], o[x] * sc);
+          mx = nm;
+        }
+        const float inv = 1.f / z;
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+          if (x < CH) O[r4(i, c0 + x, d)] = o[x] * inv;
+      }
+    } else
     for (int i = warp; i < T; i += blockDim.x >> 5) {
       const int v = s_node[i];
       if (v < 0) continue;
