@@ -402,6 +402,9 @@ typedef struct {
   const float *wq, *wk, *wv, *wo;  /* [d][ld] */
   const double* wpred;   /* [2 d] */
   double bpred;
+  const uint16_t* wtc;   /* nullable: [4][2 d d] W_q^T, W_k^T, W_v^T, W_o^T as K-major bf16
+                            hi | lo blocks (tcgen05 B operands; d = 64 or 128) */
+  int64_t tc_min_rows;   /* launches of at least this many rows use the tcgen05 kernel */
 } stgn_dysat;
 
 /* One snapshot segment of B edges (device int32 ids, all of snapshot

@@ -90,7 +90,7 @@ class DySAT(C.Structure):
                 [(n, C.c_void_p) for n in ("P", "ss", "sn", "lst_nbr", "lst_head", "lst_cnt",
                                            "hist_k", "hist_v", "emb", "mark", "work", "rows",
                                            "pos", "wq", "wk", "wv", "wo", "wpred")] +
-                [("bpred", C.c_double)])
+                [("bpred", C.c_double), ("wtc", C.c_void_p), ("tc_min_rows", C.c_int64)])
 
 
 class State(C.Structure):

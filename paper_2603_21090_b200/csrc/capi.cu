@@ -1239,6 +1239,26 @@ static bool dy_valid(const stgn_dysat* s) {
 
 static int dy_temporal(const stgn_dysat* s, const int32_t* list, const int32_t* count_ptr,
                        int64_t count_const, int64_t base, int64_t max_rows, cudaStream_t st) {
+  // tcgen05 bf16x3 GEMMs for large row counts (snapshot rolls, full recomputes); a
+  // batch's ~2B rows fill only a few 128-row tiles, where the 16-row FFMA tiles
+  // spread over more SMs and finish sooner
+  if (s->wtc && dy_tc_ok(s->d, s->heads_t) && s->ld == s->d && max_rows >= s->tc_min_rows) {
+    const int dt = s->d / s->heads_t;
+    using KFn = void (*)(stgn_dysat, const int32_t*, const int32_t*, int64_t, int64_t);
+    KFn fn = s->d == 128 ? (dt == 8 ? k_dy_temporal_tc<32, 8> : dt == 16 ? k_dy_temporal_tc<32, 16>
+                                                                          : k_dy_temporal_tc<32, 32>)
+                         : (dt == 8 ? k_dy_temporal_tc<16, 8> : k_dy_temporal_tc<16, 16>);
+    const size_t smem = dy_tc_smem(s->d);
+    CUDA_TRY(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    int dev = 0, sms = 148;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(cdiv(max_rows, 128), sms));
+    fn<<<(int)grid, DTC_THREADS, smem, st>>>(*s, list, count_ptr, count_const, base);
+    CUDA_TRY(cudaGetLastError());
+    return STGN_OK;
+  }
   const int wsm = 8192;
   const int T = dy_tile_rows(s->d, wsm);
   if (T < 4) return STGN_ERR_INVALID;

@@ -19,6 +19,7 @@
 #pragma once
 
 #include "gemm.cuh"
+#include "attn4.cuh"
 
 #define DY_TMAX 32
 #define DY_THREADS 256
@@ -282,4 +283,231 @@ k_dy_temporal(stgn_dysat s, const int32_t* list, const int32_t* count_ptr, int64
     }
     __syncthreads();
   }
+}
+
+// ---- tcgen05 temporal layer (d = 4 CW, CW in {16, 32}; head width DT <= CW) ----
+// 128-row tiles, 512 threads = 4 TMEM lane quadrants x 4 column groups; thread
+// (quadrant q, group cg, lane) owns row 32q + lane and columns [cg CW, (cg+1) CW),
+// so every head lies inside one thread (softmax over the window without shuffles).
+// bf16x3 GEMMs (hi*hi + hi*lo + lo*hi, fp32 accumulate) with y / o as the TMEM A
+// operand and W^T (K-major bf16 hi | lo blocks, stgn_dysat.wtc) staged by TMA bulk
+// copies into two shared buffers, two blocks ahead (blocks Q, K, V, O per tile).
+// TMEM: A [0, d)  D_Q [d, 2d)  D_K [2d, 3d)  D_V [3d, 4d); D_E reuses D_Q.
+#define DTC_THREADS 512
+
+static inline bool dy_tc_ok(int d, int heads_t) {
+  const int dt = d / heads_t;
+  return (d == 64 || d == 128) && (dt == 8 || dt == 16 || dt == 32) && dt <= d / 4;
+}
+static inline size_t dy_tc_smem(int d) { return 1024 + 2 * (size_t)(2 * d * d * 2); }
+
+template <int CW, int DT>
+__global__ void __launch_bounds__(DTC_THREADS, 1)
+k_dy_temporal_tc(stgn_dysat s, const int32_t* list, const int32_t* count_ptr, int64_t count_const,
+                 int64_t base) {
+  constexpr int d = 4 * CW;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sbase = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  constexpr uint32_t blk_bytes = (uint32_t)(2 * d * d * 2);
+  uint16_t* Wb0 = reinterpret_cast<uint16_t*>(sbase);
+  uint16_t* Wb1 = reinterpret_cast<uint16_t*>(sbase + blk_bytes);
+  __shared__ int s_node[128];
+  __shared__ uint64_t mbar, wbar[2];
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int quad = warp & 3, cg = warp >> 2;
+  const int64_t N = count_ptr ? (int64_t)*count_ptr : count_const;
+  const int64_t ntiles = cdiv(N, 128);
+  if ((int64_t)blockIdx.x >= ntiles) return;
+  const int64_t total_blocks = cdiv(ntiles - blockIdx.x, (int64_t)gridDim.x) * 4;
+  if (warp == 0) tmem_alloc(&tslot, 512);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    mbar_init(&wbar[0], 1);
+    mbar_init(&wbar[1], 1);
+    mbar_fence_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const uint32_t trow = tmem + ((uint32_t)(32 * quad) << 16);
+  const int row = 32 * quad + lane;
+  auto stage = [&](int64_t Gi) {  // one thread: weight block Gi % 4 -> buffer Gi & 1
+    bulk_stage((Gi & 1) ? (void*)Wb1 : (void*)Wb0, s.wtc + (Gi % 4) * (int64_t)(2 * d * d),
+               blk_bytes, &wbar[Gi & 1]);
+  };
+  if (tid == 0) {
+    stage(0);
+    if (total_blocks > 1) stage(1);
+  }
+  int64_t G = 0;
+  uint32_t mph = 0;
+  auto cta_sync_tc = [&]() {
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  };
+  auto issue = [&](int off, int dcol, bool commit) {  // tid 0: block G + off, A = TMEM [0, d)
+    const int64_t Gi = G + off;
+    mbar_wait(&wbar[Gi & 1], (uint32_t)((Gi >> 1) & 1));
+    a4_mma(tmem, 0, (Gi & 1) ? Wb1 : Wb0, d, d, dcol, &mbar, false, commit);
+  };
+  auto wait_mma = [&](int nb) {  // the one commit covering the next nb blocks; refill
+    if (tid == 0) {
+      mbar_wait(&mbar, mph & 1u);
+      for (int k = 0; k < nb; ++k)
+        if (G + k + 2 < total_blocks) stage(G + k + 2);
+    }
+    ++mph;
+    G += nb;
+    cta_sync_tc();
+  };
+  const int64_t k = s.snapshot;
+  const int W = s.window;
+  const int slot = (int)(k % W);
+  const int64_t j0 = k - W + 1 > 0 ? k - W + 1 : 0;
+  const int np = (int)(k - j0 + 1);
+  const float scale = rsqrtf((float)DT);
+  const int c0 = cg * CW;  // this thread's columns [c0, c0 + CW)
+  constexpr int DQ = d, DK = 2 * d, DV = 3 * d;
+  const float* pr = s.pos + k * s.ld + c0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t tb = tile * 128;
+    if (tid < 128) s_node[tid] = tb + tid < N ? (list ? list[tb + tid] : (int)(base + tb + tid)) : -1;
+    __syncthreads();
+    const int v = s_node[row];
+    const float* yr = s.rows + (tb + row) * s.ld + c0;
+    // ---- A = y = z + pos (bf16 hi | lo), this thread's CW / 16 blocks of 16 columns ----
+#pragma unroll
+    for (int b = 0; b < CW / 16; ++b) {
+      float x[16];
+#pragma unroll
+      for (int t = 0; t < 16; t += 4) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (v >= 0) {
+          const float4 r4v = *reinterpret_cast<const float4*>(yr + 16 * b + t);
+          const float4 p4v = __ldg(reinterpret_cast<const float4*>(pr + 16 * b + t));
+          a = make_float4(r4v.x + p4v.x, r4v.y + p4v.y, r4v.z + p4v.z, r4v.w + p4v.w);
+        }
+        x[t] = a.x; x[t + 1] = a.y; x[t + 2] = a.z; x[t + 3] = a.w;
+      }
+      const int blk = c0 / 16 + b;
+      a4_st16(trow + (uint32_t)(8 * blk), trow + (uint32_t)(d / 2 + 8 * blk), x);
+    }
+    tmem_st_wait();
+    cta_sync_tc();
+    if (tid == 0) {
+      issue(0, DQ, false);
+      issue(1, DK, true);
+    }
+    wait_mma(2);
+    if (tid == 0) issue(0, DV, true);
+    wait_mma(1);
+    // ---- this snapshot's key / value rows -> the node's history slot ----
+    float* hk = s.hist_k + ((int64_t)(v >= 0 ? v : 0) * W + slot) * s.ld + c0;
+    float* hv = s.hist_v + ((int64_t)(v >= 0 ? v : 0) * W + slot) * s.ld + c0;
+#pragma unroll
+    for (int x8 = 0; x8 < CW / 8; ++x8) {  // warp-collective TMEM loads; stores guarded
+      float a8[8], b8[8];
+      tmem_ld8_nw(trow + (uint32_t)(DK + c0 + 8 * x8), a8);
+      tmem_ld8_nw(trow + (uint32_t)(DV + c0 + 8 * x8), b8);
+      tmem_ld_wait();
+      if (v >= 0) {
+        reinterpret_cast<float4*>(hk + 8 * x8)[0] = make_float4(a8[0], a8[1], a8[2], a8[3]);
+        reinterpret_cast<float4*>(hk + 8 * x8)[1] = make_float4(a8[4], a8[5], a8[6], a8[7]);
+        reinterpret_cast<float4*>(hv + 8 * x8)[0] = make_float4(b8[0], b8[1], b8[2], b8[3]);
+        reinterpret_cast<float4*>(hv + 8 * x8)[1] = make_float4(b8[4], b8[5], b8[6], b8[7]);
+      }
+    }
+    float q[CW], o[CW];
+#pragma unroll
+    for (int x8 = 0; x8 < CW / 8; ++x8) {
+      float t8[8];
+      tmem_ld8_nw(trow + (uint32_t)(DQ + c0 + 8 * x8), t8);
+      tmem_ld_wait();
+#pragma unroll
+      for (int t = 0; t < 8; ++t) q[8 * x8 + t] = t8[t] * scale;
+    }
+#pragma unroll
+    for (int c = 0; c < CW; ++c) o[c] = 0.f;
+    if (v >= 0) {
+      // online softmax over the window, all of this thread's heads at once; the
+      // current snapshot's rows are read back from the slot just written
+      float mx[CW / DT], z[CW / DT];
+#pragma unroll
+      for (int h = 0; h < CW / DT; ++h) {
+        mx[h] = -INFINITY;
+        z[h] = 0.f;
+      }
+      for (int p = 0; p < np; ++p) {
+        const int64_t j = j0 + p;
+        const float* kr = s.hist_k + ((int64_t)v * W + (int)(j % W)) * s.ld + c0;
+        const float* vr = s.hist_v + ((int64_t)v * W + (int)(j % W)) * s.ld + c0;
+#pragma unroll
+        for (int h = 0; h < CW / DT; ++h) {
+          float lg = 0.f;
+#pragma unroll
+          for (int c = 0; c < DT; c += 4) {
+            const float4 k4 = *reinterpret_cast<const float4*>(kr + h * DT + c);
+            lg = fmaf(q[h * DT + c], k4.x, lg);
+            lg = fmaf(q[h * DT + c + 1], k4.y, lg);
+            lg = fmaf(q[h * DT + c + 2], k4.z, lg);
+            lg = fmaf(q[h * DT + c + 3], k4.w, lg);
+          }
+          const float nm = fmaxf(mx[h], lg);
+          const float sc = __expf(mx[h] - nm), pe = __expf(lg - nm);
+          z[h] = fmaf(z[h], sc, pe);
+#pragma unroll
+          for (int c = 0; c < DT; c += 4) {
+            const float4 v4 = *reinterpret_cast<const float4*>(vr + h * DT + c);
+            o[h * DT + c] = fmaf(pe, v4.x, o[h * DT + c] * sc);
+            o[h * DT + c + 1] = fmaf(pe, v4.y, o[h * DT + c + 1] * sc);
+            o[h * DT + c + 2] = fmaf(pe, v4.z, o[h * DT + c + 2] * sc);
+            o[h * DT + c + 3] = fmaf(pe, v4.w, o[h * DT + c + 3] * sc);
+          }
+          mx[h] = nm;
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < CW / DT; ++h) {
+        const float inv = 1.f / z[h];
+#pragma unroll
+        for (int c = 0; c < DT; ++c) o[h * DT + c] *= inv;
+      }
+    }
+    // ---- A = o, D_E = o W_O (over D_Q) ----
+#pragma unroll
+    for (int b = 0; b < CW / 16; ++b) {
+      float x[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) x[t] = o[16 * b + t];
+      const int blk = c0 / 16 + b;
+      a4_st16(trow + (uint32_t)(8 * blk), trow + (uint32_t)(d / 2 + 8 * blk), x);
+    }
+    tmem_st_wait();
+    cta_sync_tc();
+    if (tid == 0) issue(0, DQ, true);
+    wait_mma(1);
+    float* er = s.emb + (int64_t)(v >= 0 ? v : 0) * s.ld + c0;
+#pragma unroll
+    for (int x8 = 0; x8 < CW / 8; ++x8) {  // warp-collective TMEM loads; stores guarded
+      float t8[8];
+      tmem_ld8_nw(trow + (uint32_t)(DQ + c0 + 8 * x8), t8);
+      tmem_ld_wait();
+      if (v >= 0) {  // emb = o W_O + y, y re-read (L2)
+        const int cc = 8 * x8;
+        const float4 ra = *reinterpret_cast<const float4*>(yr + cc);
+        const float4 rb = *reinterpret_cast<const float4*>(yr + cc + 4);
+        const float4 pa = __ldg(reinterpret_cast<const float4*>(pr + cc));
+        const float4 pb = __ldg(reinterpret_cast<const float4*>(pr + cc + 4));
+        reinterpret_cast<float4*>(er + cc)[0] = make_float4(
+            t8[0] + (ra.x + pa.x), t8[1] + (ra.y + pa.y), t8[2] + (ra.z + pa.z), t8[3] + (ra.w + pa.w));
+        reinterpret_cast<float4*>(er + cc)[1] = make_float4(
+            t8[4] + (rb.x + pb.x), t8[5] + (rb.y + pb.y), t8[6] + (rb.z + pb.z), t8[7] + (rb.w + pb.w));
+      }
+    }
+    cta_sync_tc();
+  }
+  if (warp == 0) tmem_free(tmem, 512);
 }

@@ -100,6 +100,21 @@ def init_dysat_params(seed: int, cfg: DySATConfig) -> DySATParams:
         b_pred=float(rng.standard_normal()))
 
 
+def _kmajor_bf16(B):
+    """(N, K) float64 -> (2 N K,) uint16 viewed as int16: the K-major tcgen05 B
+    operand (8x8 core matrices), hi block then lo block (engine._pack_kmajor_bf16)."""
+    from .engine import _bf16_float, _bf16_rne
+    N, K = B.shape
+    hi = _bf16_rne(B)
+    lo = _bf16_rne(B - _bf16_float(hi))
+    n, k = np.meshgrid(np.arange(N), np.arange(K), indexing="ij")
+    idx = (((n // 8) * (K // 8) + k // 8) * 64 + (n % 8) * 8 + k % 8).ravel()
+    out = np.zeros((2, N * K), dtype=np.uint16)
+    out[0, idx] = hi.ravel()
+    out[1, idx] = lo.ravel()
+    return out.reshape(-1).view(np.int16)
+
+
 def _torch():
     import torch
     if not torch.cuda.is_available():
@@ -115,7 +130,8 @@ class DySATEngine:
     node recomputed). full_recompute() recomputes every node in place (the
     baseline the incremental path is measured against)."""
 
-    def __init__(self, cfg: DySATConfig, params: DySATParams, device=None):
+    def __init__(self, cfg: DySATConfig, params: DySATParams, device=None,
+                 tensor_cores: bool = True, tc_min_rows: int = 64 * 128):
         cfg.validate()
         torch = self._torch = _torch()
         self.cfg, self.params = cfg, params
@@ -141,6 +157,15 @@ class DySATEngine:
         self.wq, self.wk = f32(params.w_q, d, ld), f32(params.w_k, d, ld)
         self.wv, self.wo = f32(params.w_v, d, ld), f32(params.w_o, d, ld)
         self.wpred = torch.from_numpy(np.asarray(params.w_pred, dtype=np.float64)).to(dev)
+        # tcgen05 B operands of the temporal GEMMs (d = 64 / 128): W^T as K-major bf16
+        # hi | lo blocks (csrc/dysat.cuh k_dy_temporal_tc); None -> the FFMA kernel
+        dt = d // cfg.heads_t
+        self.tensor_cores = tensor_cores and d in (64, 128) and dt in (8, 16, 32) and dt <= d // 4
+        self.tc_min_rows = int(tc_min_rows)
+        self.wtc = (torch.from_numpy(np.stack([_kmajor_bf16(np.asarray(w, np.float64).T)
+                                               for w in (params.w_q, params.w_k, params.w_v,
+                                                         params.w_o)])).to(dev)
+                    if self.tensor_cores else None)
         i32 = torch.int32
         self.lst_nbr = torch.zeros((n, cfg.fanout), dtype=i32, device=dev)
         self.lst_head = torch.zeros(n, dtype=i32, device=dev)
@@ -178,6 +203,9 @@ class DySATEngine:
                      "mark", "work", "rows", "pos", "wq", "wk", "wv", "wo", "wpred"):
             setattr(s, name, getattr(self, name).data_ptr())
         s.bpred = float(self.params.b_pred)
+        s.wtc = self.wtc.data_ptr() if self.wtc is not None else None
+        # a batch's ~2B rows fill few 128-row tiles: below this the 16-row FFMA tiles win
+        s.tc_min_rows = self.tc_min_rows
 
     # -- batches ----------------------------------------------------------------
     def _roll_to(self, k):

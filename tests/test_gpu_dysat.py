@@ -20,6 +20,10 @@ def cuda():
 
 
 CASES = {
+    "tc_d128": dict(n=300, d_in=16, d=128, heads_s=16, heads_t=16, window=4, fanout=8,
+                    snapshot_len=40.0, max_snapshots=256, batch_size=50),
+    "tc_d64": dict(n=200, d_in=10, d=64, heads_s=4, heads_t=4, window=3, fanout=6,
+                   snapshot_len=25.0, max_snapshots=256, batch_size=40),
     "small": dict(n=60, d_in=12, d=32, heads_s=4, heads_t=2, window=3, fanout=5,
                   snapshot_len=12.0, max_snapshots=256, batch_size=16),
     "wide_heads": dict(n=50, d_in=20, d=64, heads_s=16, heads_t=8, window=1, fanout=31,
@@ -30,14 +34,17 @@ CASES = {
 
 
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_dysat_matches_oracle(cuda, name):
+@pytest.mark.parametrize("tc", [True, False])
+def test_dysat_matches_oracle(cuda, name, tc):
     from oracle.dysat_oracle import DySATOracle
     from paper_2603_21090_b200.dysat import DySATConfig, DySATEngine, init_dysat_params
     from paper_2603_21090_b200.streamio import generate_stream
     cfg = DySATConfig(**CASES[name])
     params = init_dysat_params(3, cfg)
     st = generate_stream(7, cfg.n, 300, d_e=0, attachment="preferential")
-    eng = DySATEngine(cfg, params)
+    eng = DySATEngine(cfg, params, tensor_cores=tc, tc_min_rows=1)  # every launch on tcgen05
+    dt = cfg.d // cfg.heads_t
+    assert eng.tensor_cores == (tc and cfg.d in (64, 128) and dt in (8, 16, 32) and dt <= cfg.d // 4)
     orc = DySATOracle(cfg, params)
     assert np.allclose(eng.embeddings(), orc.emb, rtol=1e-4, atol=1e-4)
     B = cfg.batch_size
