@@ -21,4 +21,10 @@ timeout 900 ncu --set full --clock-control none --import-source on --profile-fro
    -o $O/$TAG.attn4 -f python tools/prof_run.py --batches 3 > $O/$TAG.attn4.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:mem4_kernel -s 1 -c 1 \
    -o $O/$TAG.mem4 -f python tools/prof_run.py --edges 120000 --batches 3 > $O/$TAG.mem4.log 2>&1
+# DySAT (C5): launch list with DRAM bytes / FMA-pipe activity, and one full capture of the
+# tcgen05 temporal kernel (a full recompute)
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active \
+   --clock-control none -k regex:k_dy --csv --log-file $O/$TAG.dysat_launches.csv python tools/dysat_probe.py > $O/$TAG.dysat_launches.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_dy_temporal_tc -s 2 -c 1 \
+   -o $O/$TAG.dysat_tc -f python tools/dysat_probe.py > $O/$TAG.dysat_tc.log 2>&1
 tail -3 $O/$TAG.pytest.log; tail -1 $O/$TAG.smoke.log; tail -c 600 $O/$TAG.bench.json; tail -3 $O/$TAG.bench.err; tail -c 300 $O/$TAG.ref.json
