@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <utility>
+#include <mutex>
 #include <vector>
 
 #include "batch.cuh"
@@ -1421,8 +1422,23 @@ extern "C" int stgn_pipeline_many(const stgn_dims* dims, int64_t N, int64_t E, c
   if (rc) return rc;
   const int64_t nq = (int64_t)g.K * g.H * g.q_in * g.d_k;
   const int64_t nk = (int64_t)g.K * g.H * g.k_in * g.d_k;
-  float* packed = nullptr;
-  CUDA_TRY(cudaMallocAsync((void**)&packed, sizeof(float) * (nq + 2 * nk), st));
+  // packed weights in a grow-only per-device buffer: no allocation per call (an
+  // allocation per call made the call time depend on the memory pool's state)
+  static std::mutex pack_mu;
+  static float* pack_buf[64] = {};
+  static size_t pack_cap[64] = {};
+  std::lock_guard<std::mutex> lock(pack_mu);
+  const size_t need = sizeof(float) * (size_t)(nq + 2 * nk);
+  if (dev < 0 || dev >= 64) return STGN_ERR_INVALID;
+  if (need > pack_cap[dev]) {
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (pack_buf[dev]) CUDA_TRY(cudaFree(pack_buf[dev]));
+    pack_buf[dev] = nullptr;
+    pack_cap[dev] = 0;
+    CUDA_TRY(cudaMalloc((void**)&pack_buf[dev], need));
+    pack_cap[dev] = need;
+  }
+  float* packed = pack_buf[dev];
   k_pack_attn<<<256, 256, 0, st>>>(g, wq, wk, wv, packed, packed + nq, packed + nq + nk);
   AttnWeights aw;
   aw.wq = packed;
@@ -1449,8 +1465,7 @@ extern "C" int stgn_pipeline_many(const stgn_dims* dims, int64_t N, int64_t E, c
   const int grid = (int)std::min<int64_t>(cdiv(N, al.T), al.grid);
   al.fn<<<grid, STGN_THREADS, al.smem, st>>>(g, aw, rs, fs, al.T);
   CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaFreeAsync(packed, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaStreamSynchronize(st));  // the shared packed buffer is reused by the next call
   return STGN_OK;
 }
 
