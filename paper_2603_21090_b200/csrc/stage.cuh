@@ -59,6 +59,7 @@ __global__ void k_stage_affected(Geo g, StateView st, const int32_t* __restrict_
     hop_off[0] = 0;
     hop_off[1] = f1;
   }
+  if (f1 > cap) f1 = (int)cap;
   for (int hop = 1; hop <= g.K; ++hop) {
     const int64_t total = (int64_t)(f1 - f0) * g.L;
     for (int64_t x = threadIdx.x; x < total; x += blockDim.x) {
@@ -82,7 +83,9 @@ __global__ void k_stage_affected(Geo g, StateView st, const int32_t* __restrict_
     __syncthreads();
     f0 = f1;
     f1 = nA;
-    if (threadIdx.x == 0) hop_off[hop + 1] = f1;
+    if (threadIdx.x == 0) hop_off[hop + 1] = f1;  // > cap: the host reports STGN_ERR_CAPACITY
+    if (f1 > cap) f1 = (int)cap;                  // never read past the list
+    if (f0 > f1) f0 = f1;
     __syncthreads();
   }
 }

@@ -209,7 +209,13 @@ class DySATEngine:
 
     # -- batches ----------------------------------------------------------------
     def _roll_to(self, k):
-        """Advance to snapshot k (each boundary recomputes every node)."""
+        """Advance to snapshot k (each boundary recomputes every node). Only the
+        last W snapshots are ever read, so a gap longer than the window starts
+        rolling at k - W (the skipped snapshots have empty lists either way)."""
+        if k >= self.cfg.max_snapshots:
+            raise ConfigError("snapshot index beyond max_snapshots")
+        if k - self.snapshot > self.cfg.window:
+            self.snapshot = k - self.cfg.window
         while self.snapshot < k:
             self.snapshot += 1
             if self.snapshot >= self.cfg.max_snapshots:

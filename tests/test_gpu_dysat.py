@@ -80,6 +80,28 @@ def test_dysat_full_recompute_equals_incremental(cuda):
     np.testing.assert_array_equal(eng.embeddings(), before)
 
 
+def test_dysat_gap_longer_than_window(cuda):
+    """Snapshots without edges between batches, some gaps longer than W."""
+    from oracle.dysat_oracle import DySATOracle
+    from paper_2603_21090_b200.dysat import DySATConfig, DySATEngine, init_dysat_params
+    cfg = DySATConfig(**CASES["small"])   # W = 3, snapshot_len = 12
+    p = init_dysat_params(4, cfg)
+    eng, orc = DySATEngine(cfg, p), DySATOracle(cfg, p)
+    rng = np.random.default_rng(0)
+    t0 = 0.0
+    for gap in (0.0, 13.0, 60.0, 5.0, 200.0, 24.0):
+        t0 += gap
+        s, d = rng.integers(0, cfg.n, 8), rng.integers(0, cfg.n, 8)
+        t = t0 + np.sort(rng.uniform(0, 3, 8))
+        a = eng.process_batch_arrays(s, d, t)
+        b = orc.process_batch(s, d, t)
+        np.testing.assert_allclose(a, b, atol=1e-5)
+        t0 = float(t[-1])
+        e, r = eng.embeddings(), orc.emb
+        assert np.max(np.abs(e - r) / (1.0 + np.abs(r))) < 1e-4
+    assert eng.snapshot == orc.snapshot
+
+
 def test_dysat_rejects_bad_input(cuda):
     from paper_2603_21090_b200.config import ConfigError
     from paper_2603_21090_b200.dysat import DySATConfig, DySATEngine, init_dysat_params
