@@ -121,6 +121,12 @@ __device__ __forceinline__ unsigned long long a4_now() {
 #ifndef A4_PFD
 #define A4_PFD 32
 #endif
+#ifndef A4_HW
+#define A4_HW 0  // walk 1 with the event loop: two rows per warp, a half-warp per row
+#endif
+#if A4_HW && A4_EC != 2
+#error "A4_HW reuses the stage size of A4_EC = 2 (one entry of two rows per stage)"
+#endif
 
 
 struct A4W {
@@ -716,6 +722,197 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   }
 }
 
+// Walk of two rows per warp (A4_HW): lanes 0-15 walk this warp's first row,
+// lanes 16-31 its second (node < 0 / E = 0 for an idle half). Math as
+// a4_walk_row with 16 lanes per row: lane hl of a half owns key features
+// [8 hl, 8 hl + 8) of the payload, of the edge features and of the time
+// encoding (frequencies 4 hl .. 4 hl + 3). One entry of each row per stage
+// (the stage of two A4_EC = 2 chunks); the loop runs to the longer row, the
+// other half's extra entries are zero-filled with logit -inf. Per entry one
+// 16-lane transposing reduction serves both heads of both rows.
+template <int KF>
+__device__ __forceinline__ void a4_walk_half(const Geo& g, const A4W& w, const RingSrc& rs,
+                                             float* U, int node, int E, int hd, double tref,
+                                             int l, int lane, float4* stg) {
+  constexpr int NSEG = KF ? 3 : 2;
+  constexpr int NST = A4_NST;
+  const int hl = lane & 15, hf = lane >> 4;
+  const int kfo = w.kfo, kto = w.kto, kp = w.kpad;
+  const bool valid = node >= 0;  // a row with no entries still gets ubar = 0 written
+  if (!valid) {
+    node = 0;
+    E = 0;
+  }
+  const int nf4p = kfo / 4, nf4f = (kto - kfo) / 4, nf4t = (kp - kto) / 4;
+  const bool lp0 = 2 * hl < nf4p, lp1 = 2 * hl + 1 < nf4p;
+  const bool lf0 = KF && 2 * hl < nf4f, lf1 = KF && 2 * hl + 1 < nf4f;
+  const bool lt0 = 2 * hl < nf4t, lt1 = 2 * hl + 1 < nf4t;
+  const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  // rotation by w tref, frequencies 4 hl + i
+  float ca[4], sa[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    ca[i] = 1.f;
+    sa[i] = 0.f;
+    const int f = 4 * hl + i;
+    if (E > 0 && f < g.half) phase_sincos(__ldg(w.omega + f), tref, &sa[i], &ca[i]);
+  }
+  float4 qp[2][2], qf[2][2], qt[2][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float* Uh = U + h * kp;
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      const bool vp = x ? lp1 : lp0, vf = x ? lf1 : lf0, vt = x ? lt1 : lt0;
+      qp[h][x] = vp ? *reinterpret_cast<const float4*>(Uh + 8 * hl + 4 * x) : zero4;
+      qf[h][x] = vf ? *reinterpret_cast<const float4*>(Uh + kfo + 8 * hl + 4 * x) : zero4;
+      const float4 q = vt ? *reinterpret_cast<const float4*>(Uh + kto + 8 * hl + 4 * x) : zero4;
+      const float c0 = ca[2 * x], s0 = sa[2 * x], c1 = ca[2 * x + 1], s1 = sa[2 * x + 1];
+      qt[h][x] = make_float4(q.x * c0 + q.y * s0, q.x * s0 - q.y * c0, q.z * c1 + q.w * s1,
+                             q.z * s1 - q.w * c1);
+    }
+  }
+  float2 up[2][4], uf[2][4], ut[2][4];
+  float mx[2] = {-INFINITY, -INFINITY}, zs[2] = {0.f, 0.f};
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) up[h][c] = uf[h][c] = ut[h][c] = make_float2(0.f, 0.f);
+  const float* payb = rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d + 8 * hl;
+  const float* ftb = rs.ring_feat + (int64_t)node * g.L * g.ld_e + 8 * hl;
+  const float* tbb = rs.ring_tb + (int64_t)node * g.L * g.ld_t + 8 * hl;
+#if A4_HINTS
+  const uint64_t pol_pay = pol_evict_first();
+  const uint64_t pol_tb = l + 1 < g.K ? pol_evict_last() : pol_evict_first();
+#endif
+  const int nent = max(E, __shfl_xor_sync(0xffffffffu, E, 16));  // warp-uniform trip count
+  int iss_slot = 0, con_slot = 0;
+  int r_slot = hd;
+  const float* r_pay = payb + (int64_t)hd * g.ld_d;
+  const float* r_tb = tbb + (int64_t)hd * g.ld_t;
+  const float* r_ft = ftb + (int64_t)hd * g.ld_e;
+  auto issue = [&](int e) {
+    if (e < nent) {
+      float4* sb = stg + iss_slot * (NSEG * 64) + hf * 32 + 2 * hl;
+      const bool ev = e < E;
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int pb = (ev && (x ? lp1 : lp0)) ? 16 : 0, tb = (ev && (x ? lt1 : lt0)) ? 16 : 0;
+#if A4_HINTS
+        cp_async16_pol(sb + x, r_pay + 4 * x, pb, pol_pay);
+        cp_async16_pol(sb + 64 + x, r_tb + 4 * x, tb, pol_tb);
+#else
+        cp_async16(sb + x, r_pay + 4 * x, pb);
+        cp_async16(sb + 64 + x, r_tb + 4 * x, tb);
+#endif
+        if (KF) cp_async16(sb + 128 + x, r_ft + 4 * x, (ev && (x ? lf1 : lf0)) ? 16 : 0);
+      }
+      if (++r_slot == g.L) {
+        r_slot = 0;
+        r_pay = payb;
+        r_tb = tbb;
+        r_ft = ftb;
+      } else {
+        r_pay += g.ld_d;
+        r_tb += g.ld_t;
+        r_ft += g.ld_e;
+      }
+    }
+    cp_async_commit();
+    if (++iss_slot == NST) iss_slot = 0;
+  };
+#pragma unroll
+  for (int c = 0; c < NST - 1; ++c) issue(c);
+  for (int e = 0; e < nent; ++e) {
+    const int slot_c = con_slot;
+    if (++con_slot == NST) con_slot = 0;
+    issue(e + NST - 1);
+    cp_async_wait<NST - 1>();
+    const float4* sb = stg + slot_c * (NSEG * 64) + hf * 32 + 2 * hl;
+    float4 kpv[2], ktv[2], kfv[2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      kpv[x] = sb[x];
+      ktv[x] = sb[64 + x];
+      kfv[x] = KF ? sb[128 + x] : zero4;
+    }
+    float part[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float2 a = fmul2(make_float2(qp[h][0].x, qp[h][0].y), make_float2(kpv[0].x, kpv[0].y));
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        if (x) a = ffma2(make_float2(qp[h][1].x, qp[h][1].y), make_float2(kpv[1].x, kpv[1].y), a);
+        a = ffma2(make_float2(qp[h][x].z, qp[h][x].w), make_float2(kpv[x].z, kpv[x].w), a);
+        a = ffma2(make_float2(qt[h][x].x, qt[h][x].y), make_float2(ktv[x].x, ktv[x].y), a);
+        a = ffma2(make_float2(qt[h][x].z, qt[h][x].w), make_float2(ktv[x].z, ktv[x].w), a);
+        if (KF) {
+          a = ffma2(make_float2(qf[h][x].x, qf[h][x].y), make_float2(kfv[x].x, kfv[x].y), a);
+          a = ffma2(make_float2(qf[h][x].z, qf[h][x].w), make_float2(kfv[x].z, kfv[x].w), a);
+        }
+      }
+      part[h] = a.x + a.y;
+    }
+    // 16-lane transposing reduction: head 0 ends on lanes hl < 8, head 1 on hl >= 8
+    const bool b3 = hl & 8;
+    float v = (b3 ? part[1] : part[0]) + __shfl_xor_sync(0xffffffffu, b3 ? part[0] : part[1], 8);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    float lg[2];
+    lg[0] = __shfl_sync(0xffffffffu, v, hf * 16);
+    lg[1] = __shfl_sync(0xffffffffu, v, hf * 16 + 8);
+    if (e >= E) lg[0] = lg[1] = -INFINITY;  // this half's row has no entry e: weight 0
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float nm = fmaxf(mx[h], lg[h]);
+      // an idle half keeps nm = -inf: the exponents below are then NaN-free by the selects
+      const float sc = nm == -INFINITY ? 1.f : ex2f(mx[h] - nm);
+      const float p = nm == -INFINITY ? 0.f : ex2f(lg[h] - nm);
+      const float2 sc2 = make_float2(sc, sc), p2 = make_float2(p, p);
+      zs[h] = fmaf(zs[h], sc, p);
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        up[h][2 * x] = ffma2(p2, make_float2(kpv[x].x, kpv[x].y), fmul2(up[h][2 * x], sc2));
+        up[h][2 * x + 1] = ffma2(p2, make_float2(kpv[x].z, kpv[x].w), fmul2(up[h][2 * x + 1], sc2));
+        ut[h][2 * x] = ffma2(p2, make_float2(ktv[x].x, ktv[x].y), fmul2(ut[h][2 * x], sc2));
+        ut[h][2 * x + 1] = ffma2(p2, make_float2(ktv[x].z, ktv[x].w), fmul2(ut[h][2 * x + 1], sc2));
+        if (KF) {
+          uf[h][2 * x] = ffma2(p2, make_float2(kfv[x].x, kfv[x].y), fmul2(uf[h][2 * x], sc2));
+          uf[h][2 * x + 1] = ffma2(p2, make_float2(kfv[x].z, kfv[x].w), fmul2(uf[h][2 * x + 1], sc2));
+        }
+      }
+      mx[h] = nm;
+    }
+  }
+  __syncwarp();
+  if (!valid) return;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float* Uh = U + h * kp;
+    const float inv = E > 0 ? 1.f / zs[h] : 0.f;
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      if (x ? lp1 : lp0)
+        *reinterpret_cast<float4*>(Uh + 8 * hl + 4 * x) =
+            make_float4(up[h][2 * x].x * inv, up[h][2 * x].y * inv, up[h][2 * x + 1].x * inv,
+                        up[h][2 * x + 1].y * inv);
+      if (x ? lf1 : lf0)
+        *reinterpret_cast<float4*>(Uh + kfo + 8 * hl + 4 * x) =
+            make_float4(uf[h][2 * x].x * inv, uf[h][2 * x].y * inv, uf[h][2 * x + 1].x * inv,
+                        uf[h][2 * x + 1].y * inv);
+      if (x ? lt1 : lt0) {
+        const float uc0 = ut[h][2 * x].x * inv, us0 = ut[h][2 * x].y * inv;
+        const float uc1 = ut[h][2 * x + 1].x * inv, us1 = ut[h][2 * x + 1].y * inv;
+        const float c0 = ca[2 * x], s0 = sa[2 * x], c1 = ca[2 * x + 1], s1 = sa[2 * x + 1];
+        *reinterpret_cast<float4*>(Uh + kto + 8 * hl + 4 * x) =
+            make_float4(c0 * uc0 + s0 * us0, s0 * uc0 - c0 * us0, c1 * uc1 + s1 * us1,
+                        s1 * uc1 - c1 * us1);
+      }
+    }
+  }
+}
+
 // Walk 2: the rows of one 32-row quadrant, warp per row, taken from a shared
 // counter. Ring rows reach shared memory as TMA bulk copies: one lane issues
 // a chunk of A4_EC2 entries (payload, time basis and features of consecutive
@@ -1297,6 +1494,19 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
           while (!mbar_test(&qbar_full[b], uphase(q))) duties();
           for (;;) {
             int i = 0;
+#if A4_HW
+            if (lane == 0) i = atomicAdd(&qctr[b], 2);  // two rows, a half-warp each
+            i = __shfl_sync(0xffffffffu, i, 0);
+            if (i >= nrows) break;
+            {
+              const int ih = i + (lane >> 4);
+              const int r = 32 * q + ih;
+              const bool ok = ih < nrows;
+              a4_walk_half<KF>(g, w, rs, Ub + (ok ? ih : i) * w.ldu, ok ? s_node[r] : -1,
+                               ok ? s_E[r] : 0, ok ? s_head[r] : 0, ok ? s_tref[r] : 0.0, l, lane,
+                               stg_warp);
+            }
+#else
             if (lane == 0) i = atomicAdd(&qctr[b], 1);
             i = __shfl_sync(0xffffffffu, i, 0);
             if (i >= nrows) break;
@@ -1304,6 +1514,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
             if (s_node[r] >= 0)
               a4_walk_row<KF>(g, w, rs, Ub + i * w.ldu, s_node[r], s_E[r], s_head[r], s_tref[r],
                               l, lane, stg_warp, [] {}, nullptr);
+#endif
             duties();
           }
           mbar_arrive(&qbar_done[b]);
