@@ -74,8 +74,16 @@ __device__ __forceinline__ unsigned long long a4_now() {
 #ifndef A4_NUB
 #define A4_NUB 2  // quadrant row buffers (2: the next quadrant's q~ copy overlaps the walk)
 #endif
+#ifndef A4_CPK
+#define A4_CPK 0  // walk 1: compact stages (an entry's segments back to back, kpad/4 float4s,
+                  // instead of 32 float4 slots per segment), so four stages fit the buffers
+#endif
 #ifndef A4_NST
+#if A4_CPK
+#define A4_NST 4
+#else
 #define A4_NST 3  // cp.async stages (chunks in flight) per warp in the walk
+#endif
 #endif
 #ifndef A4_STATIC
 #define A4_STATIC 0  // static row assignment with one cp.async stream across rows and quadrants
@@ -102,6 +110,12 @@ __device__ __forceinline__ unsigned long long a4_now() {
 #define A4_VOF 0  // out = sum_h ubar_h (W_V,h W_O,h): the V GEMMs, the c pack and the O GEMM fold
                   // into two passes of two MMA blocks over the TMEM ubar operands
 #endif
+#ifndef A4_ISS
+#define A4_ISS 0  // walk 1: every lane copies 16 bytes of every entry from an address that is
+                  // always valid (lanes past a segment re-read the row's first 16 bytes, entries
+                  // past E the row's last entry; their weights are 0 and their q~ lanes 0), so
+                  // the issue has no per-copy size predicates; slot = hd + e with one wrap
+#endif
 #ifndef A4_RUNPTR
 #define A4_RUNPTR 1  // walk 1: running source pointers for the cp.async issue
 #endif
@@ -123,6 +137,12 @@ __device__ __forceinline__ unsigned long long a4_now() {
 #endif
 #ifndef A4_HW
 #define A4_HW 0  // walk 1 with the event loop: two rows per warp, a half-warp per row
+#endif
+#if A4_ISS && (A4_CPK || A4_HW || A4_STATIC || A4_WALK != 1 || !A4_HINTS || A4_TRIG)
+#error "A4_ISS is an issue order of walk 1 (a4_walk_row)"
+#endif
+#if A4_CPK && (A4_HW || A4_STATIC || A4_WALK != 1 || !A4_RUNPTR || !A4_HINTS || A4_TRIG)
+#error "A4_CPK is a layout of walk 1's per-warp stages (a4_walk_row)"
 #endif
 #if A4_HW && A4_EC != 2
 #error "A4_HW reuses the stage size of A4_EC = 2 (one entry of two rows per stage)"
@@ -174,6 +194,8 @@ static inline bool a4_plan(const Geo& g, A4W* w) {
 #if A4_WALK == 2
   // two chunk stages per warp: [A4_EC2][ld_d] payload, [A4_EC2][ld_t] basis, [A4_EC2][ld_e] features
   const int stage_bytes = A4_WARPS * 2 * A4_EC2 * (g.ld_d + g.ld_t + (g.d_e > 0 ? g.ld_e : 0)) * 4;
+#elif A4_CPK
+  const int stage_bytes = A4_WARPS * A4_NST * A4_EC * (w->kpad / 4) * 16;
 #else
   const int stage_bytes = A4_WARPS * A4_NST * A4_EC * (g.d_e > 0 ? 3 : 2) * 32 * 16;  // (TRIG: basis segment unused)
 #endif
@@ -534,13 +556,60 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   const float* r_tb = tbb + (int64_t)hd * g.ld_t;
   const float* r_ft = ftb + (int64_t)hd * g.ld_e;
 #endif
+#if A4_ISS
+  const float* i_pay = rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d + (lp ? 4 * lane : 0);
+  const float* i_tb = rs.ring_tb + (int64_t)node * g.L * g.ld_t + (lt ? 4 * lane : 0);
+  const float* i_ft = rs.ring_feat + (int64_t)node * g.L * g.ld_e + (lf ? 4 * lane : 0);
+#endif
+#if A4_CPK
+  // compact stage: entry u of a chunk at float4 u*SE: payload [0, kfo/4), features
+  // [kfo/4, kto/4), time basis [kto/4, kpad/4); lanes past a segment copy nothing
+  const int SE = kp / 4, o_f = kfo / 4, o_t = kto / 4;
+#endif
   auto issue = [&](int c) {
+#ifdef A4_XNOLOAD  // timing experiment only (results wrong): no ring-row copies
+    if (false) {
+#else
     if (c < nch) {
+#endif
+#if A4_CPK
+      float4* sb = stg + iss_slot * (EC * SE) + lane;
+#else
       float4* sb = stg + iss_slot * (EC * NSEG * 32) + lane;
+#endif
 #pragma unroll
       for (int u = 0; u < EC; ++u) {
         const int e = c * EC + u;
         const bool ev = e < E;
+#if A4_ISS
+        {
+          int slot = hd + (ev ? e : E - 1);
+          if (slot >= g.L) slot -= g.L;
+          cp_async16_pol(sb + (u * NSEG) * 32, i_pay + slot * g.ld_d, 16, pol_pay);
+          cp_async16_pol(sb + (u * NSEG + 1) * 32, i_tb + slot * g.ld_t, 16, pol_tb);
+          if (KF) cp_async16(sb + (u * NSEG + 2) * 32, i_ft + slot * g.ld_e, 16);
+          continue;
+        }
+#endif
+#if A4_CPK
+        {
+          const int nb = ev ? 16 : 0;  // entries past E: zero-filled (weight 0, no NaN)
+          if (lp) cp_async16_pol(sb + u * SE, r_pay, nb, pol_pay);
+          if (lt) cp_async16_pol(sb + u * SE + o_t, r_tb, nb, pol_tb);
+          if (KF && lf) cp_async16(sb + u * SE + o_f, r_ft, nb);
+          if (++r_slot == g.L) {
+            r_slot = 0;
+            r_pay = payb;
+            r_tb = tbb;
+            r_ft = ftb;
+          } else {
+            r_pay += g.ld_d;
+            r_tb += g.ld_t;
+            r_ft += g.ld_e;
+          }
+          continue;
+        }
+#endif
 #if A4_RUNPTR
         const int pay_bytes = (ev && lp) ? 16 : 0, tb_bytes = (ev && lt) ? 16 : 0;
 #if A4_HINTS
@@ -595,6 +664,18 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
     }
     cp_async_wait<NST - 1>();  // chunk c has landed (this lane's own copies)
     float4 kp[EC], kf[EC], kt[EC];
+#if A4_CPK
+    {
+      const float4* sb = stg + slot_c * (EC * SE) + lane;
+#pragma unroll
+      for (int u = 0; u < EC; ++u) {
+        kp[u] = lp ? sb[u * SE] : zero4;
+        kt[u] = lt ? sb[u * SE + o_t] : zero4;
+        kf[u] = (KF && lf) ? sb[u * SE + o_f] : zero4;
+      }
+    }
+    if (false)
+#endif
     {
       const float4* sb = stg + slot_c * (EC * NSEG * 32) + lane;
 #pragma unroll
@@ -613,6 +694,15 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
         kf[u] = KF ? sb[(u * NSEG + 2) * 32] : zero4;
       }
     }
+#ifdef A4_XNOMATH  // timing experiment only (results wrong): loads and waits, no softmax math
+#pragma unroll
+    for (int u = 0; u < EC; ++u) {
+      up[0][0] = ffma2(make_float2(1.f, 1.f), make_float2(kp[u].x, kp[u].y), up[0][0]);
+      ut[0][0] = ffma2(make_float2(1.f, 1.f), make_float2(kt[u].x, kt[u].y), ut[0][0]);
+    }
+    zs[0] = zs[1] = 1.f;
+    continue;
+#endif
     // per-lane partial logits, value index v = 2u + h
     float part[2 * EC];
 #pragma unroll
@@ -1216,7 +1306,11 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
   }
   // the walk's per-warp cp.async stages live in the two weight buffers: V_0 and
   // V_1 (blocks 3, 4 of a layer) are staged after the walk instead of during it
+#if A4_CPK
+  float4* stg_warp = reinterpret_cast<float4*>(sbase) + (size_t)warp * A4_NST * A4_EC * (w.kpad / 4);
+#else
   float4* stg_warp = reinterpret_cast<float4*>(sbase) + (size_t)warp * A4_NST * A4_EC * (KF ? 3 : 2) * 32;
+#endif
 #if A4_WALK == 2
   A4Stg S2;
   S2.stg_floats = A4_EC2 * (g.ld_d + g.ld_t + (KF ? g.ld_e : 0));

@@ -63,14 +63,20 @@ __device__ __forceinline__ bool rec_is_adj(const Scratch& s, int r) {
   return !(r & 1) || (s.in_src[r >> 1] != s.in_dst[r >> 1]);
 }
 
+#ifndef STGN_REC_HASH
+#define STGN_REC_HASH 0  // k_records_w32: the direct set as a shared-memory hash table
+#endif
+#ifndef STGN_HOP_TICKET
+#define STGN_HOP_TICKET 0  // k_hop's last block writes hop_off[hop + 1]: no k_hop_fin launch
+#endif
+
 #define GRID_STRIDE(i, n) \
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
 // Reset per-batch results; derive t_batch (the last edge's timestamp,
 // S/engine.py:415) and the window cutoff on the device.
-__global__ void k_begin(Scratch s, double window) {
-  PDL_WAIT();
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
+__device__ __forceinline__ void begin_body(const Scratch& s, double window) {
+  {
     BatchHdr* hd = s.hdr;
     hd->t_batch = s.in_t[hd->B - 1];
     hd->cutoff = isfinite(window) ? hd->t_batch - window : -INFINITY;
@@ -86,20 +92,25 @@ __global__ void k_begin(Scratch s, double window) {
     r->rb_partial_n = 0;
     r->rb_full_n = 0;
     r->ticket = 0;
+    r->hop_ticket = 0;
     r->nC = r->n_skip = r->n_hit = r->n_miss = 0;
     r->E_miss = 0;
   }
+}
+__global__ void k_begin(Scratch s, double window) {
+  PDL_WAIT();
+  if (threadIdx.x == 0 && blockIdx.x == 0) begin_body(s, window);
 }
 
 // Records r = 2i + side (side 0: owner src, side 1: owner dst). First
 // toucher of a node claims its direct-set slot; counts per node; the
 // side-0 record also appends the edge to the temporal store.
-__global__ void k_claim(Geo g, StateView st, Scratch s) {
-  PDL_WAIT();
+__device__ __forceinline__ void claim_body(const Geo& g, const StateView& st, const Scratch& s,
+                                           int64_t i0, int64_t stride) {
   const BatchHdr* hd = s.hdr;
   const int64_t B = hd->B;
   const uint32_t stamp = hd->stamp;
-  GRID_STRIDE(r, 2 * B) {
+  for (int64_t r = i0; r < 2 * B; r += stride) {
     const int rr = (int)r;
     const int node = rec_node(s, rr);
     if (atomicExch(&st.dmark[node], stamp) != stamp) {
@@ -120,11 +131,14 @@ __global__ void k_claim(Geo g, StateView st, Scratch s) {
     }
   }
 }
+__global__ void k_claim(Geo g, StateView st, Scratch s) {
+  PDL_WAIT();
+  claim_body(g, st, s, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+}
 
 // One block: exclusive scan of per-direct-node record counts; per-node
 // offsets; remembers each direct node's pre-batch cache state.
-__global__ void k_scan(Geo g, StateView st, Scratch s) {
-  PDL_WAIT();
+__device__ __forceinline__ void scan_body(const Geo& g, const StateView& st, const Scratch& s) {
   __shared__ int32_t warp_tot[32];
   __shared__ int32_t carry;
   const int nD = s.res->nD;
@@ -176,24 +190,32 @@ __global__ void k_scan(Geo g, StateView st, Scratch s) {
     s.res->hop_off[1] = nD;
   }
 }
-
-__global__ void k_place(StateView st, Scratch s) {
+__global__ void k_scan(Geo g, StateView st, Scratch s) {
   PDL_WAIT();
+  scan_body(g, st, s);
+}
+
+__device__ __forceinline__ void place_body(const StateView& st, const Scratch& s, int64_t i0,
+                                           int64_t stride) {
   const int64_t B = s.hdr->B;
-  GRID_STRIDE(r, 2 * B) {
+  for (int64_t r = i0; r < 2 * B; r += stride) {
     const int node = rec_node(s, (int)r);
     const int slot = atomicAdd(&st.nodefill[node], 1);
     s.rec_u[st.nodeoff[node] + slot] = (int)r;
   }
 }
+__global__ void k_place(StateView st, Scratch s) {
+  PDL_WAIT();
+  place_body(st, s, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+}
 
 // Rank each record inside its node's segment (segments are small: one
 // entry per incident batch edge), giving message order (ascending r) and
 // the newest-first adjacency rank.
-__global__ void k_rank(StateView st, Scratch s) {
-  PDL_WAIT();
+__device__ __forceinline__ void rank_body(const StateView& st, const Scratch& s, int64_t i0,
+                                          int64_t stride) {
   const int64_t B = s.hdr->B;
-  GRID_STRIDE(r64, 2 * B) {
+  for (int64_t r64 = i0; r64 < 2 * B; r64 += stride) {
     const int r = (int)r64;
     const int node = rec_node(s, r);
     const int off = st.nodeoff[node];
@@ -213,6 +235,27 @@ __global__ void k_rank(StateView st, Scratch s) {
     s.rec_adjrank[r] = adj ? arank : -1;
     s.rec_prev[r] = prev;
   }
+}
+__global__ void k_rank(StateView st, Scratch s) {
+  PDL_WAIT();
+  rank_body(st, s, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+}
+
+// The five ingest steps above in one block, for batches of at most INGEST1_MAX_B
+// edges: the kernel boundaries between them (each a few microseconds of launch
+// and drain for ~1K records) become block barriers. Same bodies, same results.
+#define INGEST1_MAX_B 2048
+__global__ void __launch_bounds__(1024) k_ingest1(Geo g, StateView st, Scratch s, double window) {
+  PDL_WAIT();
+  if (threadIdx.x == 0) begin_body(s, window);
+  __syncthreads();
+  claim_body(g, st, s, threadIdx.x, blockDim.x);
+  __syncthreads();
+  scan_body(g, st, s);
+  __syncthreads();
+  place_body(st, s, threadIdx.x, blockDim.x);
+  __syncthreads();
+  rank_body(st, s, threadIdx.x, blockDim.x);
 }
 
 __device__ __forceinline__ int64_t entry_index(int64_t m0, int r) {
@@ -364,6 +407,18 @@ __global__ void k_hop(Geo g, StateView st, Scratch s, int hop) {
       if (fresh) s.alist[basepos + __popc(mask & lanemask_lt())] = u;
     }
   }
+#if STGN_HOP_TICKET
+  // the last block to finish publishes the hop boundary (k_hop_fin's job)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&s.res->hop_ticket, 1u) == gridDim.x - 1) {
+      __threadfence();
+      s.res->hop_off[hop + 1] = atomicAdd(&s.res->nA, 0);
+      s.res->hop_ticket = 0;
+    }
+  }
+#endif
 }
 
 __global__ void k_hop_fin(Scratch s, int hop) {
@@ -511,6 +566,135 @@ __global__ void k_records_warp(Geo g, StateView st, Scratch s, int finite_window
       st.ring_ccnt[v] = len;
       if (was_cached) ++hit; else ++miss;
       if (size > 0 && len > 0) ++changed;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    hit += __shfl_xor_sync(0xffffffffu, hit, o);
+    miss += __shfl_xor_sync(0xffffffffu, miss, o);
+    changed += __shfl_xor_sync(0xffffffffu, changed, o);
+  }
+  if (lane == 0) {
+    if (hit) atomicAdd(&s.res->nbr_hit, hit);
+    if (miss) atomicAdd(&s.res->nbr_miss, miss);
+    if (changed) atomicAdd(&s.res->changed, changed);
+  }
+}
+
+// k_records_warp with 32 nodes per warp: lane k loads node k's header (one
+// coalesced alist load, independent per-lane header loads), then floor(32/L)
+// nodes per round in L-lane segments take their list entries; the rounds only
+// load (ring ids, direct marks) and shuffle, so unrolled rounds overlap their
+// loads, and each lane writes its own node's record once at the end.
+// The direct set (nD <= REC_HASH_SLOTS / 2 nodes) is looked up in a shared-memory
+// hash table built by every block, instead of st.dmark: the marks of random
+// neighbours are scattered 4-byte reads of a |V|-sized table (DRAM sectors).
+#define REC_HASH_SLOTS 8192
+__device__ __forceinline__ uint32_t rec_hash(int u) { return ((uint32_t)u * 2654435761u) >> 19; }
+__global__ void k_records_w32(Geo g, StateView st, Scratch s, int finite_window) {
+  PDL_WAIT();
+  const int nA = s.res->nA, nD = s.res->nD;
+  const uint32_t stamp = s.hdr->stamp;
+  __shared__ int dset[REC_HASH_SLOTS];
+  const bool use_hash = STGN_REC_HASH && nD <= REC_HASH_SLOTS / 2;
+  if (use_hash) {
+    for (int i = threadIdx.x; i < REC_HASH_SLOTS; i += blockDim.x) dset[i] = -1;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nD; i += blockDim.x) {
+      const int key = s.alist[i];
+      uint32_t h = rec_hash(key);
+      while (atomicCAS(&dset[h], -1, key) != -1) h = (h + 1) & (REC_HASH_SLOTS - 1);
+    }
+    __syncthreads();
+  }
+  auto is_direct = [&](int u) {
+    if (!use_hash) return st.dmark[u] == stamp;
+    uint32_t h = rec_hash(u);
+    for (;;) {
+      const int k = dset[h];
+      if (k == u) return true;
+      if (k < 0) return false;
+      h = (h + 1) & (REC_HASH_SLOTS - 1);
+    }
+  };
+  const double cutoff = s.hdr->cutoff;
+  const int lane = threadIdx.x & 31;
+  const int S = 32 / g.L;
+  const int seg = lane / g.L, sl = lane - seg * g.L;
+  const bool seg_live = seg < S;
+  const unsigned seg_mask = seg_live ? (((1u << g.L) - 1u) << (seg * g.L)) : 0u;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int rounds = (32 + S - 1) / S;
+  unsigned long long hit = 0, miss = 0, changed = 0;
+  for (int64_t b0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; b0 < nA;
+       b0 += warps * 32) {
+    // this lane's node: header
+    const int a_l = (int)b0 + lane;
+    const bool live_l = a_l < nA;
+    int v_l = 0, added_l = 0, expired_l = 0, len_l = 0, wc_l = 0, head_l = 0;
+    if (live_l) {
+      v_l = s.alist[a_l];
+      if (a_l < nD) {
+        const int kadj = st.nodeadj[v_l];
+        wc_l = s.d_wascached[a_l];
+        const int merged = kadj + s.d_baselen[a_l];
+        len_l = merged < g.L ? merged : g.L;
+        expired_l = wc_l ? (merged > g.L ? merged - g.L : 0) : 0;
+        added_l = kadj;
+      } else {
+        const int cc = st.ring_ccnt[v_l];
+        wc_l = cc >= 0;
+        len_l = wc_l ? cc : st.ring_cnt[v_l];
+      }
+      head_l = st.ring_head[v_l];
+    }
+    int out_upd = 0, out_len = len_l;  // this lane's node: results gathered from its segment
+#pragma unroll 4
+    for (int rr = 0; rr < rounds; ++rr) {
+      const int k = rr * S + seg;  // node (lane index) of this segment in this round
+      const int ks = (seg_live && k < 32) ? k : 0;
+      const int v = __shfl_sync(0xffffffffu, v_l, ks);
+      int len = __shfl_sync(0xffffffffu, len_l, ks);
+      const int added = __shfl_sync(0xffffffffu, added_l, ks);
+      const int head = __shfl_sync(0xffffffffu, head_l, ks);
+      const bool live = seg_live && k < 32 && (int)b0 + k < nA;
+      int n_new = added < len ? added : len;
+      int slot = live ? head + sl : 0;
+      if (slot >= g.L) slot -= g.L;
+      const int64_t rs = (int64_t)v * g.L + slot;
+      const bool in_list = live && sl < len;
+      if (finite_window) {
+        const unsigned old = (__ballot_sync(0xffffffffu, in_list && st.ring_t[rs] < cutoff) & seg_mask) >>
+                             (seg_live ? seg * g.L : 0);
+        const int keep = old ? __ffs(old) - 1 : len;
+        len = keep;
+        if (n_new > len) n_new = len;
+      }
+      const bool cand = live && sl >= n_new && sl < len;
+      const int u = cand ? st.ring_nbr[rs] : -1;
+      const bool dir = cand && is_direct(u);
+      const unsigned long long key = cand ? (((unsigned long long)(unsigned)u << 8) | (unsigned)seg)
+                                          : (0xFFFFFFFF00000000ull | (unsigned)lane);
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const bool first = (__ffs(peers) - 1) == lane;
+      const int upd = __popc(__ballot_sync(0xffffffffu, dir && first) & seg_mask);
+      // node k = rr*S + j was handled by segment j (lane j*L): its owner lane takes the values
+      const int j = lane - rr * S;
+      const int src = (j >= 0 && j < S) ? j * g.L : 0;
+      const int upd_k = __shfl_sync(0xffffffffu, upd, src);
+      const int len_k = __shfl_sync(0xffffffffu, len, src);
+      if (j >= 0 && j < S) {
+        out_upd = upd_k;
+        out_len = len_k;
+      }
+    }
+    if (live_l) {
+      const int expired = expired_l + (finite_window ? len_l - out_len : 0);
+      const int size = added_l + expired + out_upd;
+      s.a_size[a_l] = size;
+      s.a_len[a_l] = out_len;
+      st.ring_ccnt[v_l] = out_len;
+      if (wc_l) ++hit; else ++miss;
+      if (size > 0 && out_len > 0) ++changed;
     }
   }
   for (int o = 16; o > 0; o >>= 1) {

@@ -24,6 +24,12 @@
 #ifndef STGN_DRIFT_FORK
 #define STGN_DRIFT_FORK 1  // drift estimators + decision on a branch beside the recompute
 #endif
+#ifndef STGN_REC32
+#define STGN_REC32 0  // change records: k_records_w32 (32 nodes per warp) instead of k_records_warp
+#endif
+#ifndef STGN_INGEST1
+#define STGN_INGEST1 0  // batches of <= INGEST1_MAX_B edges: the five ingest kernels as one block
+#endif
 #ifndef STGN_LATE_RECORDS
 #define STGN_LATE_RECORDS 0
 #endif
@@ -545,7 +551,13 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   const bool late_records = STGN_LATE_RECORDS && !std::isfinite(e->cfg.window) &&
                             e->cfg.scope != STGN_SCOPE_DELTA;
   auto launch_records = [&](cudaStream_t rst, bool chain) {
-    if (g.L <= 32) {
+    if (STGN_REC32 && g.L <= 32) {
+      const int gw = 8 * e->num_sms;
+      if (chain)
+        chain_launch(k_records_w32, gw, T, 0, rst, g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
+      else
+        k_records_w32<<<gw, T, 0, rst>>>(g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
+    } else if (g.L <= 32) {
       if (chain)
         chain_launch(k_records_warp, 8 * e->num_sms, T, 0, rst, g, v, s, std::isfinite(e->cfg.window) ? 1 : 0);
       else
@@ -559,11 +571,16 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   if (e->cfg.scope == STGN_SCOPE_DELTA && g.K == 1 && v.attn_logz)
     cudaMemsetAsync(&v.ctl->reserved[0], 0, sizeof(int64_t), st);  // this batch's bound records
   // ingest: direct set, per-node record order, ring insert with payload freeze, store append
-  chain_launch(k_begin, 1, 32, 0, st, s, e->cfg.window);
-  chain_launch(k_claim, g_rec, T, 0, st, g, v, s);
-  chain_launch(k_scan, 1, 1024, 0, st, g, v, s);
-  chain_launch(k_place, g_rec, T, 0, st, v, s);
-  chain_launch(k_rank, g_rec, T, 0, st, v, s);
+  if (STGN_INGEST1 && e->cfg.max_batch <= INGEST1_MAX_B) {
+    chain_launch(k_ingest1, 1, 1024, 0, st, g, v, s, e->cfg.window);
+    n -= 4;
+  } else {
+    chain_launch(k_begin, 1, 32, 0, st, s, e->cfg.window);
+    chain_launch(k_claim, g_rec, T, 0, st, g, v, s);
+    chain_launch(k_scan, 1, 1024, 0, st, g, v, s);
+    chain_launch(k_place, g_rec, T, 0, st, v, s);
+    chain_launch(k_rank, g_rec, T, 0, st, v, s);
+  }
   // Branch 0 (graph mode): the memory update needs only the grouped records
   // (rec_s, doff) and pre-batch memory and writes scratch only, so it runs
   // beside the ring insertion, the BFS and the change records.
@@ -583,8 +600,12 @@ static void enqueue_batch(stgn_engine* e, cudaStream_t st, cudaGraphConditionalH
   mark();
   for (int hop = 1; hop <= g.K; ++hop) {
     chain_launch(k_hop, g_wide, T, 0, st, g, v, s, hop);
-    chain_launch(k_hop_fin, 1, 32, 0, st, s, hop);
-    n += 2;
+    if (STGN_HOP_TICKET) {
+      n += 1;
+    } else {
+      chain_launch(k_hop_fin, 1, 32, 0, st, s, hop);
+      n += 2;
+    }
   }
   mark();
   if (!late_records) launch_records(st, true);

@@ -70,7 +70,7 @@ struct BatchRes {
   double global_drift;
   int32_t rb_partial_n, rb_full_n;   // rebuild work sizes (0 unless that kind fired)
   int32_t nAD;                       // rows of the fused recompute (A pre + D post)
-  int32_t pad3;
+  uint32_t hop_ticket;               // last-block-done counter of k_hop (STGN_HOP_TICKET)
   uint32_t ticket;                   // last-block-done counter of k_drift_decide
   int32_t nC;                        // delta mode: rows of the pre-batch recompute (clist)
   int32_t n_skip, n_hit, n_miss;     // delta mode classification
