@@ -116,6 +116,9 @@ __device__ __forceinline__ unsigned long long a4_now() {
                   // past E the row's last entry; their weights are 0 and their q~ lanes 0), so
                   // the issue has no per-copy size predicates; slot = hd + e with one wrap
 #endif
+#ifndef A4_EVQW
+#define A4_EVQW 0  // event loop: a warp with no pending duty waits for the next quadrant in try_wait
+#endif
 #ifndef A4_RUNPTR
 #define A4_RUNPTR 1  // walk 1: running source pointers for the cp.async issue
 #endif
@@ -1585,7 +1588,20 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
           const int b = q & 1;
           float* Ub = b ? Ub1 : Ub0;
           const int nrows = min(32, T - 32 * q);
+#if A4_EVQW
+          // with no duty of its own left the warp blocks in try_wait (hardware
+          // suspend) instead of spinning on test_wait and taking issue slots
+          // from the walking warps
+          while (!mbar_test(&qbar_full[b], uphase(q))) {
+            if (fill_done && pack_done) {
+              mbar_wait(&qbar_full[b], uphase(q));
+              break;
+            }
+            duties();
+          }
+#else
           while (!mbar_test(&qbar_full[b], uphase(q))) duties();
+#endif
           for (;;) {
             int i = 0;
 #if A4_HW
