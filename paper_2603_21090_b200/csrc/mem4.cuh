@@ -36,6 +36,10 @@
 
 #include "attn4.cuh"
 
+#ifndef M4_L2PF
+#define M4_L2PF 0  // L2 prefetch of the weight blocks after the first two at kernel start
+#endif
+
 #ifndef M4_THREADS
 #define M4_THREADS 1024  // 4 TMEM lane quadrants x M4_NCG column groups
 #endif
@@ -155,6 +159,15 @@ mem4_kernel(Geo g, StateView st, Scratch s, M4W w, const float* __restrict__ bms
     stage(0);
     if (total_blocks > 1) stage(1);
   }
+#if M4_L2PF
+  // the later weight blocks -> L2 now, spread over the live CTAs: their TMA stages then
+  // read L2 instead of HBM (the recompute streams GBs through L2 between two batches)
+  if (tid == 32) {
+    const int live = (int)std::min<int64_t>(ntiles, (int64_t)gridDim.x);
+    for (int j = 2 + (int)blockIdx.x; j < w.nblk; j += live)
+      bulk_prefetch_l2(w.wblk + w.off[j], (uint32_t)(2 * w.np[j] * w.kp[j] * 2));
+  }
+#endif
   int64_t G = 0;
   auto issue = [&](int a_hi, int a_lo, int dcol, bool acc, int off = 0,
                    bool commit = true) {  // tid 0: block G + off
