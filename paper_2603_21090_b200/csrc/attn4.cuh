@@ -116,6 +116,9 @@ __device__ __forceinline__ unsigned long long a4_now() {
                   // past E the row's last entry; their weights are 0 and their q~ lanes 0), so
                   // the issue has no per-copy size predicates; slot = hd + e with one wrap
 #endif
+#ifndef A4_VV
+#define A4_VV 0  // V_0 and V_1 GEMMs issued back to back under one commit
+#endif
 #ifndef A4_EVQW
 #define A4_EVQW 0  // event loop: a warp with no pending duty waits for the next quadrant in try_wait
 #endif
@@ -1798,12 +1801,33 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
       }
 #else
       // ---- c_h = ubar_h W_V,h ----
+#if A4_VV
+      // V_0 and V_1 back to back under one commit (one MMA round trip): the MMAs of one
+      // thread run in issue order, so V_1's C1 columns over QT0 are written after V_0
+      // has read them
+      if (tid == 0) {
+        mbar_wait(&wbar[G & 1], (uint32_t)((G >> 1) & 1));
+        a4_mma(tmem, w.qt0, (G & 1) ? Wb1 : Wb0, w.Nv, w.Ku, 0, &mbar, false, false);
+        mbar_wait(&wbar[(G + 1) & 1], (uint32_t)(((G + 1) >> 1) & 1));
+        a4_mma(tmem, w.qt1, ((G + 1) & 1) ? Wb1 : Wb0, w.Nv, w.Ku, w.c1, &mbar, false, true);
+      }
+      mbar_wait(&mbar, mph & 1u);
+      ++mph;
+      tc_fence_after();
+      if (tid == 0) {
+        if (G + 2 < total_blocks && !deferred(G + 2)) stage(G + 2);
+        if (G + 3 < total_blocks && !deferred(G + 3)) stage(G + 3);
+      }
+      G += 2;
+      A4_MARK(7);
+#else
       gemm(w.qt0, w.Nv, w.Ku, 0);
       A4_MARK(7);
       // every thread must observe the V_0 commit phase before V_1 can complete the
       // next one (a parity wait cannot tell phase G from phase G + 2)
       cta_sync_tc();
       gemm(w.qt1, w.Nv, w.Ku, w.c1);
+#endif
       if (quad_live) {  // c -> CA (bf16 hi|lo), head h at element h*Kq
         const int nch = w.Kq / 16;
         for (int c = cg; c < 2 * nch; c += A4_NCG) {
