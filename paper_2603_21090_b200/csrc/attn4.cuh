@@ -116,6 +116,12 @@ __device__ __forceinline__ unsigned long long a4_now() {
                   // past E the row's last entry; their weights are 0 and their q~ lanes 0), so
                   // the issue has no per-copy size predicates; slot = hd + e with one wrap
 #endif
+#ifndef A4_GA
+#define A4_GA 0  // event-loop walk: dynamic grab-ahead issue stream across the rows of a quadrant
+#endif
+#if A4_GA && (!A4_EVQ || A4_HW || A4_STATIC || A4_WALK != 1 || A4_CPK || A4_TRIG)
+#error "A4_GA is an issue stream of the event-loop walk (walk 1)"
+#endif
 #ifndef A4_VV
 #define A4_VV 0  // V_0 and V_1 GEMMs issued back to back under one commit
 #endif
@@ -478,6 +484,74 @@ __device__ __forceinline__ void a4_issue_next(const Geo& g, const A4W& w, const 
   }
   cp_async_commit();
   ++is.kiss;
+}
+
+// Dynamic grab-ahead issue stream (A4_GA) over the rows of one quadrant: when the
+// row being issued runs out of chunks, the warp takes the next row from the
+// quadrant's counter and issues its first chunks while it still reduces the
+// current row, so the cp.async pipeline does not drain and refill at every row.
+// Rows taken are queued (q_rows, per warp, in shared memory, at most the
+// quadrant's 32) and walked in order.
+struct A4Dyn {
+  int r;      // row (tile index) being issued, -1 if none
+  int c;      // its next chunk
+  int nch;    // its chunk count
+  int kiss;   // groups committed
+  int qh, qt; // queue head (next row to walk) / tail (rows taken)
+  int done;   // the quadrant's counter is exhausted
+};
+template <int KF>
+__device__ __forceinline__ void a4_issue_dyn(const Geo& g, const A4W& w, const RingSrc& rs,
+                                             A4Dyn& d, const int* s_node, const int* s_E,
+                                             const int* s_head, int q, int nrows, int* qctr,
+                                             int* q_rows, int l, int lane, float4* stg) {
+  constexpr int EC = A4_EC, NSEG = KF ? 3 : 2, NST = A4_NST;
+  while (d.r < 0 || d.c >= d.nch) {
+    if (d.done) {
+      d.r = -1;
+      break;
+    }
+    int i = 0;
+    if (lane == 0) i = atomicAdd(qctr, 1);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= nrows) {
+      d.done = 1;
+      d.r = -1;
+      break;
+    }
+    const int r = 32 * q + i;
+    if (s_node[r] < 0) continue;  // no row (another rank's node): nothing to write
+    d.r = r;
+    d.c = 0;
+    d.nch = (max(s_E[r], 0) + EC - 1) / EC;  // an empty list is walked too (ubar = 0)
+    if (lane == 0) q_rows[d.qt & 31] = r;
+    ++d.qt;
+  }
+  if (d.r >= 0) {
+    const int node = s_node[d.r], E = s_E[d.r], hd = s_head[d.r];
+    const bool lp = lane < w.kfo / 4, lf = KF && lane < (w.kto - w.kfo) / 4,
+               lt = lane < (w.kpad - w.kto) / 4;
+    const float* payb = rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d + 4 * lane;
+    const float* ftb = rs.ring_feat + (int64_t)node * g.L * g.ld_e + 4 * lane;
+    const float* tbb = rs.ring_tb + (int64_t)node * g.L * g.ld_t + 4 * lane;
+    const uint64_t pol_pay = pol_evict_first();
+    const uint64_t pol_tb = l + 1 < g.K ? pol_evict_last() : pol_evict_first();
+    float4* sb = stg + (d.kiss % NST) * (EC * NSEG * 32) + lane;
+#pragma unroll
+    for (int u = 0; u < EC; ++u) {
+      const int e = d.c * EC + u;
+      const bool ev = e < E;
+      int slot = hd + e;
+      if (slot >= g.L) slot -= g.L;
+      if (EC > 2 && !ev) slot = 0;
+      cp_async16_pol(sb + (u * NSEG) * 32, payb + slot * g.ld_d, (ev && lp) ? 16 : 0, pol_pay);
+      cp_async16_pol(sb + (u * NSEG + 1) * 32, tbb + slot * g.ld_t, (ev && lt) ? 16 : 0, pol_tb);
+      if (KF) cp_async16(sb + (u * NSEG + 2) * 32, ftb + slot * g.ld_e, (ev && lf) ? 16 : 0);
+    }
+    ++d.c;
+  }
+  cp_async_commit();
+  ++d.kiss;
 }
 
 // Walk of one row (warp-per-row): softmax over its ring entries for both
@@ -1261,6 +1335,9 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
 #endif
   __shared__ int qctr[2];
   __shared__ uint32_t tslot;
+#if A4_GA
+  __shared__ int s_wq[32 * A4_WARPS];  // per warp: rows taken by the issue stream, in order
+#endif
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int quad = warp & 3, cg = warp >> 2;
@@ -1605,6 +1682,18 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
 #else
           while (!mbar_test(&qbar_full[b], uphase(q))) duties();
 #endif
+#if A4_GA
+          // this quadrant's issue stream: the first NST - 1 chunks (rows taken as needed)
+          A4Dyn dy{-1, 0, 0, 0, 0, 0, 0};
+          int kcons_dyn = 0;
+          int* q_rows = s_wq + 32 * warp;
+          auto issue_dyn = [&]() {
+            a4_issue_dyn<KF>(g, w, rs, dy, s_node, s_E, s_head, q, nrows, &qctr[b], q_rows, l,
+                             lane, stg_warp);
+          };
+#pragma unroll
+          for (int p0 = 0; p0 < A4_NST - 1; ++p0) issue_dyn();
+#endif
           for (;;) {
             int i = 0;
 #if A4_HW
@@ -1620,6 +1709,17 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
                                stg_warp);
             }
 #else
+#if A4_GA
+            if (dy.qh == dy.qt) break;  // every row taken has been walked
+            __syncwarp();
+            i = q_rows[dy.qh & 31] - 32 * q;
+            ++dy.qh;
+            {
+              const int r = 32 * q + i;
+              a4_walk_row<KF>(g, w, rs, Ub + i * w.ldu, s_node[r], s_E[r], s_head[r], s_tref[r],
+                              l, lane, stg_warp, issue_dyn, &kcons_dyn);
+            }
+#else
             if (lane == 0) i = atomicAdd(&qctr[b], 1);
             i = __shfl_sync(0xffffffffu, i, 0);
             if (i >= nrows) break;
@@ -1627,6 +1727,7 @@ attn4_kernel(Geo g, A4W w, RingSrc rs) {
             if (s_node[r] >= 0)
               a4_walk_row<KF>(g, w, rs, Ub + i * w.ldu, s_node[r], s_E[r], s_head[r], s_tref[r],
                               l, lane, stg_warp, [] {}, nullptr);
+#endif
 #endif
             duties();
           }
