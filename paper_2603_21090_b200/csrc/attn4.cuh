@@ -122,6 +122,12 @@ __device__ __forceinline__ unsigned long long a4_now() {
 #if A4_GA && (!A4_EVQ || A4_HW || A4_STATIC || A4_WALK != 1 || A4_CPK || A4_TRIG)
 #error "A4_GA is an issue stream of the event-loop walk (walk 1)"
 #endif
+#ifndef A4_SWP
+#define A4_SWP 0  // walk 1: software-pipelined chunk loop (logits of c + 1 beside the update of c)
+#endif
+#if A4_SWP && (A4_NST < 3 || A4_CPK || A4_TRIG || A4_GA || A4_STATIC || A4_HW || A4_WALK != 1)
+#error "A4_SWP is a chunk loop of walk 1 with its own issue stream (a4_walk_row, NST >= 3)"
+#endif
 #ifndef A4_VV
 #define A4_VV 0  // V_0 and V_1 GEMMs issued back to back under one commit
 #endif
@@ -732,6 +738,135 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
 #pragma unroll
     for (int c = 0; c < NST - 1; ++c) issue(c);
   }
+#if A4_SWP
+  // Software-pipelined chunk loop: the logits of chunk c + 1 (dot products and the
+  // transposing butterfly) are formed while chunk c's softmax update and accumulation
+  // run, two independent dependency chains; chunk c + 2 is in flight meanwhile.
+  auto load_k = [&](int slot, float4 (&kp)[EC], float4 (&kt)[EC], float4 (&kf)[EC]) {
+    const float4* sb = stg + slot * (EC * NSEG * 32) + lane;
+#pragma unroll
+    for (int u = 0; u < EC; ++u) {
+      kp[u] = sb[(u * NSEG) * 32];
+      kt[u] = sb[(u * NSEG + 1) * 32];
+      kf[u] = KF ? sb[(u * NSEG + 2) * 32] : zero4;
+    }
+  };
+  auto logits = [&](const float4 (&kp)[EC], const float4 (&kt)[EC], const float4 (&kf)[EC],
+                    int e0, float (&lg)[2 * EC]) {
+    // per-lane partial logits, value index v = 2u + h
+    float part[2 * EC];
+#pragma unroll
+    for (int u = 0; u < EC; ++u) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float2 a = fmul2(make_float2(qp[h].x, qp[h].y), make_float2(kp[u].x, kp[u].y));
+        a = ffma2(make_float2(qp[h].z, qp[h].w), make_float2(kp[u].z, kp[u].w), a);
+        a = ffma2(make_float2(qt[h].x, qt[h].y), make_float2(kt[u].x, kt[u].y), a);
+        a = ffma2(make_float2(qt[h].z, qt[h].w), make_float2(kt[u].z, kt[u].w), a);
+        if (KF) {
+          a = ffma2(make_float2(qf[h].x, qf[h].y), make_float2(kf[u].x, kf[u].y), a);
+          a = ffma2(make_float2(qf[h].z, qf[h].w), make_float2(kf[u].z, kf[u].w), a);
+        }
+        part[2 * u + h] = a.x + a.y;
+      }
+    }
+    // transposing butterfly: 2*EC values; value v ends on lanes v*(32/(2*EC)) ..
+    {
+      const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+#pragma unroll
+      for (int j = 0; j < EC; ++j) {
+        const float send = b4 ? part[j] : part[j + EC];
+        const float keep = b4 ? part[j + EC] : part[j];
+        part[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+      if constexpr (EC >= 2) {
+#pragma unroll
+        for (int j = 0; j < EC / 2; ++j) {
+          const float send = b3 ? part[j] : part[j + EC / 2];
+          const float keep = b3 ? part[j + EC / 2] : part[j];
+          part[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+      }
+      if constexpr (EC >= 4) {
+        const float send = b2 ? part[0] : part[1];
+        const float keep = b2 ? part[1] : part[0];
+        part[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      } else {
+        part[0] += __shfl_xor_sync(0xffffffffu, part[0], 4);
+      }
+      part[0] += __shfl_xor_sync(0xffffffffu, part[0], 2);
+      part[0] += __shfl_xor_sync(0xffffffffu, part[0], 1);
+      constexpr int stride = 32 / (2 * EC);
+#pragma unroll
+      for (int v = 0; v < 2 * EC; ++v) lg[v] = __shfl_sync(0xffffffffu, part[0], stride * v);
+    }
+    // entries past E (zero-filled stages) get logit -inf: out of the max, weight 0
+#pragma unroll
+    for (int u = 1; u < EC; ++u)
+      if (e0 + u >= E) lg[2 * u] = lg[2 * u + 1] = -INFINITY;
+  };
+  auto soft_acc = [&](const float4 (&kp)[EC], const float4 (&kt)[EC], const float4 (&kf)[EC],
+                      const float (&lg)[2 * EC]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float cm = lg[h];
+#pragma unroll
+      for (int u = 1; u < EC; ++u) cm = fmaxf(cm, lg[2 * u + h]);
+      const float nm = fmaxf(mx[h], cm);
+      const float sc = ex2f(mx[h] - nm);  // logits are in log2 units (W_K carries log2 e)
+      const float2 sc2 = make_float2(sc, sc);
+      zs[h] *= sc;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        up[h][c] = fmul2(up[h][c], sc2);
+        ut[h][c] = fmul2(ut[h][c], sc2);
+        if (KF) uf[h][c] = fmul2(uf[h][c], sc2);
+      }
+#pragma unroll
+      for (int u = 0; u < EC; ++u) {
+        const float p = ex2f(lg[2 * u + h] - nm);
+        const float2 p2 = make_float2(p, p);
+        zs[h] += p;
+        up[h][0] = ffma2(p2, make_float2(kp[u].x, kp[u].y), up[h][0]);
+        up[h][1] = ffma2(p2, make_float2(kp[u].z, kp[u].w), up[h][1]);
+        ut[h][0] = ffma2(p2, make_float2(kt[u].x, kt[u].y), ut[h][0]);
+        ut[h][1] = ffma2(p2, make_float2(kt[u].z, kt[u].w), ut[h][1]);
+        if (KF) {
+          uf[h][0] = ffma2(p2, make_float2(kf[u].x, kf[u].y), uf[h][0]);
+          uf[h][1] = ffma2(p2, make_float2(kf[u].z, kf[u].w), uf[h][1]);
+        }
+      }
+      mx[h] = nm;
+    }
+  };
+  float lg_c[2 * EC];
+  if (nch > 0) {
+    cp_async_wait<NST - 2>();  // chunk 0 has landed
+    float4 kp0[EC], kt0[EC], kf0[EC];
+    load_k(0, kp0, kt0, kf0);
+    logits(kp0, kt0, kf0, 0, lg_c);
+  }
+  int slot_s = 0;
+  for (int c = 0; c < nch; ++c) {
+    issue(c + NST - 1);  // into the slot chunk c - 1 used
+    cp_async_wait<NST - 2>();  // chunk c + 1 has landed
+    const int slot_n = slot_s + 1 == NST ? 0 : slot_s + 1;
+    float lg_n[2 * EC];
+    if (c + 1 < nch) {
+      float4 kpn[EC], ktn[EC], kfn[EC];
+      load_k(slot_n, kpn, ktn, kfn);
+      logits(kpn, ktn, kfn, (c + 1) * EC, lg_n);
+    }
+    {
+      float4 kpc[EC], ktc[EC], kfc[EC];
+      load_k(slot_s, kpc, ktc, kfc);
+      soft_acc(kpc, ktc, kfc, lg_c);
+    }
+#pragma unroll
+    for (int v = 0; v < 2 * EC; ++v) lg_c[v] = lg_n[v];
+    slot_s = slot_n;
+  }
+#else
   for (int c = 0; c < nch; ++c) {
     const int e0 = c * EC;
     int slot_c = con_slot;
@@ -867,6 +1002,7 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
       mx[h] = nm;
     }
   }
+#endif
   __syncwarp();
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
