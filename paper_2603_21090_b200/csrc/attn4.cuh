@@ -122,6 +122,12 @@ __device__ __forceinline__ unsigned long long a4_now() {
 #if A4_GA && (!A4_EVQ || A4_HW || A4_STATIC || A4_WALK != 1 || A4_CPK || A4_TRIG)
 #error "A4_GA is an issue stream of the event-loop walk (walk 1)"
 #endif
+#ifndef A4_LEAN
+#define A4_LEAN 0  // walk 1: cp.async issue from 32-bit byte offsets, always 16 valid bytes
+#endif
+#if A4_LEAN && (A4_ISS || A4_CPK || A4_TRIG || !A4_HINTS || A4_HW)
+#error "A4_LEAN is an issue order of a4_walk_row (walk 1)"
+#endif
 #ifndef A4_SWP
 #define A4_SWP 0  // walk 1: software-pipelined chunk loop (logits of c + 1 beside the update of c)
 #endif
@@ -642,6 +648,21 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   const float* r_tb = tbb + (int64_t)hd * g.ld_t;
   const float* r_ft = ftb + (int64_t)hd * g.ld_e;
 #endif
+#if A4_LEAN
+  // byte offsets of the next entry to issue from the node's slot-0 rows (lanes past a
+  // segment read lane 0's 16 bytes: every copy is 16 valid bytes, no size predicate);
+  // after the last entry the offsets stop, so a chunk's tail re-reads that entry
+  // (its logit is -inf, its weight 0)
+  const char* l_pay = reinterpret_cast<const char*>(rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d) +
+                      (lp ? 16 * lane : 0);
+  const char* l_tb = reinterpret_cast<const char*>(rs.ring_tb + (int64_t)node * g.L * g.ld_t) +
+                     (lt ? 16 * lane : 0);
+  const char* l_ft = reinterpret_cast<const char*>(rs.ring_feat + (int64_t)node * g.L * g.ld_e) +
+                     (lf ? 16 * lane : 0);
+  const uint32_t sp_pay = 4u * g.ld_d, sp_tb = 4u * g.ld_t, sp_ft = 4u * g.ld_e;
+  uint32_t o_pay = (uint32_t)hd * sp_pay, o_tb = (uint32_t)hd * sp_tb, o_ft = (uint32_t)hd * sp_ft;
+  int l_slot = hd, l_left = E;
+#endif
 #if A4_ISS
   const float* i_pay = rs.ring_pay + ((int64_t)node * g.K + l) * g.L * g.ld_d + (lp ? 4 * lane : 0);
   const float* i_tb = rs.ring_tb + (int64_t)node * g.L * g.ld_t + (lt ? 4 * lane : 0);
@@ -667,6 +688,25 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
       for (int u = 0; u < EC; ++u) {
         const int e = c * EC + u;
         const bool ev = e < E;
+#if A4_LEAN
+        {
+          cp_async16_pol(sb + (u * NSEG) * 32, l_pay + o_pay, 16, pol_pay);
+          cp_async16_pol(sb + (u * NSEG + 1) * 32, l_tb + o_tb, 16, pol_tb);
+          if (KF) cp_async16(sb + (u * NSEG + 2) * 32, l_ft + o_ft, 16);
+          if (--l_left > 0) {
+            if (++l_slot == g.L) {
+              l_slot = 0;
+              o_pay = o_tb = o_ft = 0;
+            } else {
+              o_pay += sp_pay;
+              o_tb += sp_tb;
+              if (KF) o_ft += sp_ft;
+            }
+          }
+          (void)ev;
+          continue;
+        }
+#endif
 #if A4_ISS
         {
           int slot = hd + (ev ? e : E - 1);
