@@ -122,6 +122,9 @@ __device__ __forceinline__ unsigned long long a4_now() {
 #if A4_GA && (!A4_EVQ || A4_HW || A4_STATIC || A4_WALK != 1 || A4_CPK || A4_TRIG)
 #error "A4_GA is an issue stream of the event-loop walk (walk 1)"
 #endif
+#ifndef A4_HEADROT
+#define A4_HEADROT 0  // walk 1: the row's rotation by w t_ref read from the newest slot's stored basis
+#endif
 #ifndef A4_LEAN
 #define A4_LEAN 0  // walk 1: cp.async issue from 32-bit byte offsets, always 16 valid bytes
 #endif
@@ -601,8 +604,19 @@ __device__ __forceinline__ void a4_walk_row(const Geo& g, const A4W& w, const Ri
   const double om1 = f1 ? __ldg(w.omega + 2 * lane + 1) : 0.0;
 #else
   float ca0 = 1.f, sa0 = 0.f, ca1 = 1.f, sa1 = 0.f;
+#if A4_HEADROT
+  // t_ref is the time of the row's newest ring entry (slot hd), whose stored basis is
+  // [cos w t_ref, sin w t_ref] from the same phase_sincos: one 16-byte load instead
+  // of two float64 phase reductions per lane, bit-identical
+  if (E > 0 && lt && 2 * lane < g.half) {
+    const float4 b = *reinterpret_cast<const float4*>(rs.ring_tb + ((int64_t)node * g.L + hd) * g.ld_t + 4 * lane);
+    ca0 = b.x; sa0 = b.y;
+    if (2 * lane + 1 < g.half) { ca1 = b.z; sa1 = b.w; }
+  }
+#else
   if (lt && 2 * lane < g.half) phase_sincos(__ldg(w.omega + 2 * lane), tref, &sa0, &ca0);
   if (lt && 2 * lane + 1 < g.half) phase_sincos(__ldg(w.omega + 2 * lane + 1), tref, &sa1, &ca1);
+#endif
 #endif
   float4 qp[2], qf[2], qt[2];
 #pragma unroll
